@@ -1,0 +1,125 @@
+/* specmoe_b200.h -- C ABI of the B200-native self-assisted speculative-decoding engine.
+ *
+ * This is the drop-in boundary below the reference's C++ API (/root/reference/proj/core):
+ * plain pointers, sizes and status codes, no STL, no torch types.  Each entry point names the
+ * reference interface it replaces.  The C++ drop-in headers (include/specmoe/ headers) and the Python
+ * host mirror (paper_2604_10152_b200/engine.py) are both built on these calls.
+ *
+ * Status codes (reference common.hpp:12-21 exit codes + CUDA): 0 ok, 1 ConfigError,
+ * 2 InvariantError, 3 CUDA/NCCL error.  smoe_last_error() returns the thread-local message.
+ */
+#ifndef SPECMOE_B200_H
+#define SPECMOE_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SMOE_OK = 0, SMOE_CONFIG = 1, SMOE_INVARIANT = 2, SMOE_CUDA = 3 };
+enum { SMOE_F32 = 0, SMOE_BF16 = 1 };                      /* weight / operand storage */
+enum { SMOE_EXPERT_TANH2 = 0, SMOE_EXPERT_SWIGLU3 = 1 };   /* model.cpp:54-59 / Mixtral */
+enum { SMOE_GEMM_AUTO = 0, SMOE_GEMM_SIMT = 1, SMOE_GEMM_TCGEN05 = 2 };
+enum { SMOE_POLICY_RANDOM = 0, SMOE_POLICY_HOT_GLOBAL = 1, SMOE_POLICY_HOT_TEMPORAL = 2 }; /* drafting.hpp:40 */
+enum { SMOE_PHASE_SPECULATION = 0, SMOE_PHASE_VERIFICATION = 1, SMOE_PHASE_BASELINE = 2 }; /* memsim.hpp:21 */
+
+typedef struct smoe_engine smoe_engine;
+
+/* ModelSpec (model.hpp:16-32) + device configuration. */
+typedef struct {
+    int num_layers, experts, top_k, hidden, ffn, vocab;
+    double gate_skew;
+    uint64_t seed;
+    const uint8_t* moe_mask; /* num_layers entries or NULL (every layer MoE) */
+    int expert_kind;         /* SMOE_EXPERT_* */
+    int weight_type;         /* SMOE_F32 (parity) / SMOE_BF16 (perf) */
+    int max_batch, max_gamma;
+    int gemm_backend;        /* SMOE_GEMM_* ; AUTO = tcgen05 for bf16, SIMT for f32 */
+    int device;
+    int offload;             /* 0: all experts HBM-resident; 1: pinned host pool + HBM slots (C3) */
+    int hbm_expert_slots;    /* offload: HBM slot count (0 = pinned draft sets + one layer's transients) */
+} smoe_engine_config;
+
+/* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy/seed (greedy). */
+typedef struct {
+    int gamma, n_draft, max_new_tokens, use_affinity, warmup_steps, policy, collect_trace;
+    uint64_t run_seed;
+    uint64_t device_capacity_bytes, bytes_per_expert; /* ledger accounting (reference units) */
+    double host_bandwidth, ssd_bandwidth, compute_rate, compute_cost_per_expert;
+} smoe_run_config;
+
+typedef struct { int phase, step, layer, expert; uint64_t bytes; } smoe_ledger_entry; /* memsim.hpp:44-49 */
+typedef struct { int seq, phase, accepted, correction, tokens_generated; } smoe_outcome; /* specdec.hpp:32-39 */
+
+/* RunResult (specdec.hpp:70-78) with RunMetrics (41-57) flattened, plus measured device time. */
+typedef struct {
+    int B, max_new, moe_layers, experts, top_k, gamma;
+    int* tokens;
+    int* n_tokens;
+    int n_ledger;
+    smoe_ledger_entry* ledger;
+    int n_outcomes;
+    smoe_outcome* outcomes;
+    int* outcome_drafts;
+    int n_trace;
+    int* trace;
+    uint64_t* hotness;
+    double tau_mean;
+    uint64_t tokens_total;
+    int phases;
+    double speculation_s, verification_s, modeled_seconds, tokens_per_sec;
+    uint64_t bytes_spec, bytes_verify, bytes_baseline, bytes_total, setup_bytes, warmup_bytes;
+    double lambda, c_measured;
+    double wall_s;          /* host wall time of the loop */
+    double gpu_s;           /* CUDA-event time of the loop on the engine stream */
+    uint64_t h2d_expert_bytes; /* real bytes migrated by the expert store (offload mode) */
+    double h2d_s;           /* CUDA-event time spent in expert migration copies */
+} smoe_run_result;
+
+const char* smoe_last_error(void);
+
+/* Engine lifetime.  Replaces the implicit state of build_model (model.hpp:61) + ResidencyState. */
+int smoe_engine_create(const smoe_engine_config* cfg, smoe_engine** out);
+void smoe_engine_destroy(smoe_engine* e);
+int smoe_engine_info(smoe_engine* e, uint64_t* device_bytes, uint64_t* bytes_per_expert_real, int* moe_layers);
+void* smoe_engine_stream(smoe_engine* e); /* the cudaStream_t every hot-path kernel is launched on */
+
+/* Weights.  exact: the reference's mt19937_64 polar stream (model.cpp:106-143, common.hpp:46-55),
+ * converted to the engine's storage type, with the affinity table computed in float64 exactly as
+ * drafting.cpp:28-57.  device: counter-based normal RNG on the GPU (perf shapes).
+ * upload: a float64 tensor in the reference layout (model.hpp:34-55). */
+int smoe_init_weights_exact(smoe_engine* e);
+int smoe_init_weights_device(smoe_engine* e, uint64_t seed);
+int smoe_upload_tensor(smoe_engine* e, const char* name, int layer, int expert, const double* src, long long n);
+/* AffinityTable (drafting.hpp:14-21): [moe_layers][E][E] float64. */
+int smoe_set_affinity(smoe_engine* e, const double* dist);
+int smoe_build_affinity_device(smoe_engine* e);
+int smoe_get_affinity(smoe_engine* e, double* out);
+
+/* forward (model.hpp:114-116) for one prefix: logits [V] f32, raw/final picks [moe_layers][K].
+ * restricted: [moe_layers][n_draft] sorted draft sets or NULL. */
+int smoe_forward(smoe_engine* e, const int* prefix, int n, const int* restricted, int n_draft, int use_affinity,
+                 float* logits_out, int* raw_out, int* final_out);
+
+/* run_specmoe (specdec.hpp:122-124) / run_ondemand (baselines.hpp:24-26), greedy. */
+int smoe_run_specmoe(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len,
+                     smoe_run_result** out);
+int smoe_run_ondemand(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len,
+                      smoe_run_result** out);
+void smoe_free_result(smoe_run_result* r);
+
+/* Stepped interface for benchmarking one speculative phase at a time (a "step" = draft pass of
+ * gamma tokens + batched verify + accept/rollback + expert store for all active sequences). */
+int smoe_spec_begin(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len);
+int smoe_spec_step(smoe_engine* e, int* tokens_accepted_out, int* active_out);
+int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
+
+/* Kernel timing hooks for bench.py: events recorded around the dominant kernel class. */
+int smoe_profile_reset(smoe_engine* e);
+int smoe_profile_read(smoe_engine* e, const char* kernel_class, double* total_ms, long long* launches,
+                      double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

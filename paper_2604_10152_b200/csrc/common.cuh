@@ -1,0 +1,72 @@
+// common.cuh -- shared device/host definitions for the B200 spec-decode engine.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace smoe {
+
+// Status codes returned through the C ABI: mirror the reference's exit codes
+// (common.hpp:12-21: ConfigError -> 1, InvariantError -> 2) plus 3 for CUDA/NCCL failures.
+enum Status : int { kOk = 0, kConfig = 1, kInvariant = 2, kCuda = 3 };
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SMOE_CUDA(x)                                                                               \
+    do {                                                                                           \
+        cudaError_t e__ = (x);                                                                     \
+        if (e__ != cudaSuccess)                                                                    \
+            throw ::smoe::Error(::smoe::kCuda, std::string(#x) + ": " + cudaGetErrorString(e__) + \
+                                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+// Weight / operand storage types.
+enum WType : int { kF32 = 0, kBF16 = 1 };
+
+// Expert FFN forms: tanh2 = reference (model.cpp:54-59), swiglu3 = Mixtral.
+enum ExpertKind : int { kTanh2 = 0, kSwiglu3 = 1 };
+
+// GEMM epilogues.
+enum Epi : int {
+    kEpiStoreF32 = 0,   // Y[f32] = acc
+    kEpiResidAdd = 1,   // Y[f32] += acc                    (mix: x += Mix rms(x))
+    kEpiTanh = 2,       // Y[op]  = tanh(acc)               (tanh2 up projection)
+    kEpiSwiglu = 3,     // Y[op]  = silu(acc_w1) * acc_w3   (swiglu3 gated up projection)
+};
+
+// Device-resident error flag bits (checked once per phase, SURVEY 5 failure detection).
+enum Flag : int { kFlagNonFiniteLogits = 1, kFlagEmptyRemap = 2, kFlagNonFiniteGate = 4 };
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // common.hpp:27-32
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ inline uint64_t substream(uint64_t seed, uint64_t t0, uint64_t t1 = 0) {  // common.hpp:35-37
+    return splitmix64(seed ^ splitmix64(t0 ^ splitmix64(t1)));
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace smoe

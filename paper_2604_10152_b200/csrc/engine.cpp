@@ -1,0 +1,541 @@
+// engine.cpp -- device model, weights, draft tables and the batched forward pass.
+//
+// Data layout in HBM: every GEMM weight is stored K-major with the
+// output feature as the row ("out x in"), so a 128-row tile is one TMA box for tcgen05 and one
+// 16-byte-vector row walk for the CUDA-core path:
+//   mix  [L][d][d]           (reference mix is already out x in, model.cpp:29-39)
+//   up   [S][U][d]           (reference up is d x f -> transposed; swiglu3: rows [0,f) w1, [f,2f) w3)
+//   down [S][d][f]           (reference down is f x d -> transposed)
+//   head [V][d]              (reference head is d x V -> transposed)
+//   gate [M][E][d] f32, bias [M][E] f32, embedding [V][d] float64 (prefix sums stay float64)
+// S = one slot per (MoE layer, expert) plus one per dense layer.
+#include "engine.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+
+namespace smoe {
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    SMOE_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+void* dalloc_bytes(size_t n) {
+    void* p = nullptr;
+    SMOE_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1)));
+    return p;
+}
+
+// Reference seeded normal stream: std::mt19937_64 + Marsaglia polar, second variate discarded
+// (common.hpp:40-55).  Kept in the engine so exact-weight init never touches the oracle.
+struct PolarStream {
+    std::mt19937_64 rng;
+    explicit PolarStream(uint64_t s) : rng(s) {}
+    double u01() { return static_cast<double>(rng() >> 11) * 0x1.0p-53; }
+    double next() {
+        for (;;) {
+            double u = 2.0 * u01() - 1.0;
+            double v = 2.0 * u01() - 1.0;
+            double s = u * u + v * v;
+            if (s > 0.0 && s < 1.0) return u * std::sqrt(-2.0 * std::log(s) / s);
+        }
+    }
+    void fill(std::vector<double>& out, size_t n, double sd) {
+        out.resize(n);
+        for (size_t i = 0; i < n; ++i) out[i] = sd * next();
+    }
+};
+
+}  // namespace
+
+Engine::Engine(const smoe_engine_config& c) {
+    L = c.num_layers; E = c.experts; K = c.top_k; d = c.hidden; f = c.ffn; V = c.vocab;
+    skew = c.gate_skew; seed = c.seed; kind = c.expert_kind;
+    wt = c.weight_type == SMOE_F32 ? kF32 : kBF16;
+    Bmax = std::max(1, c.max_batch);
+    Gmax = std::max(1, c.max_gamma);
+    stride = Gmax + 1;
+    Tmax = Bmax * (Gmax + 1);
+    device = c.device;
+    offload = c.offload;
+    if (E < 1 || K < 1 || K > E) throw Error(kConfig, "model: 1 <= top_k <= experts_per_block violated");
+    if (E > 64) throw Error(kConfig, "engine: experts_per_block <= 64 (gate kernel bitmask) violated");
+    if (K > 16) throw Error(kConfig, "engine: top_k <= 16 violated");
+    if (V < 2) throw Error(kConfig, "model: vocab_size >= 2 violated");
+    if (d < 1 || f < 1 || L < 1) throw Error(kConfig, "model: dims >= 1 violated");
+    if (skew < 0.0) throw Error(kConfig, "model: gate_skew >= 0 violated");
+    if (d % 8 || f % 8) throw Error(kConfig, "engine: hidden_dim and ffn_dim must be multiples of 8 (16-byte rows)");
+    if (kind != kTanh2 && kind != kSwiglu3) throw Error(kConfig, "engine: unknown expert kind");
+    mask.assign(L, 1);
+    if (c.moe_mask)
+        for (int l = 0; l < L; ++l) mask[l] = c.moe_mask[l] ? 1 : 0;
+    moe_ord.assign(L, -1);
+    for (int l = 0; l < L; ++l)
+        if (mask[l]) { moe_ord[l] = (int)moe_index.size(); moe_index.push_back(l); }
+    M = (int)moe_index.size();
+    if (M == 0) throw Error(kConfig, "model: at least one layer must be an MoE block");
+    n_dense = L - M;
+    U = kind == kSwiglu3 ? 2 * f : f;
+    if (c.gemm_backend == SMOE_GEMM_SIMT) use_tc = 0;
+    else if (c.gemm_backend == SMOE_GEMM_TCGEN05) use_tc = 1;
+    else use_tc = wt == kBF16 ? 1 : 0;
+    if (use_tc && wt != kBF16) throw Error(kConfig, "engine: the tcgen05 path needs bf16 weights");
+
+    SMOE_CUDA(cudaSetDevice(device));
+    SMOE_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    SMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+
+    const size_t ws = wt == kF32 ? 4 : 2;
+    n_slots = M * E + n_dense;
+    emb64 = dalloc<double>((size_t)V * d);
+    mix = dalloc_bytes((size_t)L * d * d * ws);
+    gate_w = dalloc<float>((size_t)M * E * d);
+    gate_b = dalloc<float>((size_t)M * E);
+    up_pool = dalloc_bytes((size_t)n_slots * U * d * ws);
+    down_pool = dalloc_bytes((size_t)n_slots * d * f * ws);
+    head = dalloc_bytes((size_t)V * d * ws);
+    h_slot_of.resize((size_t)M * E);
+    for (int i = 0; i < M * E; ++i) h_slot_of[i] = i;
+    dense_slot.assign(L, -1);
+    for (int l = 0, k = 0; l < L; ++l)
+        if (!mask[l]) dense_slot[l] = M * E + k++;
+    slot_of = dalloc<int>((size_t)M * E);
+    SMOE_CUDA(cudaMemcpy(slot_of, h_slot_of.data(), sizeof(int) * M * E, cudaMemcpyHostToDevice));
+    std::vector<float> bias((size_t)M * E);
+    for (int m = 0; m < M; ++m)
+        for (int e = 0; e < E; ++e) bias[(size_t)m * E + e] = (float)(skew * (1.0 - (double)e / E));  // model.cpp:128-130
+    SMOE_CUDA(cudaMemcpy(gate_b, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice));
+
+    seq_sum = dalloc<double>((size_t)Bmax * d);
+    seq_len = dalloc<int>(Bmax);
+    drafts = dalloc<int>((size_t)Bmax * stride);
+    vam = dalloc<int>((size_t)Bmax * stride);
+    SMOE_CUDA(cudaMemset(drafts, 0, sizeof(int) * Bmax * stride));
+    SMOE_CUDA(cudaMemset(vam, 0, sizeof(int) * Bmax * stride));
+    row_seq = dalloc<int>(2 * (size_t)Tmax);
+    row_extra = dalloc<int>(2 * (size_t)Tmax);
+    row_plen = dalloc<int>(Tmax);
+    x = dalloc<float>((size_t)Tmax * d);
+    xa = dalloc_bytes((size_t)Tmax * d * ws);
+    raw_log = dalloc<int>((size_t)(Gmax + 1) * M * Tmax * K);
+    fin_log = dalloc<int>((size_t)(Gmax + 1) * M * Tmax * K);
+    wgt = dalloc<float>((size_t)Tmax * K);
+    pos = dalloc<int>((size_t)Tmax * K);
+    group_off = dalloc<int>(E + 1);
+    group_slot = dalloc<int>(E);
+    xperm = dalloc_bytes((size_t)Tmax * K * d * ws);
+    hbuf = dalloc_bytes((size_t)Tmax * K * f * ws);
+    ybuf = dalloc<float>((size_t)Tmax * K * d);
+    logits = dalloc<float>((size_t)Tmax * V);
+    amax = dalloc<int>(Tmax);
+    in_draft = dalloc<uint8_t>((size_t)M * E);
+    draft_sorted = dalloc<int>((size_t)M * E);
+    rank = dalloc<int>((size_t)M * E * E);
+    acc = dalloc<int>(Bmax);
+    corr = dalloc<int>(Bmax);
+    commit_toks = dalloc<int>((size_t)Bmax * stride);
+    commit_take = dalloc<int>(Bmax);
+    seqs = dalloc<int>(Bmax);
+    flags = dalloc<int>(1);
+    SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
+    h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
+    SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
+
+    op_mix = {mix, (long long)L * d, d};
+    op_up = {up_pool, (long long)n_slots * U, d};
+    op_down = {down_pool, (long long)n_slots * d, f};
+    op_head = {head, (long long)V, d};
+    op_xa = {xa, (long long)Tmax, d};
+    op_xperm = {xperm, (long long)Tmax * K, d};
+    op_h = {hbuf, (long long)Tmax * K, f};
+}
+
+Engine::~Engine() {
+    auto fr = [](void* p) { if (p) cudaFree(p); };
+    if (stream) cudaStreamSynchronize(stream);
+    fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
+    fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
+    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf);
+    fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
+    fr(commit_take); fr(seqs); fr(flags); fr(scratch64);
+    if (h_small) cudaFreeHost(h_small);
+    if (host_up) cudaFreeHost(host_up);
+    if (host_down) cudaFreeHost(host_down);
+    for (auto& kv : prof)
+        for (auto& p : kv.second.ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+uint64_t Engine::real_bytes_per_expert() const {
+    return (uint64_t)(kind == kSwiglu3 ? 3 : 2) * d * f * (wt == kF32 ? 4 : 2);
+}
+
+void Engine::sync() { SMOE_CUDA(cudaStreamSynchronize(stream)); }
+
+void Engine::check_flags() {
+    int h = 0;
+    SMOE_CUDA(cudaMemcpy(&h, flags, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) {
+        SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
+        if (h & kFlagNonFiniteLogits) throw Error(kInvariant, "greedy_next: non-finite logits");
+        if (h & kFlagNonFiniteGate) throw Error(kInvariant, "softmax: non-finite input");
+        if (h & kFlagEmptyRemap) throw Error(kInvariant, "nearest_draft_expert: empty candidate set");
+    }
+}
+
+void Engine::upload_ints(int* dst, const int* src, size_t n) {
+    // synchronous-safe: stage through pinned memory then wait, so callers may reuse src at once
+    if (n == 0) return;
+    SMOE_CUDA(cudaStreamSynchronize(stream));
+    if (n > h_small_n) {
+        SMOE_CUDA(cudaFreeHost(h_small));
+        h_small_n = n * 2;
+        SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
+    }
+    std::memcpy(h_small, src, n * sizeof(int));
+    SMOE_CUDA(cudaMemcpyAsync(dst, h_small, n * sizeof(int), cudaMemcpyHostToDevice, stream));
+    SMOE_CUDA(cudaStreamSynchronize(stream));
+}
+
+// ------------------------------------------------------------------ weights
+void Engine::upload_tensor(const std::string& name, int layer, int expert, const double* src, long long n) {
+    auto need = [&](long long want) {
+        if (n != want) throw Error(kConfig, "upload_tensor: " + name + " size mismatch");
+    };
+    auto stage = [&](long long cnt) -> double* {
+        if ((size_t)cnt > scratch64_n) {
+            if (scratch64) SMOE_CUDA(cudaFree(scratch64));
+            scratch64_n = (size_t)cnt;
+            scratch64 = dalloc<double>(scratch64_n);
+        }
+        SMOE_CUDA(cudaMemcpy(scratch64, src, sizeof(double) * cnt, cudaMemcpyHostToDevice));
+        return scratch64;
+    };
+    const size_t ws = wt == kF32 ? 4 : 2;
+    auto at = [&](void* base, size_t elems) { return static_cast<char*>(base) + elems * ws; };
+    auto slot_for = [&]() -> int {
+        if (layer < 0 || layer >= L) throw Error(kConfig, "upload_tensor: layer out of range");
+        if (mask[layer]) {
+            if (expert < 0 || expert >= E) throw Error(kConfig, "upload_tensor: expert out of range");
+            return h_slot_of[(size_t)moe_ord[layer] * E + expert];
+        }
+        return dense_slot[layer];
+    };
+    if (name == "embedding") {
+        need((long long)V * d);
+        SMOE_CUDA(cudaMemcpy(emb64, src, sizeof(double) * n, cudaMemcpyHostToDevice));
+    } else if (name == "head") {
+        need((long long)d * V);
+        launch_convert_transpose(stage(n), d, V, head, wt, stream);
+    } else if (name == "mix") {
+        need((long long)d * d);
+        launch_convert(stage(n), n, at(mix, (size_t)layer * d * d), wt, stream);
+    } else if (name == "gate") {
+        need((long long)d * E);
+        if (layer < 0 || layer >= L || !mask[layer]) throw Error(kConfig, "upload_tensor: gate on a dense layer");
+        launch_convert_transpose(stage(n), d, E, gate_w + (size_t)moe_ord[layer] * E * d, kF32, stream);
+    } else if (name == "gate_bias") {
+        need(E);
+        launch_convert(stage(n), n, gate_b + (size_t)moe_ord[layer] * E, kF32, stream);
+    } else if (name == "up" || name == "w1") {
+        need((long long)d * f);
+        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream);
+    } else if (name == "w3") {
+        need((long long)d * f);
+        if (kind != kSwiglu3) throw Error(kConfig, "upload_tensor: w3 needs the swiglu3 expert kind");
+        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d + (size_t)f * d), wt, stream);
+    } else if (name == "down" || name == "w2") {
+        need((long long)f * d);
+        launch_convert_transpose(stage(n), f, d, at(down_pool, (size_t)slot_for() * d * f), wt, stream);
+    } else {
+        throw Error(kConfig, "upload_tensor: unknown tensor " + name);
+    }
+    SMOE_CUDA(cudaGetLastError());
+    sync();
+}
+
+// model.cpp:106-143 draw order; affinity (drafting.cpp:28-57) from the same float64 values.
+void Engine::init_exact() {
+    PolarStream ps(seed);
+    const double sd = 1.0 / std::sqrt((double)d);
+    std::vector<double> buf;
+    ps.fill(buf, (size_t)V * d, sd);
+    upload_tensor("embedding", -1, -1, buf.data(), (long long)buf.size());
+    affinity.assign((size_t)M * E * E, 0.0);
+    const int nmat = kind == kSwiglu3 ? 3 : 2;
+    std::vector<std::vector<double>> ex((size_t)E * nmat);
+    for (int l = 0; l < L; ++l) {
+        ps.fill(buf, (size_t)d * d, sd);
+        upload_tensor("mix", l, -1, buf.data(), (long long)buf.size());
+        if (mask[l]) {
+            ps.fill(buf, (size_t)d * E, sd);
+            upload_tensor("gate", l, -1, buf.data(), (long long)buf.size());
+            for (int e = 0; e < E; ++e) {
+                const char* names3[3] = {"w1", "w3", "w2"};
+                const char* names2[2] = {"up", "down"};
+                for (int q = 0; q < nmat; ++q) {
+                    auto& v = ex[(size_t)e * nmat + q];
+                    ps.fill(v, (size_t)d * f, sd);
+                    upload_tensor(nmat == 3 ? names3[q] : names2[q], l, e, v.data(), (long long)v.size());
+                }
+            }
+            double* D = affinity.data() + (size_t)moe_ord[l] * E * E;
+            for (int i = 0; i < E; ++i)
+                for (int j = i + 1; j < E; ++j) {
+                    double ss = 0.0;
+                    for (int q = 0; q < nmat; ++q) {
+                        const double* a = ex[(size_t)i * nmat + q].data();
+                        const double* b = ex[(size_t)j * nmat + q].data();
+                        const size_t n = (size_t)d * f;
+                        for (size_t k = 0; k < n; ++k) {
+                            double df = a[k] - b[k];
+                            ss += df * df;
+                        }
+                    }
+                    D[(size_t)i * E + j] = D[(size_t)j * E + i] = std::sqrt(ss);
+                }
+        } else {
+            const char* names3[3] = {"w1", "w3", "w2"};
+            const char* names2[2] = {"up", "down"};
+            for (int q = 0; q < nmat; ++q) {
+                ps.fill(buf, (size_t)d * f, sd);
+                upload_tensor(nmat == 3 ? names3[q] : names2[q], l, -1, buf.data(), (long long)buf.size());
+            }
+        }
+    }
+    ps.fill(buf, (size_t)d * V, sd);
+    upload_tensor("head", -1, -1, buf.data(), (long long)buf.size());
+    have_affinity = true;
+}
+
+void Engine::init_device(uint64_t s) {
+    const double sd = 1.0 / std::sqrt((double)d);
+    uint64_t tid = 1;
+    launch_fill_normal_f64(emb64, (long long)V * d, sd, s, tid++, stream);
+    launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
+    launch_fill_normal(gate_w, kF32, (long long)M * E * d, sd, s, tid++, stream);
+    launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid++, stream);
+    launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid++, stream);
+    launch_fill_normal(head, wt, (long long)V * d, sd, s, tid++, stream);
+    SMOE_CUDA(cudaGetLastError());
+    sync();
+    have_affinity = false;
+}
+
+void Engine::build_affinity_device() {
+    constexpr int kChunks = 64;  // matches kernels.cu kPairChunks
+    const size_t need = (size_t)E * E * kChunks;
+    if (need > scratch64_n) {
+        if (scratch64) SMOE_CUDA(cudaFree(scratch64));
+        scratch64_n = need;
+        scratch64 = dalloc<double>(need);
+    }
+    affinity.assign((size_t)M * E * E, 0.0);
+    std::vector<double> part(need);
+    const size_t ws = wt == kF32 ? 4 : 2;
+    for (int m = 0; m < M; ++m) {
+        SMOE_CUDA(cudaMemsetAsync(scratch64, 0, need * sizeof(double), stream));
+        const int* slots = slot_of + (size_t)m * E;
+        launch_pairwise_sqdist(up_pool, wt, (long long)U * d, (long long)U * d, slots, E, scratch64, stream);
+        launch_pairwise_sqdist(down_pool, wt, (long long)d * f, (long long)d * f, slots, E, scratch64, stream);
+        (void)ws;
+        SMOE_CUDA(cudaMemcpyAsync(part.data(), scratch64, need * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        sync();
+        double* D = affinity.data() + (size_t)m * E * E;
+        for (int i = 0; i < E; ++i)
+            for (int j = i + 1; j < E; ++j) {
+                double s = 0.0;
+                for (int c = 0; c < kChunks; ++c) s += part[((size_t)i * E + j) * kChunks + c];
+                D[(size_t)i * E + j] = D[(size_t)j * E + i] = std::sqrt(s);
+            }
+    }
+    have_affinity = true;
+}
+
+// ------------------------------------------------------------------ draft tables
+// For each MoE layer and raw expert r: the draft members ordered by (affinity distance to r, index)
+// -- the order nearest_draft_expert (drafting.cpp:123-138) scans implicitly.  The device walks this
+// list and takes the first member not already chosen, so no float64 compare happens on the GPU.
+void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft) {
+    if ((int)sets.size() != M) throw Error(kInvariant, "forward: restricted set count != MoE layer count");
+    if (n_draft < K) throw Error(kInvariant, "forward: restricted set smaller than top_k");
+    std::vector<uint8_t> ind((size_t)M * E, 0);
+    std::vector<int> sorted((size_t)M * E, 0), rk((size_t)M * E * n_draft, 0);
+    for (int m = 0; m < M; ++m) {
+        std::vector<int> srt(sets[m]);
+        if ((int)srt.size() != n_draft) throw Error(kInvariant, "forward: restricted set size mismatch");
+        std::sort(srt.begin(), srt.end());
+        for (int i = 0; i < n_draft; ++i) {
+            if (srt[i] < 0 || srt[i] >= E) throw Error(kInvariant, "forward: draft expert out of range");
+            ind[(size_t)m * E + srt[i]] = 1;
+            sorted[(size_t)m * E + i] = srt[i];
+        }
+        for (int r = 0; r < E; ++r) {
+            std::vector<int> o(srt);
+            if (have_affinity) {
+                const double* D = affinity.data() + (size_t)m * E * E + (size_t)r * E;
+                std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
+                    if (D[a] != D[b]) return D[a] < D[b];
+                    return a < b;
+                });
+            }
+            std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * n_draft);
+        }
+    }
+    SMOE_CUDA(cudaMemcpy(in_draft, ind.data(), ind.size(), cudaMemcpyHostToDevice));
+    upload_ints(draft_sorted, sorted.data(), sorted.size());
+    upload_ints(rank, rk.data(), rk.size());
+    cur_n_draft = n_draft;
+}
+
+// ------------------------------------------------------------------ profiling
+void Engine::prof_begin(const char* cls, cudaEvent_t* a) {
+    *a = nullptr;
+    if (!profiling) return;
+    SMOE_CUDA(cudaEventCreate(a));
+    SMOE_CUDA(cudaEventRecord(*a, stream));
+    (void)cls;
+}
+void Engine::prof_end(const char* cls, cudaEvent_t a, double bytes) {
+    if (!profiling || !a) return;
+    cudaEvent_t b;
+    SMOE_CUDA(cudaEventCreate(&b));
+    SMOE_CUDA(cudaEventRecord(b, stream));
+    Prof& p = prof[cls];
+    p.ev.emplace_back(a, b);
+    p.n += 1;
+    p.bytes += bytes;
+}
+void Engine::prof_collect() {
+    sync();
+    for (auto& kv : prof) {
+        for (auto& pr : kv.second.ev) {
+            float ms = 0.f;
+            SMOE_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            kv.second.ms += ms;
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        kv.second.ev.clear();
+    }
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, long long a_rows_per_slot, int Nout,
+                  int Kd, const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
+                  const void* X, const TcOperand& bmap, void* Y, int ldy, Epi epi, const char* cls, double bytes) {
+    cudaEvent_t ev;
+    prof_begin(cls, &ev);
+    if (use_tc) {
+        TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound,
+                     Y, ldy, epi};
+        launch_gemm_tc(a, stream);
+    } else {
+        GemmArgs a{W, slot_stride, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound, X, Y, ldy, epi};
+        launch_gemm_simt(a, wt, stream);
+    }
+    prof_end(cls, ev, bytes);
+}
+
+// ------------------------------------------------------------------ the batched forward pass
+// One pass over T rows (model.cpp:192-263 applied to every row at once).
+void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
+                  int log_slot) {
+    if (T <= 0) return;
+    if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
+    const size_t ws = wt == kF32 ? 4 : 2;
+    launch_x0(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, stream);
+    const double wbytes_dd = (double)d * d * ws;
+    for (int l = 0; l < L; ++l) {
+        launch_rms(x, T, d, xa, wt, stream);
+        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, T, l, T, xa, op_xa, x, d, kEpiResidAdd,
+             "dense_gemm", wbytes_dd);
+        const int mo = moe_ord[l];
+        const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
+        if (mo >= 0) {
+            int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
+            int* fl = fin_log + ((size_t)log_slot * M + mo) * Tmax * K;
+            GateArgs g{x, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E, xa, wt, rl, fl, wgt,
+                       restricted ? in_draft + (size_t)mo * E : nullptr, draft_sorted + (size_t)mo * E,
+                       rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft, use_aff, mo, row_plen, flags};
+            launch_gate(g, stream);
+            launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
+            launch_gather(xa, pos, T, K, d, xperm, wt, stream);
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf,
+                 f, kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh, "expert_gemm", ebytes_up);
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf,
+                 d, kEpiStoreF32, "expert_gemm", ebytes_dn);
+            launch_combine(x, ybuf, pos, wgt, T, K, d, 0, stream);
+        } else {
+            launch_rms(x, T, d, xa, wt, stream);
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, T, dense_slot[l], T, xa, op_xa,
+                 hbuf, f, kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh, "dense_gemm", ebytes_up);
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, nullptr, nullptr, 1, T, dense_slot[l], T, hbuf, op_h,
+                 ybuf, d, kEpiStoreF32, "dense_gemm", ebytes_dn);
+            launch_combine(x, ybuf, nullptr, nullptr, T, 1, d, 1, stream);
+        }
+    }
+    launch_rms(x, T, d, xa, wt, stream);
+    gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32, "head_gemm",
+         (double)V * d * ws);
+    launch_argmax(logits, T, V, amax, flags, stream);
+    SMOE_CUDA(cudaGetLastError());
+}
+
+void Engine::reset_sequences(const std::vector<std::vector<int>>& prompts) {
+    const int B = (int)prompts.size();
+    if (B > Bmax) throw Error(kConfig, "engine: batch exceeds max_batch");
+    SMOE_CUDA(cudaMemsetAsync(seq_sum, 0, sizeof(double) * Bmax * d, stream));
+    SMOE_CUDA(cudaMemsetAsync(seq_len, 0, sizeof(int) * Bmax, stream));
+    size_t plen = 0;
+    for (auto& p : prompts) plen = std::max(plen, p.size());
+    std::vector<int> toks((size_t)B * plen, 0), take(B), sq(B);
+    for (int b = 0; b < B; ++b) {
+        for (int v : prompts[b])
+            if (v < 0 || v >= V) throw Error(kInvariant, "forward: token out of range");
+        std::copy(prompts[b].begin(), prompts[b].end(), toks.begin() + (size_t)b * plen);
+        take[b] = (int)prompts[b].size();
+        sq[b] = b;
+    }
+    int* dtoks = dalloc<int>(toks.size());
+    upload_ints(dtoks, toks.data(), toks.size());
+    upload_ints(commit_take, take.data(), B);
+    upload_ints(seqs, sq.data(), B);
+    launch_commit(seq_sum, seq_len, emb64, seqs, dtoks, (int)plen, commit_take, B, d, stream);
+    sync();
+    SMOE_CUDA(cudaFree(dtoks));
+}
+
+void Engine::forward_one(const std::vector<int>& prefix, const int* restricted, int n_draft, int use_aff,
+                         float* logits_out, int* raw_out, int* fin_out) {
+    if (prefix.empty()) throw Error(kInvariant, "forward: empty prefix");
+    if (use_aff && !have_affinity) throw Error(kInvariant, "forward: affinity table required but missing");
+    if (restricted) {
+        std::vector<std::vector<int>> sets(M);
+        for (int m = 0; m < M; ++m) sets[m].assign(restricted + (size_t)m * n_draft, restricted + (size_t)(m + 1) * n_draft);
+        set_draft_sets(sets, n_draft);
+    }
+    reset_sequences({prefix});
+    int zero = 0;
+    upload_ints(row_seq, &zero, 1);
+    pass(1, row_seq, nullptr, 0, restricted != nullptr, use_aff, 0);
+    sync();
+    check_flags();
+    if (logits_out) SMOE_CUDA(cudaMemcpy(logits_out, logits, sizeof(float) * V, cudaMemcpyDeviceToHost));
+    for (int m = 0; m < M; ++m) {
+        if (raw_out) SMOE_CUDA(cudaMemcpy(raw_out + (size_t)m * K, raw_log + (size_t)m * Tmax * K, sizeof(int) * K,
+                                          cudaMemcpyDeviceToHost));
+        if (fin_out) SMOE_CUDA(cudaMemcpy(fin_out + (size_t)m * K, fin_log + (size_t)m * Tmax * K, sizeof(int) * K,
+                                          cudaMemcpyDeviceToHost));
+    }
+}
+
+}  // namespace smoe

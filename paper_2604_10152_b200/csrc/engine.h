@@ -1,0 +1,201 @@
+// engine.h -- the B200 engine: device-resident model, per-sequence prefix state, batched draft /
+// verify passes, expert store and the speculative-decode loop.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/specmoe_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace smoe {
+
+// tcgen05 grouped GEMM (gemm_tc.cu).  A = weights (TMA, K-major, 128-row tiles), B = activations.
+struct TcOperand {
+    const void* base;  // bf16, row-major [rows][K]
+    long long rows;
+    int K;
+};
+struct TcGemmArgs {
+    TcOperand A;        // weight pool, 2D [slots*rows_per_slot, K]
+    long long a_rows_per_slot;
+    TcOperand B;        // activations [rows, K]
+    int Nout, K;
+    const int* group_off;  // nullptr -> single group {0, single_rows} with slot single_slot
+    const int* group_slot;
+    int G, single_rows, single_slot;
+    int rows_bound;
+    void* Y;
+    int ldy;
+    Epi epi;
+};
+void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
+
+struct RunCfg {
+    int gamma = 10, n_draft = 4, max_new_tokens = 32, use_affinity = 1, warmup_steps = 64, policy = 2,
+        collect_trace = 0;
+    uint64_t run_seed = 0;
+    uint64_t device_capacity_bytes = 0, bytes_per_expert = 0;
+    double host_bandwidth = 64e9, ssd_bandwidth = 0.0, compute_rate = 1e6, compute_cost_per_expert = 2e-6;
+};
+
+struct LedgerEntry { int phase, step, layer, expert; uint64_t bytes; };
+struct Outcome { int seq, phase, accepted, correction, generated; std::vector<int> drafts; };
+struct TraceRow { int step, seq, layer; std::vector<int> experts; };
+
+struct RunOut {
+    int B = 0, max_new = 0, gamma = 0;
+    std::vector<std::vector<int>> tokens;
+    std::vector<LedgerEntry> ledger;
+    std::vector<Outcome> outcomes;
+    std::vector<TraceRow> trace;
+    std::vector<uint64_t> hotness;  // [M][E]
+    double tau_mean = 1.0;
+    uint64_t tokens_total = 0;
+    int phases = 0;
+    double speculation_s = 0, verification_s = 0, modeled_seconds = 0, tokens_per_sec = 0;
+    uint64_t bytes_spec = 0, bytes_verify = 0, bytes_baseline = 0, bytes_total = 0, setup_bytes = 0,
+             warmup_bytes = 0;
+    double lambda = 1.0, c_measured = 0.0;
+    double wall_s = 0, gpu_s = 0, h2d_s = 0;
+    uint64_t h2d_expert_bytes = 0;
+};
+
+struct SpecState;  // stepped loop state (loop.cpp)
+struct SpecStateDeleter {
+    void operator()(SpecState* s) const;
+};
+
+class Engine {
+public:
+    explicit Engine(const smoe_engine_config& c);
+    ~Engine();
+
+    // ---- configuration
+    int L, E, K, d, f, V, M;
+    int kind;        // ExpertKind
+    WType wt;        // storage / operand type
+    int use_tc;      // tcgen05 path for GEMMs
+    int Bmax, Gmax, Tmax, stride;
+    double skew;
+    uint64_t seed;
+    std::vector<uint8_t> mask;
+    std::vector<int> moe_index;   // ordinal -> raw layer
+    std::vector<int> moe_ord;     // raw layer -> ordinal or -1
+    int n_dense;
+    int offload, n_slots;
+    int U;                        // rows per slot in the up pool (f or 2f)
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    int device = 0;
+
+    // ---- weights (device)
+    double* emb64 = nullptr;  // [V][d]
+    void* mix = nullptr;      // [L][d][d]
+    float* gate_w = nullptr;  // [M][E][d]
+    float* gate_b = nullptr;  // [M][E]
+    void* up_pool = nullptr;  // [S][U][d]
+    void* down_pool = nullptr;  // [S][d][f]
+    void* head = nullptr;     // [V][d]
+    int* slot_of = nullptr;   // [M][E] device
+    std::vector<int> h_slot_of;
+    std::vector<int> dense_slot;  // raw layer -> slot in pools (dense layers)
+    std::vector<double> affinity;  // [M][E][E]
+    bool have_affinity = false;
+
+    // ---- expert store (offload mode): pinned host pools, slots
+    void* host_up = nullptr;    // [M*E][U][d] pinned
+    void* host_down = nullptr;  // [M*E][d][f] pinned
+
+    // ---- per-sequence state / buffers (device)
+    double* seq_sum = nullptr;  // [Bmax][d]
+    int* seq_len = nullptr;     // [Bmax]
+    int* drafts = nullptr;      // [Bmax][stride]
+    int* vam = nullptr;         // [Bmax][stride]
+    int *row_seq = nullptr, *row_extra = nullptr, *row_plen = nullptr;  // row_seq/row_extra: [2*Tmax]
+    float* x = nullptr;
+    void* xa = nullptr;
+    int *raw_log = nullptr, *fin_log = nullptr;  // [Gmax+1][M][Tmax][K]
+    float* wgt = nullptr;
+    int *pos = nullptr, *group_off = nullptr, *group_slot = nullptr;
+    void* xperm = nullptr;  // [Tmax*K][d]
+    void* hbuf = nullptr;   // [Tmax*K][f]
+    float* ybuf = nullptr;  // [Tmax*K][d]
+    float* logits = nullptr;  // [Tmax][V]
+    int* amax = nullptr;
+    uint8_t* in_draft = nullptr;  // [M][E]
+    int* draft_sorted = nullptr;  // [M][Nmax]
+    int* rank = nullptr;          // [M][E][Nmax]
+    int* acc = nullptr;
+    int* corr = nullptr;
+    int* commit_toks = nullptr;  // [Bmax][stride]
+    int* commit_take = nullptr;  // [Bmax]
+    int* seqs = nullptr;         // [Bmax]
+    int* flags = nullptr;
+    double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
+    size_t scratch64_n = 0;
+    // pinned host staging
+    int* h_small = nullptr;  // generic pinned int staging
+    size_t h_small_n = 0;
+
+    // tcgen05 operands (tensor maps are built and cached per box shape by gemm_tc.cu)
+    TcOperand op_mix, op_up, op_down, op_head, op_xa, op_xperm, op_h;
+
+    // ---- profiling (CUDA events around kernel classes)
+    bool profiling = false;
+    struct Prof { double ms = 0; long long n = 0; double bytes = 0; std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
+    std::map<std::string, Prof> prof;
+    void prof_begin(const char* cls, cudaEvent_t* a);
+    void prof_end(const char* cls, cudaEvent_t a, double bytes);
+    void prof_collect();
+
+    // ---- weights init
+    void init_exact();
+    void init_device(uint64_t seed);
+    void upload_tensor(const std::string& name, int layer, int expert, const double* src, long long n);
+    void build_affinity_device();
+
+    // ---- draft tables
+    void set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft);  // sorted per layer
+    int cur_n_draft = 0;
+
+    // ---- passes
+    // rows r=0..T-1: sequence slot row_seq[r], pending-draft count row_extra[r] (or extra_uniform).
+    // restricted = draft semantics.  log_slot selects where raw/fin picks are logged.
+    void pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
+              int log_slot);
+    void gemm(const void* W, long long slot_stride, const TcOperand& aop, long long a_rows_per_slot, int Nout, int Kd,
+              const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
+              const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes);
+
+    // ---- host<->device helpers
+    void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream
+    void sync();
+    void check_flags();
+
+    // ---- public ops
+    void forward_one(const std::vector<int>& prefix, const int* restricted, int n_draft, int use_aff,
+                     float* logits_out, int* raw_out, int* fin_out);
+    void reset_sequences(const std::vector<std::vector<int>>& prompts);
+
+    // ---- store (offload)
+    uint64_t real_bytes_per_expert() const;
+    uint64_t h2d_bytes = 0;
+    double h2d_ms = 0;
+
+    // stepped loop
+    std::unique_ptr<SpecState, SpecStateDeleter> st;
+};
+
+// loop.cpp
+RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
+RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
+void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
+int spec_step(Engine& e, int* accepted_tokens);  // returns number of active sequences after the step
+RunOut spec_end(Engine& e);
+
+}  // namespace smoe

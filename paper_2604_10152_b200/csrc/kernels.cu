@@ -1,0 +1,472 @@
+// kernels.cu -- state, normalisation, gating/routing, permutation, combine, argmax, accept and
+// commit kernels of the spec-decode hot path (sm_100a).  These move a few MB per pass, so they
+// are latency-bound; they are written as single-pass, coalesced, 16-byte-vectorised kernels.
+#include <math.h>
+
+#include "kernels.h"
+
+namespace smoe {
+
+namespace {
+
+constexpr int kPairChunks = 64;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order block reduction (warp butterflies then warp 0): the result depends only on the
+// block size, never on T, so every row is computed identically in every pass (batch invariance).
+__device__ float block_sum(float v, float* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    float t = lane < nw ? red[lane] : 0.f;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) red[32] = t;
+    __syncthreads();
+    return red[32];
+}
+
+template <typename T>
+__device__ __forceinline__ void store_op(void* base, long long idx, float v) {
+    reinterpret_cast<T*>(base)[idx] = from_f<T>(v);
+}
+
+// ------------------------------------------------------------------ K1 prefix state
+__global__ void k_x0(const double* __restrict__ emb, const double* __restrict__ ssum, const int* __restrict__ slen,
+                     const int* __restrict__ pend, int pstride, const int* __restrict__ row_seq,
+                     const int* __restrict__ row_extra, int extra_u, int d, float* __restrict__ x,
+                     int* __restrict__ row_plen) {
+    const int r = blockIdx.x;
+    const int b = row_seq[r];
+    const int e = row_extra ? row_extra[r] : extra_u;
+    const int n = slen[b] + e;
+    const int* toks = pend + (long long)b * pstride;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        double acc = ssum[(long long)b * d + i];
+        for (int j = 0; j < e; ++j) acc += emb[(long long)toks[j] * d + i];
+        x[(long long)r * d + i] = (float)(acc / (double)n);
+    }
+    if (threadIdx.x == 0) row_plen[r] = n;
+}
+
+// ------------------------------------------------------------------ K2 rms
+template <typename OT>
+__global__ void k_rms(const float* __restrict__ x, int d, void* __restrict__ xa) {
+    __shared__ float red[33];
+    const float* xr = x + (long long)blockIdx.x * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+    ss = block_sum(ss, red);
+    const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) store_op<OT>(xa, (long long)blockIdx.x * d + i, xr[i] * inv);
+}
+
+// ------------------------------------------------------------------ K4/K5 gate + remap
+template <typename OT>
+__global__ void k_gate(GateArgs a) {
+    extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[33]
+    float* xf = sm;
+    float* gl = xf + a.d;
+    float* red = gl + 2 * a.E;
+    const int r = blockIdx.x, d = a.d, E = a.E, K = a.K;
+    const float* xr = a.x + (long long)r * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float v = xr[i];
+        xf[i] = v;
+        ss += v * v;
+    }
+    ss = block_sum(ss, red);
+    const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float v = xf[i] * inv;
+        xf[i] = v;
+        store_op<OT>(a.xa, (long long)r * d + i, v);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = w; e < E; e += nw) {
+        const float* gw = a.gate_w + (long long)e * d;
+        float acc = 0.f;
+        for (int i = lane; i < d; i += 32) acc += gw[i] * xf[i];
+        acc = warp_sum(acc);
+        if (lane == 0) gl[e] = acc + a.gate_b[e];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    // softmax (model.cpp:145-157), max-subtracted
+    float mx = gl[0];
+    bool finite = true;
+    for (int e = 0; e < E; ++e) {
+        finite &= isfinite(gl[e]);
+        if (gl[e] > mx) mx = gl[e];
+    }
+    if (!finite) atomicOr(a.flags, kFlagNonFiniteGate);
+    float* p = gl + E;
+    float sum = 0.f;
+    for (int e = 0; e < E; ++e) {
+        p[e] = expf(gl[e] - mx);
+        sum += p[e];
+    }
+    // top-K: repeated first-max selection == stable sort descending (model.cpp:159-170)
+    unsigned long long taken = 0ull;  // E <= 64
+    int chosen[16];
+    for (int k = 0; k < K; ++k) {
+        int best = -1;
+        for (int e = 0; e < E; ++e)
+            if (!((taken >> e) & 1ull) && (best < 0 || gl[e] > gl[best])) best = e;
+        taken |= 1ull << best;
+        const int pick = best;
+        int ex = pick;
+        if (a.in_draft) {
+            bool dup = false;
+            for (int j = 0; j < k; ++j) dup |= chosen[j] == pick;
+            if (!(a.in_draft[pick] && !dup)) {
+                ex = -1;
+                if (a.use_affinity) {  // nearest by (distance, index): first non-excluded rank
+                    for (int j = 0; j < a.N && ex < 0; ++j) {
+                        int c = a.rank[pick * a.N + j];
+                        bool ex_c = false;
+                        for (int q = 0; q < k; ++q) ex_c |= chosen[q] == c;
+                        if (!ex_c) ex = c;
+                    }
+                } else {  // hash surrogate (drafting.cpp:140-151)
+                    int cnt = 0;
+                    for (int j = 0; j < a.N; ++j) {
+                        bool ex_c = false;
+                        for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
+                        cnt += !ex_c;
+                    }
+                    if (cnt > 0) {
+                        uint64_t h = substream(0x5eed5eedull,
+                                               ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
+                                               (uint64_t)a.row_plen[r]);
+                        int want = (int)(h % (uint64_t)cnt);
+                        for (int j = 0; j < a.N; ++j) {
+                            bool ex_c = false;
+                            for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
+                            if (!ex_c && want-- == 0) { ex = a.draft_sorted[j]; break; }
+                        }
+                    }
+                }
+                if (ex < 0) {
+                    atomicOr(a.flags, kFlagEmptyRemap);
+                    ex = pick;
+                }
+            }
+        }
+        chosen[k] = ex;
+        a.raw[r * K + k] = pick;
+        a.fin[r * K + k] = ex;
+        a.wgt[r * K + k] = p[pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
+    }
+}
+
+// ------------------------------------------------------------------ K6 permutation
+__global__ void k_route(const int* __restrict__ fin, int n, int E, const int* __restrict__ slot_of,
+                        int* __restrict__ off, int* __restrict__ gslot, int* __restrict__ pos) {
+    extern __shared__ int s[];  // fin[n], cnt[E+1]
+    int* f = s;
+    int* cnt = s + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) f[i] = fin[i];
+    for (int i = threadIdx.x; i <= E; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[f[i]], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int e = 0; e < E; ++e) {
+            int c = cnt[e];
+            cnt[e] = run;
+            off[e] = run;
+            gslot[e] = slot_of[e];
+            run += c;
+        }
+        off[E] = run;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int e = f[i];
+        int rank = 0;
+        for (int q = 0; q < i; ++q) rank += f[q] == e;
+        pos[i] = cnt[e] + rank;
+    }
+}
+
+__global__ void k_single_group(int T, int slot, int* off, int* gslot) {
+    off[0] = 0;
+    off[1] = T;
+    gslot[0] = slot;
+}
+
+__global__ void k_gather(const uint4* __restrict__ xa, const int* __restrict__ pos, int K, int vecs,
+                         uint4* __restrict__ xp) {
+    const int p = blockIdx.x;
+    const int t = p / K;
+    const uint4* src = xa + (long long)t * vecs;
+    uint4* dst = xp + (long long)pos[p] * vecs;
+    for (int i = threadIdx.x; i < vecs; i += blockDim.x) dst[i] = src[i];
+}
+
+// ------------------------------------------------------------------ K9 combine
+__global__ void k_combine(float* __restrict__ x, const float* __restrict__ y, const int* __restrict__ pos,
+                          const float* __restrict__ wgt, int K, int d, int dense) {
+    const int t = blockIdx.x;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float acc;
+        if (dense) {
+            acc = y[(long long)t * d + i];
+        } else {
+            acc = 0.f;
+            for (int k = 0; k < K; ++k) acc += wgt[t * K + k] * y[(long long)pos[t * K + k] * d + i];
+        }
+        x[(long long)t * d + i] += acc;
+    }
+}
+
+// ------------------------------------------------------------------ K10 argmax
+__global__ void k_argmax(const float* __restrict__ lg, int V, int* __restrict__ out, int* flags) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    const float* row = lg + (long long)blockIdx.x * V;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    bool fin = true;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        float v = row[i];
+        fin &= isfinite(v);
+        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    if (!fin) atomicOr(flags, kFlagNonFiniteLogits);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sv[w] = bv; si[w] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 1; j < (int)(blockDim.x >> 5); ++j)
+            if (sv[j] > bv || (sv[j] == bv && si[j] < bi)) { bv = sv[j]; bi = si[j]; }
+        out[blockIdx.x] = bi == 0x7fffffff ? 0 : bi;
+    }
+}
+
+__global__ void k_scatter_tokens(const int* src, const int* row_seq, const int* row_extra, int extra_u, int T,
+                                 int* dst, int stride) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= T) return;
+    int e = row_extra ? row_extra[r] : extra_u;
+    dst[(long long)row_seq[r] * stride + e] = src[r];
+}
+
+__global__ void k_accept(const int* drafts, const int* vam, const int* seqs, int na, int gamma, int stride, int* acc,
+                         int* corr) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    const int b = seqs[i];
+    const int* dr = drafts + (long long)b * stride;
+    const int* am = vam + (long long)b * stride;
+    int a = 0;
+    while (a < gamma && dr[a] == am[a]) ++a;
+    acc[i] = a;
+    corr[i] = am[a];
+}
+
+__global__ void k_commit(double* ssum, int* slen, const double* emb, const int* seqs, const int* toks, int tstride,
+                         const int* take, int d) {
+    const int j = blockIdx.x;
+    const int b = seqs[j];
+    const int n = take[j];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        double s = ssum[(long long)b * d + i];
+        for (int t = 0; t < n; ++t) s += emb[(long long)toks[(long long)j * tstride + t] * d + i];
+        ssum[(long long)b * d + i] = s;
+    }
+    if (threadIdx.x == 0) slen[b] += n;
+}
+
+// ------------------------------------------------------------------ init / conversion
+__device__ __forceinline__ double normal_at(uint64_t seed, uint64_t tid, long long i) {
+    uint64_t h = splitmix64(seed ^ splitmix64(tid * 0x9E3779B97F4A7C15ull + (uint64_t)i));
+    uint64_t h2 = splitmix64(h ^ 0xD1B54A32D192ED03ull);
+    double u1 = ((double)(h >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+    double u2 = (double)(h2 >> 11) * 0x1.0p-53;
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+template <typename T>
+__global__ void k_fill_normal(T* dst, long long n, double sd, uint64_t seed, uint64_t tid) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = from_f<T>((float)(sd * normal_at(seed, tid, i)));
+}
+__global__ void k_fill_normal_f64(double* dst, long long n, double sd, uint64_t seed, uint64_t tid) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = sd * normal_at(seed, tid, i);
+}
+
+template <typename T>
+__global__ void k_convert_transpose(const double* __restrict__ src, int rows, int cols, T* __restrict__ dst) {
+    __shared__ double tile[32][33];
+    int c = blockIdx.x * 32 + threadIdx.x;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int r = blockIdx.y * 32 + j;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = src[(long long)r * cols + c];
+    }
+    __syncthreads();
+    int r = blockIdx.y * 32 + threadIdx.x;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int cc = blockIdx.x * 32 + j;
+        if (r < rows && cc < cols) dst[(long long)cc * rows + r] = from_f<T>((float)tile[threadIdx.x][j]);
+    }
+}
+template <typename T>
+__global__ void k_convert(const double* __restrict__ src, long long n, T* __restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = from_f<T>((float)src[i]);
+}
+
+template <typename T>
+__global__ void k_pair_sqdist(const T* __restrict__ pool, long long stride, long long n, const int* __restrict__ slots,
+                              int E, double* __restrict__ out) {
+    // blockIdx.x = pair (i,j) with i<j enumerated row-major; blockIdx.y = chunk
+    int p = blockIdx.x, i = 0;
+    while (p >= E - 1 - i) { p -= E - 1 - i; ++i; }
+    const int j = i + 1 + p;
+    const T* a = pool + (long long)slots[i] * stride;
+    const T* b = pool + (long long)slots[j] * stride;
+    const long long per = (n + gridDim.y - 1) / gridDim.y;
+    const long long s0 = per * blockIdx.y, s1 = min(n, s0 + per);
+    double acc = 0.0;
+    for (long long k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
+        double df = (double)to_f<T>(a[k]) - (double)to_f<T>(b[k]);
+        acc += df * df;
+    }
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[((long long)i * E + j) * gridDim.y + blockIdx.y] += t;
+    }
+}
+
+}  // namespace
+
+void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
+               const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
+               cudaStream_t s) {
+    if (T <= 0) return;
+    k_x0<<<T, 128, 0, s>>>(emb64, seq_sum, seq_len, pend, pend_stride, row_seq, row_extra, extra_uniform, d, x,
+                           row_plen);
+}
+
+void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s) {
+    if (T <= 0) return;
+    if (op == kF32) k_rms<float><<<T, 256, 0, s>>>(x, d, xa);
+    else k_rms<__nv_bfloat16><<<T, 256, 0, s>>>(x, d, xa);
+}
+
+void launch_gate(const GateArgs& a, cudaStream_t s) {
+    if (a.T <= 0) return;
+    size_t smem = sizeof(float) * (a.d + 2 * a.E + 33);
+    if (a.op == kF32) k_gate<float><<<a.T, 256, smem, s>>>(a);
+    else k_gate<__nv_bfloat16><<<a.T, 256, smem, s>>>(a);
+}
+
+void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot, int* pos,
+                  cudaStream_t s) {
+    const int n = T * K;
+    k_route<<<1, 1024, sizeof(int) * (n + E + 1), s>>>(fin, n, E, slot_of, group_off, group_slot, pos);
+}
+
+void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaStream_t s) {
+    k_single_group<<<1, 1, 0, s>>>(T, slot, group_off, group_slot);
+}
+
+void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s) {
+    if (T <= 0) return;
+    const int vecs = d * (op == kF32 ? 4 : 2) / 16;
+    k_gather<<<T * K, 128, 0, s>>>(reinterpret_cast<const uint4*>(xa), pos, K, vecs, reinterpret_cast<uint4*>(xperm));
+}
+
+void launch_combine(float* x, const float* y, const int* pos, const float* wgt, int T, int K, int d, int dense,
+                    cudaStream_t s) {
+    if (T <= 0) return;
+    k_combine<<<T, 256, 0, s>>>(x, y, pos, wgt, K, d, dense);
+}
+
+void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
+    if (T <= 0) return;
+    k_argmax<<<T, 512, 0, s>>>(logits, V, out, flags);
+}
+
+void launch_scatter_tokens(const int* src, const int* row_seq, const int* row_extra, int extra_uniform, int T, int* dst,
+                           int stride, cudaStream_t s) {
+    if (T <= 0) return;
+    k_scatter_tokens<<<ceil_div(T, 128), 128, 0, s>>>(src, row_seq, row_extra, extra_uniform, T, dst, stride);
+}
+
+void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, int gamma, int stride, int* acc,
+                   int* corr, cudaStream_t s) {
+    if (na <= 0) return;
+    k_accept<<<ceil_div(na, 128), 128, 0, s>>>(drafts, vam, seqs, na, gamma, stride, acc, corr);
+}
+
+void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
+                   int tok_stride, const int* take, int na, int d, cudaStream_t s) {
+    if (na <= 0) return;
+    k_commit<<<na, 256, 0, s>>>(seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
+}
+
+void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
+                        cudaStream_t s) {
+    int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
+    if (grid <= 0) return;
+    if (t == kF32) k_fill_normal<float><<<grid, 256, 0, s>>>((float*)dst, n, stddev, seed, tensor_id);
+    else k_fill_normal<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst, n, stddev, seed, tensor_id);
+}
+void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
+                            cudaStream_t s) {
+    int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
+    if (grid <= 0) return;
+    k_fill_normal_f64<<<grid, 256, 0, s>>>(dst, n, stddev, seed, tensor_id);
+}
+
+void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s) {
+    dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32)), block(32, 8);
+    if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst);
+    else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst);
+}
+void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s) {
+    int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
+    if (grid <= 0) return;
+    if (t == kF32) k_convert<float><<<grid, 256, 0, s>>>(src, n, (float*)dst);
+    else k_convert<__nv_bfloat16><<<grid, 256, 0, s>>>(src, n, (__nv_bfloat16*)dst);
+}
+void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s) {
+    launch_convert(src, n, dst, kF32, s);
+}
+
+void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, long long n, const int* slots, int E,
+                            double* out, cudaStream_t s) {
+    if (E < 2) return;
+    dim3 grid(E * (E - 1) / 2, kPairChunks);
+    if (t == kF32)
+        k_pair_sqdist<float><<<grid, 512, 0, s>>>((const float*)pool, slot_stride, n, slots, E, out);
+    else
+        k_pair_sqdist<__nv_bfloat16><<<grid, 512, 0, s>>>((const __nv_bfloat16*)pool, slot_stride, n, slots, E, out);
+}
+
+}  // namespace smoe

@@ -1,0 +1,109 @@
+// kernels.h -- launchers for the sm_100a kernels of the spec-decode hot path.
+// Every launcher enqueues on the given stream and never synchronises.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace smoe {
+
+// K1 (model.cpp:212-217): x[r] = (sum[b] + sum_{j<e} emb[pend[b][j]]) / (len[b] + e), computed in
+// float64 in the reference's sequential order, stored as f32.  e = row_extra[r] (or extra_uniform
+// when row_extra == nullptr); also writes the row's prefix length (for the surrogate remap).
+void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
+               const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
+               cudaStream_t s);
+
+// K2 (model.cpp:19-26): xa[r] = x[r] * (mean(x^2) + 1e-12)^-1/2 in the operand type.
+void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s);
+
+// K4+K5 (model.cpp:229-246, drafting.cpp:123-151): fused rms + gate GEMV + bias + softmax +
+// top-K + (restricted) remap.  Writes the normalised row (operand type) for the experts, raw/final
+// picks [T][K] and the combine weight p[raw] [T][K].
+struct GateArgs {
+    const float* x;
+    int T, d, E, K;
+    const float* gate_w;  // [E][d]
+    const float* gate_b;  // [E]
+    void* xa;             // out [T][d] operand type
+    WType op;
+    int* raw;             // out [T][K]
+    int* fin;             // out [T][K]
+    float* wgt;           // out [T][K]
+    // restricted (draft) mode; in_draft == nullptr => target semantics
+    const uint8_t* in_draft;  // [E]
+    const int* draft_sorted;  // [N]
+    const int* rank;          // [E][N] draft members ordered by (affinity distance, index)
+    int N;
+    int use_affinity;
+    int moe_ordinal;
+    const int* row_plen;      // prefix length per row (surrogate hash)
+    int* flags;
+};
+void launch_gate(const GateArgs& a, cudaStream_t s);
+
+// K6: stable (expert, token, k) permutation.  group_off [E+1], group_slot [E] (slot of each expert
+// in the weight pool via slot_of[E]), pos [T*K] = destination row of pick (t,k).
+void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot,
+                  int* pos, cudaStream_t s);
+// Single group {0, T} -> slot (dense layers / head / mix).
+void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaStream_t s);
+// xperm[pos[t*K+k]] = xa[t]
+void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s);
+
+// K9 (model.cpp:248-257): x[t] += sum_k wgt[t,k] * y[pos[t,k]] (k in order); dense: x[t] += y[t].
+void launch_combine(float* x, const float* y, const int* pos, const float* wgt, int T, int K, int d, int dense,
+                    cudaStream_t s);
+
+// K10 (model.cpp:172-176): per-row argmax, first max wins; non-finite -> flag.
+void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s);
+
+// dst[row_seq[r]*stride + extra(r)] = src[r]
+void launch_scatter_tokens(const int* src, const int* row_seq, const int* row_extra, int extra_uniform, int T,
+                           int* dst, int stride, cudaStream_t s);
+
+// K11 (specdec.cpp:63-80): a = longest prefix drafts[i] == vam[i]; corr = vam[a].
+void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, int gamma, int stride, int* acc,
+                   int* corr, cudaStream_t s);
+
+// State advance / rollback (F6): sum[b] += emb[tok] for the taken tokens, len[b] += take.
+void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
+                   int tok_stride, const int* take, int na, int d, cudaStream_t s);
+
+// Grouped skinny GEMM on CUDA cores (f32 or bf16 weights, f32 accumulation):
+//   for group g with slot s = group_slot[g] >= 0 and rows [group_off[g], group_off[g+1]):
+//     acc[r][n] = sum_k W[s][n][k] * X[r][k]       (n < Nout)
+//   epilogue per Epi.  For kEpiSwiglu, W[s] has 2*Nout rows: [0,Nout) w1, [Nout,2Nout) w3.
+struct GemmArgs {
+    const void* W;
+    long long slot_stride;  // elements between slots
+    int Nout, K;
+    const int* group_off;  // nullptr -> single group {0, single_rows} with slot single_slot
+    const int* group_slot;
+    int G;
+    int single_rows, single_slot;
+    int rows_bound;  // upper bound on rows in any group (host-known)
+    const void* X;   // [rows][K] operand type
+    void* Y;         // [rows][ldy]
+    int ldy;
+    Epi epi;
+};
+void launch_gemm_simt(const GemmArgs& a, WType wt, cudaStream_t s);
+
+// Device init / conversion helpers.
+void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
+                        cudaStream_t s);
+void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
+                            cudaStream_t s);
+// dst[c][r] = (T)src[r][c] for a rows x cols float64 source (reference row-major -> K-major).
+void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s);
+void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s);
+void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
+
+// Pairwise L2 distance of expert weights (drafting.cpp:28-57) accumulated in float64:
+// out[i*E+j] += sum_k (a_i[k]-a_j[k])^2 over one matrix pool region, for all i<j.
+void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, long long n, const int* slots, int E,
+                            double* out, cudaStream_t s);
+
+}  // namespace smoe

@@ -1,0 +1,558 @@
+// loop.cpp -- the self-assisted speculative-decoding loop (specdec.cpp:190-397) and the on-demand
+// comparator (baselines.cpp:29-99) on top of the device engine.
+//
+// Device side, per phase and without any host round trip in between: gamma restricted draft passes
+// (T = active sequences), one unrestricted verify pass (T = active * (gamma+1)), the accept kernel.
+// Host side, once per phase: read back accepted counts, corrections and the raw routing picks,
+// then run the reference's bookkeeping -- coalesced ensure_resident, acceptance/truncation, hotness,
+// hot_temporal selection + pin, flush -- exactly as the reference orders it, so tokens, ledger,
+// outcomes and modeled metrics equal the oracle's.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <random>
+
+#include "engine.h"
+
+namespace smoe {
+
+namespace {
+
+// ------------------------------------------------------------------ memsim replica (memsim.cpp)
+struct Ledger {
+    std::vector<LedgerEntry> e;
+    uint64_t tot[3] = {0, 0, 0}, total = 0;
+    void add(int phase, int step, int key, int E, uint64_t bytes) {
+        e.push_back(LedgerEntry{phase, step, key / E, key % E, bytes});
+        tot[phase] += bytes;
+        total += bytes;
+    }
+    void reset() {
+        e.clear();
+        tot[0] = tot[1] = tot[2] = 0;
+        total = 0;
+    }
+};
+
+void tier_check(const RunCfg& c, int n_draft, int M) {  // memsim.cpp:21-31
+    if (c.host_bandwidth <= 0.0) throw Error(kConfig, "tier: host_bandwidth > 0 violated");
+    if (c.ssd_bandwidth < 0.0) throw Error(kConfig, "tier: ssd_bandwidth >= 0 violated");
+    if (c.bytes_per_expert == 0) throw Error(kConfig, "tier: bytes_per_expert > 0 violated");
+    if (c.compute_rate <= 0.0) throw Error(kConfig, "tier: compute_rate > 0 violated");
+    if (c.compute_cost_per_expert < 0.0) throw Error(kConfig, "tier: expert compute cost >= 0 violated");
+    if (c.device_capacity_bytes < (uint64_t)n_draft * (uint64_t)M * c.bytes_per_expert)
+        throw Error(kConfig, "tier: device capacity below N * moe_layers * bytes_per_expert");
+}
+
+double step_cost(uint64_t toks, uint64_t experts, uint64_t bytes, const RunCfg& c, bool overlap) {  // memsim.cpp:163-172
+    const double comp = (double)toks / c.compute_rate + (double)experts * c.compute_cost_per_expert;
+    const double mig = (double)bytes / (c.ssd_bandwidth > 0.0 ? c.ssd_bandwidth : c.host_bandwidth);
+    return overlap ? std::max(comp, mig) : comp + mig;
+}
+
+// Residency: keys are (moe_layer * E + expert); iteration in key order == std::set<ExpertKey> order.
+class Residency {
+public:
+    Residency(int M, int E, const RunCfg& c) : M_(M), E_(E), cap_(c.device_capacity_bytes), bpe_(c.bytes_per_expert) {
+        tier_check(c, 0, M);
+        arrival_.assign((size_t)M * E, -1);
+        pinned_.assign((size_t)M * E, 0);
+    }
+    bool resident(int k) const { return arrival_[k] >= 0; }
+    bool pinned(int k) const { return pinned_[k] != 0; }
+    // memsim.cpp:102-113
+    uint64_t ensure(const std::vector<uint8_t>& keys, int phase, int step, Ledger& lg) {
+        uint64_t b = 0;
+        for (int k = 0; k < M_ * E_; ++k) {
+            if (!keys[k] || resident(k)) continue;
+            admit(k, keys);
+            lg.add(phase, step, k, E_, bpe_);
+            b += bpe_;
+        }
+        return b;
+    }
+    // memsim.cpp:115-150
+    uint64_t pin(const std::vector<std::vector<int>>& sets, Ledger& lg, int phase, int step) {
+        if ((int)sets.size() != M_) throw Error(kInvariant, "pin_draft_experts: set count != MoE layer count");
+        std::vector<uint8_t> target((size_t)M_ * E_, 0);
+        for (int l = 0; l < M_; ++l)
+            for (int e : sets[l]) {
+                if (e < 0 || e >= E_) throw Error(kInvariant, "residency: expert key out of range");
+                uint8_t& t = target[(size_t)l * E_ + e];
+                if (t) throw Error(kInvariant, "pin_draft_experts: duplicate expert in draft set");
+                t = 1;
+            }
+        for (int k = 0; k < M_ * E_; ++k)
+            if (pinned_[k] && !target[k]) pinned_[k] = 0;
+        uint64_t b = 0;
+        for (int k = 0; k < M_ * E_; ++k) {
+            if (!target[k]) continue;
+            if (!resident(k)) {
+                admit(k, target);
+                lg.add(phase, step, k, E_, bpe_);
+                b += bpe_;
+            }
+            pinned_[k] = 1;
+        }
+        return b;
+    }
+    void flush() {  // memsim.cpp:152-161
+        for (int k = 0; k < M_ * E_; ++k)
+            if (resident(k) && !pinned_[k]) { arrival_[k] = -1; used_ -= bpe_; }
+    }
+
+private:
+    void admit(int key, const std::vector<uint8_t>& keep) {  // memsim.cpp:81-100
+        while (used_ + bpe_ > cap_) {
+            int victim = -1;
+            for (int k = 0; k < M_ * E_; ++k) {
+                if (!resident(k) || pinned_[k] || keep[k]) continue;
+                if (victim < 0 || arrival_[k] < arrival_[victim]) victim = k;
+            }
+            if (victim < 0) throw Error(kInvariant, "residency: device capacity exhausted with no evictable expert");
+            arrival_[victim] = -1;
+            used_ -= bpe_;
+        }
+        arrival_[key] = (int64_t)seq_++;
+        used_ += bpe_;
+    }
+    int M_, E_;
+    uint64_t cap_, bpe_, used_ = 0, seq_ = 0;
+    std::vector<int64_t> arrival_;
+    std::vector<uint8_t> pinned_;
+};
+
+// ------------------------------------------------------------------ drafting replica (drafting.cpp:153-227)
+double unif(std::mt19937_64& r) { return (double)(r() >> 11) * 0x1.0p-53; }
+
+std::vector<std::vector<int>> select_sets(int policy, const std::vector<uint64_t>& counts, int M, int E,
+                                          const std::vector<std::vector<int>>& current, int n, std::mt19937_64& rng) {
+    if (n > E) throw Error(kConfig, "select_draft_experts: n_draft > experts_per_block");
+    std::vector<std::vector<int>> out(M);
+    for (int l = 0; l < M; ++l) {
+        if (policy == SMOE_POLICY_RANDOM) {
+            std::vector<int> pool(E);
+            for (int i = 0; i < E; ++i) pool[i] = i;
+            for (int i = 0; i < n; ++i) {
+                size_t j = (size_t)i + (size_t)(unif(rng) * (double)((size_t)E - (size_t)i));
+                std::swap(pool[i], pool[j]);
+            }
+            pool.resize(n);
+            std::sort(pool.begin(), pool.end());
+            out[l] = pool;
+            continue;
+        }
+        const uint64_t* c = counts.data() + (size_t)l * E;
+        std::vector<int> idx(E);
+        for (int i = 0; i < E; ++i) idx[i] = i;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return c[a] > c[b]; });
+        std::vector<int> picked;
+        for (int i = 0; i < std::min(n, E); ++i)
+            if (c[idx[i]] > 0) picked.push_back(idx[i]);
+        if ((int)picked.size() < n && l < (int)current.size())
+            for (int e : current[l]) {
+                if ((int)picked.size() == n) break;
+                if (std::find(picked.begin(), picked.end(), e) == picked.end()) picked.push_back(e);
+            }
+        if ((int)picked.size() != n) throw Error(kInvariant, "select_draft_experts: cannot assemble N draft experts");
+        std::sort(picked.begin(), picked.end());
+        out[l] = picked;
+    }
+    return out;
+}
+
+void validate_decode(const RunCfg& c, int B, int plen) {  // specdec.cpp:15-23
+    if (c.gamma < 1) throw Error(kConfig, "spec: gamma >= 1 violated");
+    if (B < 1) throw Error(kConfig, "spec: batch >= 1 violated");
+    if (c.max_new_tokens < 1) throw Error(kConfig, "spec: max_new_tokens >= 1 violated");
+    if (plen < 1) throw Error(kConfig, "spec: prompt_len >= 1 violated");
+    if (c.warmup_steps < 1) throw Error(kConfig, "spec: warmup_steps >= 1 violated");
+}
+
+int prompt_len_of(const std::vector<std::vector<int>>& prompts) {
+    size_t n = prompts.empty() ? 0 : prompts[0].size();
+    for (auto& p : prompts)
+        if (p.size() != n) throw Error(kConfig, "prompts must share one length");
+    return (int)n;
+}
+
+// Copy the raw (or final) picks of `T` rows of pass slot `slot` to host: out[m][T*K].
+void read_log(Engine& e, const int* log, int slot, int T, std::vector<int>& out) {
+    out.resize((size_t)e.M * T * e.K);
+    SMOE_CUDA(cudaMemcpy2DAsync(out.data(), sizeof(int) * T * e.K, log + (size_t)slot * e.M * e.Tmax * e.K,
+                                sizeof(int) * e.Tmax * e.K, sizeof(int) * T * e.K, e.M, cudaMemcpyDeviceToHost,
+                                e.stream));
+}
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    std::chrono::steady_clock::time_point w0;
+    void start(cudaStream_t s) {
+        if (!a) { SMOE_CUDA(cudaEventCreate(&a)); SMOE_CUDA(cudaEventCreate(&b)); }
+        w0 = std::chrono::steady_clock::now();
+        SMOE_CUDA(cudaEventRecord(a, s));
+    }
+    void stop(cudaStream_t s, double* gpu_s, double* wall_s) {
+        SMOE_CUDA(cudaEventRecord(b, s));
+        SMOE_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        SMOE_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *gpu_s = ms * 1e-3;
+        *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+}  // namespace
+
+struct SpecState {
+    RunCfg c;
+    int B = 0, M = 0, E = 0, K = 0, g = 0, nd = 0;
+    std::mt19937_64 prng;
+    std::unique_ptr<Residency> res;
+    Ledger led;
+    std::vector<std::vector<int>> sets;
+    bool sets_dirty = true;
+    std::vector<uint64_t> pc;  // phase hotness counter [M][E]
+    RunOut out;
+    std::vector<int> gen;
+    uint64_t tau_sum = 0, tau_cnt = 0;
+    double spec_s = 0, ver_s = 0, step_s = 0;
+    std::vector<uint64_t> lam;  // 4 per phase
+    int phase = 0;
+    Timer timer;
+    // scratch
+    std::vector<int> h_acc, h_corr, h_drafts, vraw, dfin, rows;
+};
+
+void SpecStateDeleter::operator()(SpecState* s) const { delete s; }
+
+// hot_global warmup (specdec.cpp:223-245): greedy on-demand steps over the prompts.
+static void hot_global_warmup(Engine& e, SpecState& S, const std::vector<std::vector<int>>& prompts) {
+    const int B = S.B, M = S.M, E = S.E, K = S.K;
+    std::vector<uint64_t> wc((size_t)M * E, 0);
+    Ledger wl;
+    Residency wr(M, E, S.c);
+    e.reset_sequences(prompts);
+    std::vector<int> rs(B), one(B, 1), raw, am(B);
+    for (int b = 0; b < B; ++b) rs[b] = b;
+    e.upload_ints(e.row_seq, rs.data(), B);
+    e.upload_ints(e.seqs, rs.data(), B);
+    e.upload_ints(e.commit_take, one.data(), B);
+    for (int step = 0; step < S.c.warmup_steps; ++step) {
+        e.pass(B, e.row_seq, nullptr, 0, false, 0, 0);
+        read_log(e, e.raw_log, 0, B, raw);
+        SMOE_CUDA(cudaMemcpyAsync(am.data(), e.amax, sizeof(int) * B, cudaMemcpyDeviceToHost, e.stream));
+        e.sync();
+        e.check_flags();
+        std::vector<uint8_t> need((size_t)M * E, 0);
+        for (int m = 0; m < M; ++m)
+            for (int b = 0; b < B; ++b)
+                for (int k = 0; k < K; ++k) {
+                    int key = m * E + raw[((size_t)m * B + b) * K + k];
+                    need[key] = 1;
+                    wc[key]++;
+                }
+        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream);
+        wr.ensure(need, 2, step, wl);
+        wr.flush();
+    }
+    S.out.warmup_bytes = wl.total;
+    S.sets = select_sets(SMOE_POLICY_HOT_GLOBAL, wc, M, E, S.sets, S.nd, S.prng);
+}
+
+void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts) {
+    std::unique_ptr<SpecState, SpecStateDeleter> S(new SpecState);
+    S->c = c;
+    const int plen = prompt_len_of(prompts);
+    validate_decode(c, (int)prompts.size(), plen);
+    S->B = (int)prompts.size();
+    S->M = e.M; S->E = e.E; S->K = e.K; S->g = c.gamma; S->nd = c.n_draft;
+    if (S->nd < e.K) throw Error(kConfig, "spec: n_draft >= top_k violated");
+    if (S->nd > e.E) throw Error(kConfig, "spec: n_draft <= experts_per_block violated");
+    tier_check(c, S->nd, e.M);
+    if (c.use_affinity && !e.have_affinity) throw Error(kInvariant, "run_specmoe: affinity table required but missing");
+    if (S->B > e.Bmax) throw Error(kConfig, "engine: batch exceeds max_batch");
+    if (S->g > e.Gmax) throw Error(kConfig, "engine: gamma exceeds max_gamma");
+    S->prng.seed(substream(c.run_seed, 0x706f6c69ull));
+    S->res = std::make_unique<Residency>(e.M, e.E, c);
+    S->pc.assign((size_t)e.M * e.E, 0);
+    S->out.B = S->B; S->out.max_new = c.max_new_tokens; S->out.gamma = c.gamma;
+    S->out.tokens.assign(S->B, {});
+    S->out.hotness.assign((size_t)e.M * e.E, 0);
+    S->sets = select_sets(SMOE_POLICY_RANDOM, S->pc, e.M, e.E, {}, S->nd, S->prng);
+    if (c.policy == SMOE_POLICY_HOT_GLOBAL) hot_global_warmup(e, *S, prompts);
+    S->res->pin(S->sets, S->led, 1, -1);
+    S->out.setup_bytes = S->led.total;
+    S->led.reset();
+    e.reset_sequences(prompts);
+    S->gen.assign(S->B, 0);
+    e.h2d_bytes = 0;
+    e.h2d_ms = 0;
+    S->timer.start(e.stream);
+    e.st = std::move(S);
+}
+
+int spec_step(Engine& e, int* accepted_tokens) {
+    SpecState& S = *e.st;
+    const int B = S.B, M = S.M, E = S.E, K = S.K, g = S.g;
+    if (accepted_tokens) *accepted_tokens = 0;
+    std::vector<int> act;
+    for (int b = 0; b < B; ++b)
+        if (S.gen[b] < S.c.max_new_tokens) act.push_back(b);
+    if (act.empty()) return 0;
+    const int na = (int)act.size();
+    for (int m = 0; m < M; ++m)
+        for (int ex : S.sets[m])
+            if (!S.res->pinned(m * E + ex) || !S.res->resident(m * E + ex))
+                throw Error(kInvariant, "run_specmoe: draft expert not pinned on device");
+    if (S.sets_dirty) {
+        e.set_draft_sets(S.sets, S.nd);
+        S.sets_dirty = false;
+    }
+    // rows: [0, na*(g+1)) verify (seq, i); [Tmax, Tmax+na) draft (seq)
+    const int TV = na * (g + 1);
+    S.rows.assign((size_t)2 * TV + na, 0);
+    for (int s = 0; s < na; ++s)
+        for (int i = 0; i <= g; ++i) {
+            S.rows[(size_t)s * (g + 1) + i] = act[s];
+            S.rows[(size_t)TV + s * (g + 1) + i] = i;
+        }
+    for (int s = 0; s < na; ++s) S.rows[(size_t)2 * TV + s] = act[s];
+    e.upload_ints(e.row_seq, S.rows.data(), TV);
+    e.upload_ints(e.row_extra, S.rows.data() + TV, TV);
+    int* drows = e.row_seq + e.Tmax;
+    e.upload_ints(drows, S.rows.data() + 2 * TV, na);
+    e.upload_ints(e.seqs, act.data(), na);
+
+    // (a) speculation: gamma restricted passes, drafts stay on device
+    for (int t = 0; t < g; ++t) {
+        e.pass(na, drows, nullptr, t, true, S.c.use_affinity, t);
+        launch_scatter_tokens(e.amax, drows, nullptr, t, na, e.drafts, e.stride, e.stream);
+    }
+    // (b) verification: one pass over all gamma+1 positions of every active sequence
+    e.pass(TV, e.row_seq, e.row_extra, 0, false, 0, g);
+    launch_scatter_tokens(e.amax, e.row_seq, e.row_extra, 0, TV, e.vam, e.stride, e.stream);
+    // (c) accept
+    launch_accept(e.drafts, e.vam, e.seqs, na, g, e.stride, e.acc, e.corr, e.stream);
+    S.h_acc.resize(na); S.h_corr.resize(na); S.h_drafts.resize((size_t)e.Bmax * e.stride);
+    SMOE_CUDA(cudaMemcpyAsync(S.h_acc.data(), e.acc, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
+    SMOE_CUDA(cudaMemcpyAsync(S.h_corr.data(), e.corr, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
+    SMOE_CUDA(cudaMemcpyAsync(S.h_drafts.data(), e.drafts, sizeof(int) * e.Bmax * e.stride, cudaMemcpyDeviceToHost,
+                              e.stream));
+    read_log(e, e.raw_log, g, TV, S.vraw);
+    std::vector<std::vector<int>> dfin(g);
+    for (int t = 0; t < g; ++t) read_log(e, e.fin_log, t, na, dfin[t]);
+    e.sync();
+    e.check_flags();
+
+    // modeled speculation time (specdec.cpp:282-288)
+    for (int t = 0; t < g; ++t) {
+        std::vector<uint8_t> ex((size_t)M * E, 0);
+        uint64_t distinct = 0;
+        for (int m = 0; m < M; ++m)
+            for (int q = 0; q < na * K; ++q) {
+                int key = m * E + dfin[t][(size_t)m * na * K + q];
+                if (!ex[key]) { ex[key] = 1; ++distinct; }
+            }
+        S.spec_s += step_cost((uint64_t)na, distinct, 0, S.c, false);
+    }
+    // coalesced union over the batch and all positions (specdec.cpp:303-317)
+    auto vraw_at = [&](int s, int i, int m, int k) { return S.vraw[((size_t)m * TV + (size_t)s * (g + 1) + i) * K + k]; };
+    std::vector<uint8_t> need((size_t)M * E, 0), first((size_t)M * E, 0);
+    uint64_t n_need = 0, n_first = 0;
+    for (int s = 0; s < na; ++s)
+        for (int i = 0; i <= g; ++i)
+            for (int m = 0; m < M; ++m)
+                for (int k = 0; k < K; ++k) {
+                    int key = m * E + vraw_at(s, i, m, k);
+                    if (!need[key]) { need[key] = 1; ++n_need; }
+                    if (i == 0 && !first[key]) { first[key] = 1; ++n_first; }
+                }
+    uint64_t spec_before = S.led.tot[0];
+    const uint64_t vb = S.res->ensure(need, 1, S.phase, S.led);
+    if (S.led.tot[0] != spec_before) throw Error(kInvariant, "run_specmoe: speculation phase migrated bytes");
+    const uint64_t vt = (uint64_t)na * (uint64_t)(g + 1);
+    S.ver_s += step_cost(vt, n_need, vb, S.c, false);
+    S.lam.insert(S.lam.end(), {vt, n_need, (uint64_t)na, n_first});
+    S.step_s += step_cost((uint64_t)na, n_first, n_first * S.c.bytes_per_expert, S.c, false);
+
+    // acceptance bookkeeping and per-sequence advance (specdec.cpp:330-362)
+    std::vector<int> ctoks((size_t)na * e.stride, 0), ctake(na, 0);
+    int total_take = 0;
+    for (int s = 0; s < na; ++s) {
+        const int b = act[s];
+        const int a = S.h_acc[s];
+        Outcome o{b, S.phase, a, S.h_corr[s], a + 1, {}};
+        for (int i = 0; i < g; ++i) o.drafts.push_back(S.h_drafts[(size_t)b * e.stride + i]);
+        S.tau_sum += (uint64_t)(a + 1);
+        ++S.tau_cnt;
+        const int take = std::min(a + 1, S.c.max_new_tokens - S.gen[b]);
+        for (int t = 0; t < take; ++t) {
+            const int tok = t < a ? o.drafts[t] : o.correction;
+            ctoks[(size_t)s * e.stride + t] = tok;
+            S.out.tokens[b].push_back(tok);
+        }
+        ctake[s] = take;
+        total_take += take;
+        S.gen[b] += take;
+        S.out.outcomes.push_back(std::move(o));
+        for (int i = 0; i <= g; ++i)
+            for (int m = 0; m < M; ++m)
+                for (int k = 0; k < K; ++k) {
+                    int key = m * E + vraw_at(s, i, m, k);
+                    S.pc[key]++;
+                    S.out.hotness[key]++;
+                }
+        if (S.c.collect_trace)
+            for (int i = 0; i <= g; ++i)
+                for (int m = 0; m < M; ++m) {
+                    TraceRow tr{S.phase, b, m, {}};
+                    for (int k = 0; k < K; ++k) tr.experts.push_back(vraw_at(s, i, m, k));
+                    S.out.trace.push_back(std::move(tr));
+                }
+    }
+    // rollback / advance of the device prefix state: only the taken tokens enter the running sums
+    e.upload_ints(e.commit_toks, ctoks.data(), ctoks.size());
+    e.upload_ints(e.commit_take, ctake.data(), na);
+    launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.commit_toks, e.stride, e.commit_take, na, e.d, e.stream);
+
+    if (S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
+        auto next = select_sets(SMOE_POLICY_HOT_TEMPORAL, S.pc, M, E, S.sets, S.nd, S.prng);
+        S.res->pin(next, S.led, 1, S.phase);
+        if (next != S.sets) S.sets_dirty = true;
+        S.sets = std::move(next);
+    }
+    std::fill(S.pc.begin(), S.pc.end(), 0);
+    S.res->flush();
+    ++S.phase;
+    if (accepted_tokens) *accepted_tokens = total_take;
+    return na;
+}
+
+RunOut spec_end(Engine& e) {
+    SpecState& S = *e.st;
+    RunOut& R = S.out;
+    S.timer.stop(e.stream, &R.gpu_s, &R.wall_s);
+    R.phases = S.phase;
+    R.tau_mean = S.tau_cnt ? (double)S.tau_sum / (double)S.tau_cnt : 1.0;
+    R.tokens_total = 0;
+    for (auto& t : R.tokens) R.tokens_total += t.size();
+    R.speculation_s = S.spec_s;
+    R.verification_s = S.ver_s;
+    R.modeled_seconds = S.spec_s + S.ver_s;
+    R.tokens_per_sec = R.modeled_seconds > 0.0 ? (double)R.tokens_total / R.modeled_seconds : 0.0;
+    R.bytes_spec = S.led.tot[0];
+    R.bytes_verify = S.led.tot[1];
+    R.bytes_baseline = S.led.tot[2];
+    R.bytes_total = S.led.total;
+    if (S.lam.empty()) {
+        R.lambda = 1.0;
+    } else {  // specdec.cpp:159-172
+        double vs = 0.0, ss = 0.0;
+        for (size_t i = 0; i < S.lam.size(); i += 4) {
+            vs += step_cost(S.lam[i], S.lam[i + 1], S.lam[i + 1] * S.c.bytes_per_expert, S.c, false);
+            ss += step_cost(S.lam[i + 2], S.lam[i + 3], S.lam[i + 3] * S.c.bytes_per_expert, S.c, false);
+        }
+        if (ss <= 0.0) throw Error(kInvariant, "measure_lambda: zero single-step latency");
+        R.lambda = vs / ss;
+    }
+    R.c_measured = (S.phase > 0 && S.step_s > 0.0)
+                       ? (S.spec_s / ((double)S.phase * S.g)) / (S.step_s / (double)S.phase)
+                       : 0.0;
+    R.ledger = S.led.e;
+    R.h2d_expert_bytes = e.h2d_bytes;
+    R.h2d_s = e.h2d_ms * 1e-3;
+    RunOut out = std::move(R);
+    e.st.reset();
+    return out;
+}
+
+RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts) {
+    spec_begin(e, c, prompts);
+    try {
+        while (spec_step(e, nullptr) > 0) {
+        }
+    } catch (...) {
+        e.st.reset();
+        throw;
+    }
+    return spec_end(e);
+}
+
+// baselines.cpp:29-99 (greedy, no pinned set, no overlap)
+RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts) {
+    const int plen = prompt_len_of(prompts);
+    const int B = (int)prompts.size();
+    if (c.gamma < 1) throw Error(kConfig, "spec: gamma >= 1 violated");
+    if (c.max_new_tokens < 1) throw Error(kConfig, "spec: max_new_tokens >= 1 violated");
+    if (c.warmup_steps < 1) throw Error(kConfig, "spec: warmup_steps >= 1 violated");
+    if (plen < 1) throw Error(kConfig, "spec: prompt_len >= 1 violated");
+    if (B < 1) throw Error(kConfig, "baseline run: no prompts");
+    if (B > e.Bmax) throw Error(kConfig, "engine: batch exceeds max_batch");
+    const int M = e.M, E = e.E, K = e.K;
+    tier_check(c, 0, M);
+    Residency res(M, E, c);
+    Ledger led;
+    RunOut R;
+    R.B = B; R.max_new = c.max_new_tokens; R.gamma = 0;
+    R.tokens.assign(B, {});
+    R.hotness.assign((size_t)M * E, 0);
+    e.reset_sequences(prompts);
+    std::vector<int> rs(B), one(B, 1), raw, am(B);
+    for (int b = 0; b < B; ++b) rs[b] = b;
+    e.upload_ints(e.row_seq, rs.data(), B);
+    e.upload_ints(e.seqs, rs.data(), B);
+    e.upload_ints(e.commit_take, one.data(), B);
+    Timer tm;
+    tm.start(e.stream);
+    double modeled = 0.0;
+    for (int step = 0; step < c.max_new_tokens; ++step) {
+        e.pass(B, e.row_seq, nullptr, 0, false, 0, 0);
+        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream);
+        read_log(e, e.raw_log, 0, B, raw);
+        SMOE_CUDA(cudaMemcpyAsync(am.data(), e.amax, sizeof(int) * B, cudaMemcpyDeviceToHost, e.stream));
+        e.sync();
+        e.check_flags();
+        std::vector<uint8_t> need((size_t)M * E, 0);
+        uint64_t n_need = 0;
+        for (int b = 0; b < B; ++b) {
+            for (int m = 0; m < M; ++m)
+                for (int k = 0; k < K; ++k) {
+                    int key = m * E + raw[((size_t)m * B + b) * K + k];
+                    if (!need[key]) { need[key] = 1; ++n_need; }
+                    R.hotness[key]++;
+                }
+            R.tokens[b].push_back(am[b]);
+            if (c.collect_trace)
+                for (int m = 0; m < M; ++m) {
+                    TraceRow tr{step, b, m, {}};
+                    for (int k = 0; k < K; ++k) tr.experts.push_back(raw[((size_t)m * B + b) * K + k]);
+                    R.trace.push_back(std::move(tr));
+                }
+        }
+        const uint64_t bytes = res.ensure(need, 2, step, led);
+        modeled += step_cost((uint64_t)B, n_need, bytes, c, false);
+        res.flush();
+    }
+    tm.stop(e.stream, &R.gpu_s, &R.wall_s);
+    R.phases = c.max_new_tokens;
+    R.tau_mean = 1.0;
+    R.tokens_total = (uint64_t)B * c.max_new_tokens;
+    R.modeled_seconds = modeled;
+    R.verification_s = modeled;
+    R.tokens_per_sec = modeled > 0.0 ? (double)R.tokens_total / modeled : 0.0;
+    R.bytes_spec = led.tot[0];
+    R.bytes_verify = led.tot[1];
+    R.bytes_baseline = led.tot[2];
+    R.bytes_total = led.total;
+    R.lambda = 1.0;
+    R.c_measured = 0.0;
+    R.ledger = led.e;
+    return R;
+}
+
+}  // namespace smoe

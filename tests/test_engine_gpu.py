@@ -1,0 +1,164 @@
+"""GPU parity tests: the sm_100a engine (through the C ABI) against the reference oracle.
+
+Bars:
+  * P1/P2 -- fp32 mode: routing indices (raw and post-remap), accepted counts, outcomes, greedy
+    tokens, ledger and the modeled metrics equal the float64 reference bit for bit; logits agree
+    within 2e-5 of the logit scale (fp32 vs fp64 arithmetic).
+  * P3 -- bf16 mode (tcgen05): losslessness (speculative == on-demand on the same engine, exact),
+    batch invariance, and tcgen05 vs CUDA-core GEMMs within bf16 tolerance.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2604_10152_b200.engine import BF16, F32, GEMM_SIMT, GEMM_TCGEN05, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
+from paper_2604_10152_b200.prompts import make_prompts
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+LOGIT_TOL = 2e-5  # fp32 engine vs float64 reference, relative to max |logit|
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name + ".json")) as f:
+        return json.load(f)
+
+
+def run_dict(r, drop=("wall_s", "gpu_s", "h2d_expert_bytes", "h2d_s")):
+    return {"tokens": r.tokens, "ledger": [list(x) for x in r.ledger],
+            "outcomes": [list(o[:5]) + [list(o[5])] for o in r.outcomes],
+            "trace": [[t[0], t[1], t[2], list(t[3])] for t in r.trace],
+            "hotness": r.hotness.tolist(),
+            "metrics": {k: v for k, v in r.metrics.items() if k not in drop}}
+
+
+def spec_of(d):
+    return ModelSpec(**{k: v for k, v in d.items() if k in ModelSpec.__dataclass_fields__})
+
+
+@pytest.fixture(scope="module")
+def toy_engines():
+    out = []
+    for g in gold("toy"):
+        e = Engine(spec_of(g["spec"]), weight_type=F32, max_batch=8, max_gamma=10).init_exact()
+        out.append((g, e))
+    yield out
+    for _, e in out:
+        e.close()
+
+
+def test_f32_forward_matches_reference(toy_engines):
+    g = gold("spec_forward")
+    e = Engine(spec_of(g["spec"]), weight_type=F32, max_batch=1, max_gamma=1).init_exact()
+    lg, raw, _ = e.forward(g["prefix"])
+    ref = np.asarray(g["logits"])
+    assert np.max(np.abs(lg - ref)) <= LOGIT_TOL * np.max(np.abs(ref))
+    assert raw.tolist() == g["raw"]
+    assert int(np.argmax(lg)) == int(np.argmax(ref))
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_f32_affinity_bitexact(toy_engines, i):
+    g, e = toy_engines[i]
+    assert e.affinity().tolist() == g["affinity"]
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_f32_specmoe_equals_reference(toy_engines, i):
+    """run_specmoe (specdec.cpp:190-397) on the GPU == the reference, field for field."""
+    g, e = toy_engines[i]
+    cfg = RunCfg(**g["cfg"])
+    got = run_dict(e.run_specmoe(cfg, g["prompts"]))
+    want = g["specmoe"]
+    for key in ("tokens", "outcomes", "trace", "ledger", "hotness", "metrics"):
+        assert got[key] == want[key], key
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_f32_ondemand_equals_reference(toy_engines, i):
+    g, e = toy_engines[i]
+    got = run_dict(e.run_ondemand(RunCfg(**g["cfg"]), g["prompts"]))
+    assert got == g["ondemand"]
+
+
+def test_f32_restricted_forward_remap_equals_oracle(toy_engines, port):
+    """Draft semantics (model.cpp:237-246): affinity and hash-surrogate remaps, exact."""
+    g, e = toy_engines[1]
+    m = port.build(spec_of(g["spec"]))
+    rng = np.random.RandomState(0)
+    for trial in range(12):
+        nd = [2, 3, 4, 8][trial % 4]
+        sets = [sorted(rng.choice(16, nd, replace=False).tolist()) for _ in range(4)]
+        prefix = rng.randint(0, 64, size=rng.randint(1, 12)).tolist()
+        for aff in (True, False):
+            lg, raw, fin = e.forward(prefix, sets, use_affinity=aff)
+            rl, rr, rf = m.forward(prefix, sets, use_affinity=aff)
+            assert raw.tolist() == rr.tolist() and fin.tolist() == rf.tolist()
+            assert np.max(np.abs(lg - rl)) <= LOGIT_TOL * np.max(np.abs(rl))
+
+
+def test_c1_f32_parity():
+    """BASELINE configs[0] (L4 E8 K2 d512): tokens / routing trace / ledger equal the reference."""
+    g = gold("c1")
+    e = Engine(spec_of(g["spec"]), weight_type=F32, max_batch=1, max_gamma=4).init_exact()
+    lg, raw, _ = e.forward(g["prompts"][0])
+    ref = np.asarray(g["forward_logits"])
+    assert np.max(np.abs(lg - ref)) <= LOGIT_TOL * np.max(np.abs(ref))
+    assert raw.tolist() == g["forward_raw"]
+    assert e.affinity().tolist() == g["affinity"]
+    got = run_dict(e.run_specmoe(RunCfg(**g["cfg"]), g["prompts"]))
+    for key in ("tokens", "outcomes", "trace", "ledger", "metrics"):
+        assert got[key] == g["specmoe"][key], key
+
+
+def test_f32_losslessness_many_seeds():
+    """SPEC.md:512 acceptance 1 on the GPU: spec == on-demand for N in {2,4,8,16}, gamma in {5,10}."""
+    for seed in range(6):
+        s = ModelSpec(num_layers=4, experts=16, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.5, seed=seed)
+        e = Engine(s, weight_type=F32, max_batch=2, max_gamma=10).init_exact()
+        prompts = make_prompts(seed, 2, 8, 64)
+        od = e.run_ondemand(RunCfg(max_new_tokens=20, run_seed=seed), prompts)
+        for nd, gm in [(2, 5), (4, 10), (8, 5), (16, 10)]:
+            sp = e.run_specmoe(RunCfg(gamma=gm, n_draft=nd, max_new_tokens=20, run_seed=seed), prompts)
+            assert sp.tokens == od.tokens
+            if nd == 16:
+                assert all(o[2] == gm for o in sp.outcomes)
+        e.close()
+
+
+# ---------------------------------------------------------------- bf16 / tcgen05
+def _c1_like(kind, skew=0.0):
+    return ModelSpec(num_layers=4, experts=8, top_k=2, hidden=512, ffn=1024, vocab=1024, gate_skew=skew, seed=1,
+                     expert_kind=kind)
+
+
+@pytest.mark.parametrize("kind", [TANH2, SWIGLU3])
+def test_tcgen05_matches_cuda_core_gemm(kind):
+    """Same bf16 weights through the tcgen05 path and the CUDA-core path: logits within bf16 noise."""
+    s = _c1_like(kind)
+    a = Engine(s, weight_type=BF16, gemm=GEMM_TCGEN05, max_batch=4, max_gamma=4).init_device(7)
+    b = Engine(s, weight_type=BF16, gemm=GEMM_SIMT, max_batch=4, max_gamma=4).init_device(7)
+    for prefix in ([1, 2, 3], list(range(40)), [1000] * 9):
+        la, ra, _ = a.forward(prefix)
+        lb, rb, _ = b.forward(prefix)
+        scale = np.max(np.abs(lb))
+        assert np.max(np.abs(la - lb)) <= 3e-2 * scale, (np.max(np.abs(la - lb)), scale)
+        assert np.mean(ra == rb) >= 0.75
+
+
+@pytest.mark.parametrize("kind", [TANH2, SWIGLU3])
+def test_bf16_lossless_and_batch_invariant(kind):
+    """P3: on the tcgen05 engine, speculative output == on-demand output exactly, and every
+    sequence's output is independent of the batch it runs in."""
+    s = _c1_like(kind, skew=1.0)
+    e = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4).init_device(3)
+    e.build_affinity_device()
+    prompts = make_prompts(5, 4, 8, s.vocab)
+    od = e.run_ondemand(RunCfg(gamma=4, max_new_tokens=24), prompts)
+    sp = e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=24), prompts)
+    assert sp.tokens == od.tokens
+    one = e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=24), prompts[2:3])
+    assert one.tokens[0] == sp.tokens[2]
+    assert sp.metrics["bytes_spec"] == 0
