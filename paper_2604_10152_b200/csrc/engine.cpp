@@ -107,11 +107,11 @@ Engine::Engine(const smoe_engine_config& c) {
     for (int l = 0, k = 0; l < L; ++l)
         if (!mask[l]) dense_slot[l] = M * E + k++;
     slot_of = dalloc<int>((size_t)M * E);
-    SMOE_CUDA(cudaMemcpy(slot_of, h_slot_of.data(), sizeof(int) * M * E, cudaMemcpyHostToDevice));
+    h2d(slot_of, h_slot_of.data(), sizeof(int) * M * E);
     std::vector<float> bias((size_t)M * E);
     for (int m = 0; m < M; ++m)
         for (int e = 0; e < E; ++e) bias[(size_t)m * E + e] = (float)(skew * (1.0 - (double)e / E));  // model.cpp:128-130
-    SMOE_CUDA(cudaMemcpy(gate_b, bias.data(), sizeof(float) * bias.size(), cudaMemcpyHostToDevice));
+    h2d(gate_b, bias.data(), sizeof(float) * bias.size());
 
     seq_sum = dalloc<double>((size_t)Bmax * d);
     seq_len = dalloc<int>(Bmax);
@@ -155,6 +155,7 @@ Engine::Engine(const smoe_engine_config& c) {
     op_xa = {xa, (long long)Tmax, d};
     op_xperm = {xperm, (long long)Tmax * K, d};
     op_h = {hbuf, (long long)Tmax * K, f};
+    SMOE_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets above vs. the non-blocking engine stream
 }
 
 Engine::~Engine() {
@@ -180,11 +181,20 @@ uint64_t Engine::real_bytes_per_expert() const {
 
 void Engine::sync() { SMOE_CUDA(cudaStreamSynchronize(stream)); }
 
+// Host->device copy ordered on the engine stream.  (A plain cudaMemcpy from pageable memory may
+// return before its DMA lands and is not ordered with a non-blocking stream.)
+void Engine::h2d(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    SMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    sync();
+}
+
 void Engine::check_flags() {
     int h = 0;
     SMOE_CUDA(cudaMemcpy(&h, flags, sizeof(int), cudaMemcpyDeviceToHost));
     if (h) {
-        SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
+        SMOE_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+        sync();
         if (h & kFlagNonFiniteLogits) throw Error(kInvariant, "greedy_next: non-finite logits");
         if (h & kFlagNonFiniteGate) throw Error(kInvariant, "softmax: non-finite input");
         if (h & kFlagEmptyRemap) throw Error(kInvariant, "nearest_draft_expert: empty candidate set");
@@ -216,7 +226,7 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
             scratch64_n = (size_t)cnt;
             scratch64 = dalloc<double>(scratch64_n);
         }
-        SMOE_CUDA(cudaMemcpy(scratch64, src, sizeof(double) * cnt, cudaMemcpyHostToDevice));
+        h2d(scratch64, src, sizeof(double) * cnt);
         return scratch64;
     };
     const size_t ws = wt == kF32 ? 4 : 2;
@@ -231,7 +241,7 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     };
     if (name == "embedding") {
         need((long long)V * d);
-        SMOE_CUDA(cudaMemcpy(emb64, src, sizeof(double) * n, cudaMemcpyHostToDevice));
+        h2d(emb64, src, sizeof(double) * n);
     } else if (name == "head") {
         need((long long)d * V);
         launch_convert_transpose(stage(n), d, V, head, wt, stream);
@@ -390,7 +400,7 @@ void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_dra
             std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * n_draft);
         }
     }
-    SMOE_CUDA(cudaMemcpy(in_draft, ind.data(), ind.size(), cudaMemcpyHostToDevice));
+    h2d(in_draft, ind.data(), ind.size());
     upload_ints(draft_sorted, sorted.data(), sorted.size());
     upload_ints(rank, rk.data(), rk.size());
     cur_n_draft = n_draft;

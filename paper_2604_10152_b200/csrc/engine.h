@@ -175,6 +175,7 @@ public:
     // ---- host<->device helpers
     void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream
     void sync();
+    void h2d(void* dst, const void* src, size_t bytes);
     void check_flags();
 
     // ---- public ops
