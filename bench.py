@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""bench.py -- accepted decode tokens/s of the self-assisted speculative-decoding loop on B200.
+
+Default workload (BASELINE.json configs[1], the metric's config): Mixtral-8x7B shape
+(L32 E8 K2 d4096 f14336 V32000, SwiGLU experts, bf16 weights, random init), all experts
+HBM-resident, batch 32, gamma 4, N 4 draft experts, hot_temporal + affinity, greedy.
+A "step" = one speculative phase over the batch: gamma restricted draft passes, one batched verify
+pass over B*(gamma+1) positions, accept/rollback, hotness + re-pin + ledger.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--shape c1|c2|c4] [--batch B]
+
+N > 1 (torchrun): one replica per GPU with independent sequences (weak scaling); time = max over
+ranks, value = tokens of all ranks / that time.  --impl reference times the reference's own CPU
+implementation (oracle/_ref, compiled from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "accepted decode tokens/sec, Mixtral-8x7B shape, batch 1-64; expert bytes/token"
+SHAPES = {
+    "c1": dict(num_layers=4, experts=8, top_k=2, hidden=512, ffn=1024, vocab=1024),
+    "c2": dict(num_layers=32, experts=8, top_k=2, hidden=4096, ffn=14336, vocab=32000),
+    "c4": dict(num_layers=28, experts=64, top_k=6, hidden=2048, ffn=1408, vocab=102400, moe_mask=[0] + [1] * 27),
+}
+SHAPE_NAMES = {"c1": "tiny synthetic MoE (C1)", "c2": "Mixtral-8x7B shape (C2)", "c4": "fine-grained E64 K6 (C4)"}
+
+
+def args_parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--shape", default="c2", choices=sorted(SHAPES))
+    p.add_argument("--expert", default="swiglu3", choices=["swiglu3", "tanh2"])
+    p.add_argument("--batch", type=int, default=32)
+    p.add_argument("--gamma", type=int, default=4)
+    p.add_argument("--n-draft", type=int, default=4)
+    p.add_argument("--e2e-tokens", type=int, default=12)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- clocks (B200_PROFILING.md)
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.proc, self.path = dev, None, f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU reference (oracle/_ref)
+def forward_macs(s: dict, n_layers: int, mats: int) -> float:
+    """Multiply-adds of one reference forward() (model.cpp:192-263) with n_layers MoE layers."""
+    d, f, E, K, V = s["hidden"], s["ffn"], s["experts"], s["top_k"], s["vocab"]
+    return n_layers * (d * d + d * E + K * mats * d * f) + d * V
+
+
+def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: int) -> dict:
+    """Time the reference's own CPU path on a bounded sample of the workload.
+
+    Sample: a one-MoE-layer slice of the shape (full d, f, E, K, V), built by the reference's
+    build_model; `threads` host threads run forward() concurrently on the shared weights; tau comes
+    from one reference run_specmoe phase on the slice.  forward() is a per-layer loop, so its time is
+    extrapolated to the full depth (and from the reference's 2-matrix expert to SwiGLU's 3) by its
+    multiply-add count.  tokens/s = forwards/s * tau / (2*gamma + 1)."""
+    from oracle.oracle import LIBS, ModelSpec as OSpec, Oracle, RunCfg as ORun
+    from paper_2604_10152_b200.prompts import make_prompts
+    kind = "ref" if os.path.exists(LIBS["ref"]) else "port"
+    full = dict(SHAPES[shape])
+    full.pop("moe_mask", None)
+    slice_spec = dict(full, num_layers=1, seed=0)
+    o = Oracle(kind)
+    t0 = time.time()
+    m = o.build(OSpec(**slice_spec))
+    build_s = time.time() - t0
+    prompt = make_prompts(0, 1, 8, full["vocab"])
+    t1 = m.time_forward(prompt[0], threads=1, iters=1)
+    tp = m.time_forward(prompt[0], threads=threads, iters=1)
+    sp = m.run_specmoe(ORun(gamma=gamma, n_draft=min(n_draft, full["experts"]), max_new_tokens=gamma + 1,
+                            run_seed=0), prompt)
+    tau = sp.metrics["tau_mean"]
+    mats = 3 if expert == "swiglu3" else 2
+    n_moe = SHAPES[shape]["num_layers"] if "moe_mask" not in SHAPES[shape] else sum(SHAPES[shape]["moe_mask"])
+    scale = forward_macs(full, SHAPES[shape]["num_layers"], mats) / forward_macs(full, 1, 2)
+    fwd_s_full = tp * scale  # wall of one forward per thread, full depth
+    value = threads * tau / ((2 * gamma + 1) * fwd_s_full)
+    return {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference" if kind == "ref" else "port",
+            "sample": (f"{kind} build of a 1-MoE-layer slice of {SHAPE_NAMES[shape]} (tanh2, fp64); "
+                       f"{threads} threads x 1 forward() = {tp:.3f}s (1 thread {t1:.3f}s); tau {tau:.3f} from one "
+                       f"reference run_specmoe phase (gamma {gamma}); extrapolated x{scale:.1f} by forward MACs "
+                       f"to L={n_moe} {expert}; slice build {build_s:.0f}s untimed"),
+            "tau": tau, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale}
+
+
+# ---------------------------------------------------------------- the B200 arm
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def ncu_traffic():
+    """dram bytes per expert-GEMM launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_expert_gemm.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_b200(a) -> None:
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2604_10152_b200.engine import BF16, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+
+    shp = dict(SHAPES[a.shape])
+    spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
+    eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local)
+    eng.init_device(0)
+    eng.build_affinity_device()
+    prompts = make_prompts(1000 + rank, a.batch, 8, spec.vocab)
+    cfg = RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30, run_seed=rank)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+
+    eng.spec_begin(cfg, prompts)
+    for _ in range(a.warmup):
+        eng.spec_step()
+    eng.counters(reset=True)
+    eng.profile_reset()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    tokens = 0
+    for _ in range(a.steps):
+        t, _act = eng.spec_step()
+        tokens += t
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    cnt = eng.counters(reset=True)
+    prof = eng.profile_read("expert_gemm")
+    dense = eng.profile_read("dense_gemm")
+    head = eng.profile_read("head_gemm")
+    res = eng.spec_end()
+    if world > 1:
+        t = torch.tensor([ms, float(tokens)], device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms, tokens = float(mx[0].item()), int(t[1].item())
+
+    # ---- e2e through the public API (host prompts in, host tokens out; per-phase H2D/D2H inside)
+    eng.counters(reset=True)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    r2 = eng.run_specmoe(RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=a.e2e_tokens, run_seed=rank),
+                         prompts)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - w0
+    c2 = eng.counters()
+    e2e_tokens = r2.metrics["tokens_total"]
+    if world > 1:
+        t = torch.tensor([e2e_s, float(e2e_tokens)], device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_s, e2e_tokens = float(mx[0].item()), int(t[1].item())
+    phases2 = max(1, r2.metrics["phases"])
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    pk = peaks()
+    achieved = cnt["alg_expert_bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init N(0,1/sqrt(d)) weights, synthetic prompts)",
+        "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert} experts HBM-resident, B={a.batch}/GPU, "
+                               f"gamma={a.gamma}, N={a.n_draft}, hot_temporal+affinity, greedy",
+                   "model": f"{a.shape} L{spec.num_layers} E{spec.experts} K{spec.top_k} d{spec.hidden} f{spec.ffn} "
+                            f"V{spec.vocab}",
+                   "global_batch": a.batch * world, "seq_len": 8, "parallelism": f"replicas{world}",
+                   "l2": "inputs larger than L2: every verify pass streams all touched expert weights "
+                         "(>= 10 GB) from HBM"},
+        "tau": res.metrics["tau_mean"],
+        "expert_bytes_per_token": {
+            "hbm": cnt["alg_expert_bytes"] * world / max(1, tokens),
+            "pcie": 0, "pcie_note": "HBM-resident config: no migration (see C3 offload)",
+            "ledger_reference_units": res.metrics["bytes_total"] / max(1, res.metrics["tokens_total"])},
+        "e2e": {"value": e2e_tokens / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(c2["ctl_h2d"] / phases2), "d2h_bytes_per_step": int(c2["ctl_d2h"] / phases2),
+                "note": f"run_specmoe via the C ABI, {a.e2e_tokens} new tokens per sequence, host prompts in / host "
+                        f"tokens out, per-phase control copies inside"},
+        "gpu_launches": int(cnt["launches"]),
+        "roofline": {"bound": "hbm", "kernel": "k_gemm_tc (tcgen05 grouped expert GEMM)", "achieved": achieved,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "traffic": ncu_traffic(), "launches": prof["launches"],
+                     "avg_launch_ms": prof["ms"] / max(1, prof["launches"]),
+                     "share_of_step": prof["ms"] / ms if ms else None,
+                     "algorithmic_bytes": "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
+        "breakdown_ms": {"expert_gemm": prof["ms"], "dense_gemm": dense["ms"], "head_gemm": head["ms"], "step_total": ms},
+        "clocks": clocks,
+    }
+    if not a.no_cpu_baseline and world == 1:
+        thr = a.cpu_threads or os.cpu_count()
+        try:
+            line["cpu_baseline"] = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr)
+        except Exception as ex:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(a) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    thr = a.cpu_threads or os.cpu_count()
+    steps = []
+    cb = None
+    for _ in range(max(1, a.steps if a.steps <= 2 else 2)):
+        cb = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr)
+        steps.append(cb["value"])
+    value = statistics.median(steps)
+    cb = dict(cb, value=value)
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": world,
+            "steps": len(steps), "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference build_model seeded weights, synthetic prompts)",
+            "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert}, gamma={a.gamma}, N={a.n_draft}, "
+                                   f"reference CPU path (oracle/_ref) on {thr} host threads",
+                       "global_batch": thr, "seq_len": 8, "parallelism": f"cpu{thr}"},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = args_parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

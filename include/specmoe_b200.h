@@ -114,6 +114,12 @@ int smoe_spec_begin(smoe_engine* e, const smoe_run_config* cfg, const int* promp
 int smoe_spec_step(smoe_engine* e, int* tokens_accepted_out, int* active_out);
 int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
 
+/* Counters since the last reset: hot-path kernel launches, algorithmic HBM bytes of the expert GEMMs
+ * (distinct experts touched per pass x bytes per expert) and of the dense GEMMs, and control-path
+ * host<->device bytes (rows, accepted counts, routing logs). */
+int smoe_counters(smoe_engine* e, uint64_t* launches, double* alg_expert_bytes, double* alg_dense_bytes,
+                  uint64_t* ctl_h2d, uint64_t* ctl_d2h, int reset);
+
 /* Kernel timing hooks for bench.py: events recorded around the dominant kernel class. */
 int smoe_profile_reset(smoe_engine* e);
 int smoe_profile_read(smoe_engine* e, const char* kernel_class, double* total_ms, long long* launches,

@@ -170,6 +170,8 @@ class Oracle:
         L.om_nearest_draft_expert.argtypes = [dp, C.c_int, C.c_int, ip, C.c_int, ip, C.c_int]
         L.om_select_draft_experts.argtypes = [C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_int, ip, C.c_int,
                                               C.c_uint64, ip]
+        L.om_time_forward.restype = C.c_double
+        L.om_time_forward.argtypes = [vp, ip, C.c_int, C.c_int, C.c_int]
         L.om_skewness.restype = C.c_double
         L.om_skewness.argtypes = [C.POINTER(C.c_uint64), C.c_int, C.c_int, C.c_uint64, C.c_double]
 
@@ -245,6 +247,14 @@ class OracleModel:
         if rc:
             raise OracleError(rc, err.value.decode())
         return logits, raw.reshape(sp.moe_layers, sp.top_k), fin.reshape(sp.moe_layers, sp.top_k)
+
+    def time_forward(self, prefix, threads: int = 1, iters: int = 1) -> float:
+        """Wall seconds for `threads` concurrent threads x `iters` forward() calls each."""
+        p, pp = _iarr(prefix)
+        t = self.o.lib.om_time_forward(self.h, pp, len(p), threads, iters)
+        if t < 0:
+            raise OracleError(2, "time_forward failed")
+        return t
 
     # ---------------------------------------------------------------- loops
     def _cfg(self, cfg: RunCfg) -> OmRunCfg:

@@ -91,6 +91,10 @@ om_result* om_run_ondemand(void* model, const om_run_cfg* cfg, const int* prompt
                            char* err, int errlen);
 void om_free_result(om_result* r);
 
+/* CPU-baseline timing (bench.py): `threads` host threads each run `iters` forward() calls on the
+ * shared read-only weights.  Returns wall seconds, or < 0 on error. */
+double om_time_forward(void* model, const int* prefix, int n, int threads, int iters);
+
 /* Host primitives (SPEC KATs). */
 int om_route_topk(const double* logits, int n, int k, int* out);
 int om_greedy_next(const double* logits, int n);

@@ -12,6 +12,7 @@
 #include <exception>
 #include <set>
 #include <span>
+#include <thread>
 #include <vector>
 
 #include "oracle_abi.h"
@@ -227,6 +228,23 @@ om_result* om_run_ondemand(void* model, const om_run_cfg* c, const int* prompts,
     } catch (const std::exception& e) {
         report(e, err, errlen);
         return nullptr;
+    }
+}
+
+double om_time_forward(void* model, const int* prefix, int n, int threads, int iters) {
+    try {
+        const ModelWeights& w = *static_cast<ModelWeights*>(model);
+        std::span<const int> p(prefix, (size_t)n);
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int i = 0; i < threads; ++i)
+            th.emplace_back([&] {
+                for (int it = 0; it < iters; ++it) (void)forward(w, p);
+            });
+        for (auto& t : th) t.join();
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    } catch (const std::exception&) {
+        return -1.0;
     }
 }
 

@@ -17,6 +17,7 @@
 #include "oracle_abi.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <setjmp.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -978,6 +979,26 @@ om_result* om_run_ondemand(void* model, const om_run_cfg* cfg, const int* prompt
     om_result* r = run_ondemand_((omodel*)model, cfg, prompts, B, plen);
     LEAVE();
     return r;
+}
+
+/* ------------------------------------------------------------------ CPU-baseline timing */
+typedef struct { omodel* m; const int* p; int n, iters; } fwd_job;
+static void* fwd_worker(void* arg) {
+    fwd_job* j = (fwd_job*)arg;
+    double* lg = (double*)malloc(sizeof(double) * (size_t)j->m->V);
+    char err[64];
+    for (int i = 0; i < j->iters; ++i) om_forward(j->m, j->p, j->n, NULL, 0, NULL, lg, NULL, NULL, err, 64);
+    free(lg);
+    return NULL;
+}
+double om_time_forward(void* model, const int* prefix, int n, int threads, int iters) {
+    fwd_job job = {(omodel*)model, prefix, n, iters};
+    pthread_t th[256];
+    if (threads > 256) threads = 256;
+    double t0 = now_s();
+    for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, fwd_worker, &job);
+    for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+    return now_s() - t0;
 }
 
 /* ------------------------------------------------------------------ host primitives */

@@ -207,6 +207,22 @@ int smoe_spec_end(smoe_engine* h, smoe_run_result** out) {
     });
 }
 
+int smoe_counters(smoe_engine* h, uint64_t* launches, double* alg_expert_bytes, double* alg_dense_bytes,
+                  uint64_t* ctl_h2d, uint64_t* ctl_d2h, int reset) {
+    return guarded([&] {
+        auto& e = *h->e;
+        if (launches) *launches = e.launches;
+        if (alg_expert_bytes) *alg_expert_bytes = e.alg_expert_bytes;
+        if (alg_dense_bytes) *alg_dense_bytes = e.alg_dense_bytes;
+        if (ctl_h2d) *ctl_h2d = e.ctl_h2d;
+        if (ctl_d2h) *ctl_d2h = e.ctl_d2h;
+        if (reset) {
+            e.launches = e.ctl_h2d = e.ctl_d2h = 0;
+            e.alg_expert_bytes = e.alg_dense_bytes = 0;
+        }
+    });
+}
+
 int smoe_profile_reset(smoe_engine* h) {
     return guarded([&] {
         h->e->prof_collect();

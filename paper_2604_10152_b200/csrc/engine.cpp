@@ -211,6 +211,7 @@ void Engine::upload_ints(int* dst, const int* src, size_t n) {
         SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
     }
     std::memcpy(h_small, src, n * sizeof(int));
+    ctl_h2d += n * sizeof(int);
     SMOE_CUDA(cudaMemcpyAsync(dst, h_small, n * sizeof(int), cudaMemcpyHostToDevice, stream));
     SMOE_CUDA(cudaStreamSynchronize(stream));
 }
@@ -498,6 +499,8 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
          (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
+    launches += 4 + (uint64_t)M * 8 + (uint64_t)n_dense * 6;
+    alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
 }
 
 void Engine::reset_sequences(const std::vector<std::vector<int>>& prompts) {

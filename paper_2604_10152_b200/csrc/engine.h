@@ -183,6 +183,10 @@ public:
                      float* logits_out, int* raw_out, int* fin_out);
     void reset_sequences(const std::vector<std::vector<int>>& prompts);
 
+    // ---- counters (bench.py): kernel launches, algorithmic HBM bytes, control-path PCIe bytes
+    uint64_t launches = 0, ctl_h2d = 0, ctl_d2h = 0;
+    double alg_expert_bytes = 0, alg_dense_bytes = 0;
+
     // ---- store (offload)
     uint64_t real_bytes_per_expert() const;
     uint64_t h2d_bytes = 0;

@@ -348,6 +348,22 @@ int spec_step(Engine& e, int* accepted_tokens) {
     for (int t = 0; t < g; ++t) read_log(e, e.fin_log, t, na, dfin[t]);
     e.sync();
     e.check_flags();
+    e.launches += (uint64_t)g + 2;  // scatters + accept (commit counted below)
+    e.ctl_d2h += sizeof(int) * ((size_t)2 * na + (size_t)e.Bmax * e.stride + (size_t)M * K * (TV + (size_t)g * na));
+    {  // algorithmic expert bytes: every distinct (layer, expert) a pass touches streams its weights once
+        const double bpe = (double)e.real_bytes_per_expert();
+        for (int t = 0; t < g; ++t)
+            for (int m = 0; m < M; ++m) {
+                uint64_t seen = 0;
+                for (int q = 0; q < na * K; ++q) seen |= 1ull << dfin[t][(size_t)m * na * K + q];
+                e.alg_expert_bytes += bpe * __builtin_popcountll(seen);
+            }
+        for (int m = 0; m < M; ++m) {
+            uint64_t seen = 0;
+            for (int q = 0; q < TV * K; ++q) seen |= 1ull << S.vraw[(size_t)m * TV * K + q];
+            e.alg_expert_bytes += bpe * __builtin_popcountll(seen);
+        }
+    }
 
     // modeled speculation time (specdec.cpp:282-288)
     for (int t = 0; t < g; ++t) {
@@ -419,6 +435,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
     e.upload_ints(e.commit_toks, ctoks.data(), ctoks.size());
     e.upload_ints(e.commit_take, ctake.data(), na);
     launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.commit_toks, e.stride, e.commit_take, na, e.d, e.stream);
+    e.launches += 1;
 
     if (S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
         auto next = select_sets(SMOE_POLICY_HOT_TEMPORAL, S.pc, M, E, S.sets, S.nd, S.prng);

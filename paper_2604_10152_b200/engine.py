@@ -27,8 +27,8 @@ PHASES = {0: "speculation", 1: "verification", 2: "baseline-step"}
 EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe_engine_info", "smoe_engine_stream",
            "smoe_init_weights_exact", "smoe_init_weights_device", "smoe_upload_tensor", "smoe_set_affinity",
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
-           "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_profile_reset",
-           "smoe_profile_read"]
+           "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters",
+           "smoe_profile_reset", "smoe_profile_read"]
 
 
 class EngineError(RuntimeError):
@@ -116,6 +116,8 @@ def lib():
     L.smoe_spec_begin.argtypes = [vp, C.POINTER(RunConfig), ip, C.c_int, C.c_int]
     L.smoe_spec_step.argtypes = [vp, ip, ip]
     L.smoe_spec_end.argtypes = [vp, C.POINTER(C.POINTER(RunResultC))]
+    L.smoe_counters.argtypes = [vp, C.POINTER(C.c_uint64), dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                C.c_int]
     L.smoe_profile_reset.argtypes = [vp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
     _LIB = L
@@ -328,6 +330,14 @@ class Engine:
         out = C.POINTER(RunResultC)()
         _check(lib().smoe_spec_end(self.h, C.byref(out)))
         return _collect(out)
+
+    def counters(self, reset: bool = False) -> dict:
+        la, h2d, d2h = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        eb, db = C.c_double(), C.c_double()
+        _check(lib().smoe_counters(self.h, C.byref(la), C.byref(eb), C.byref(db), C.byref(h2d), C.byref(d2h),
+                                   int(reset)))
+        return {"launches": la.value, "alg_expert_bytes": eb.value, "alg_dense_bytes": db.value,
+                "ctl_h2d": h2d.value, "ctl_d2h": d2h.value}
 
     def profile_reset(self):
         _check(lib().smoe_profile_reset(self.h))
