@@ -120,6 +120,12 @@ int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
 int smoe_counters(smoe_engine* e, uint64_t* launches, double* alg_expert_bytes, double* alg_dense_bytes,
                   uint64_t* ctl_h2d, uint64_t* ctl_d2h, int reset);
 
+/* Expert GEMMs timed alone (bench.py roofline): T tokens routed round-robin over every expert of
+ * MoE layer 0; average CUDA-event ms per up (w1/w3 or up) and down launch, and the algorithmic bytes
+ * each launch must move (weights of touched experts + activations). */
+int smoe_bench_expert_gemm(smoe_engine* e, int T, int iters, double* up_ms, double* down_ms, double* bytes_up,
+                           double* bytes_down);
+
 /* Kernel timing hooks for bench.py: events recorded around the dominant kernel class. */
 int smoe_profile_reset(smoe_engine* e);
 int smoe_profile_read(smoe_engine* e, const char* kernel_class, double* total_ms, long long* launches,

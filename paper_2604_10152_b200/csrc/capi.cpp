@@ -223,6 +223,11 @@ int smoe_counters(smoe_engine* h, uint64_t* launches, double* alg_expert_bytes, 
     });
 }
 
+int smoe_bench_expert_gemm(smoe_engine* h, int T, int iters, double* up_ms, double* down_ms, double* bytes_up,
+                           double* bytes_down) {
+    return guarded([&] { h->e->bench_expert_gemm(T, iters, up_ms, down_ms, bytes_up, bytes_down); });
+}
+
 int smoe_profile_reset(smoe_engine* h) {
     return guarded([&] {
         h->e->prof_collect();

@@ -132,7 +132,19 @@ Engine::Engine(const smoe_engine_config& c) {
     group_slot = dalloc<int>(E);
     xperm = dalloc_bytes((size_t)Tmax * K * d * ws);
     hbuf = dalloc_bytes((size_t)Tmax * K * f * ws);
-    ybuf = dalloc<float>((size_t)Tmax * K * d);
+    // split-K counts are fixed per GEMM shape (never T-dependent) so results stay batch invariant
+    if (use_tc) {
+        const int nkb_d = (d + 63) / 64, nkb_f = (f + 63) / 64;
+        auto pick = [](int nkb, int want) {  // effective split count: ceil(nkb / ceil(nkb / want))
+            want = std::max(1, std::min(want, nkb));
+            const int per = (nkb + want - 1) / want;
+            return (nkb + per - 1) / per;
+        };
+        s_mix = pick(nkb_d, std::max(1, 296 / std::max(1, (d + 127) / 128)));
+        s_down = pick(nkb_f, 4);
+    }
+    ybuf = dalloc<float>((size_t)s_down * Tmax * K * d);
+    pmix = dalloc<float>((size_t)s_mix * Tmax * d);
     logits = dalloc<float>((size_t)Tmax * V);
     amax = dalloc<int>(Tmax);
     in_draft = dalloc<uint8_t>((size_t)M * E);
@@ -145,6 +157,8 @@ Engine::Engine(const smoe_engine_config& c) {
     seqs = dalloc<int>(Bmax);
     flags = dalloc<int>(1);
     SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
+    sched = dalloc<int>(2);
+    SMOE_CUDA(cudaMemset(sched, 0, 2 * sizeof(int)));
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
@@ -163,9 +177,9 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
-    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf);
+    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
-    fr(commit_take); fr(seqs); fr(flags); fr(scratch64);
+    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
     if (host_up) cudaFreeHost(host_up);
     if (host_down) cudaFreeHost(host_down);
@@ -258,11 +272,13 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
         launch_convert(stage(n), n, gate_b + (size_t)moe_ord[layer] * E, kF32, stream);
     } else if (name == "up" || name == "w1") {
         need((long long)d * f);
-        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream);
+        // SwiGLU: w1 feature j -> pool row 2j, w3 feature j -> row 2j+1 (one 128-row tile = 64 features)
+        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream,
+                                 kind == kSwiglu3 ? 2 : 1, 0);
     } else if (name == "w3") {
         need((long long)d * f);
         if (kind != kSwiglu3) throw Error(kConfig, "upload_tensor: w3 needs the swiglu3 expert kind");
-        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d + (size_t)f * d), wt, stream);
+        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream, 2, 1);
     } else if (name == "down" || name == "w2") {
         need((long long)f * d);
         launch_convert_transpose(stage(n), f, d, at(down_pool, (size_t)slot_for() * d * f), wt, stream);
@@ -442,14 +458,17 @@ void Engine::prof_collect() {
 // ------------------------------------------------------------------ GEMM dispatch
 void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, long long a_rows_per_slot, int Nout,
                   int Kd, const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
-                  const void* X, const TcOperand& bmap, void* Y, int ldy, Epi epi, const char* cls, double bytes) {
+                  const void* X, const TcOperand& bmap, void* Y, int ldy, Epi epi, const char* cls, double bytes,
+                  int splits, long long split_stride) {
     cudaEvent_t ev;
     prof_begin(cls, &ev);
     if (use_tc) {
+        if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
         TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound,
-                     Y, ldy, epi};
+                     Y, ldy, epi, splits, split_stride, sched};
         launch_gemm_tc(a, stream);
     } else {
+        if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");
         GemmArgs a{W, slot_stride, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound, X, Y, ldy, epi};
         launch_gemm_simt(a, wt, stream);
     }
@@ -463,44 +482,85 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     if (T <= 0) return;
     if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
     const size_t ws = wt == kF32 ? 4 : 2;
-    launch_x0(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, stream);
+    const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)Tmax * K * d;
+    // K1+K2: x0 and the first rms
+    launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
+                  stream);
     const double wbytes_dd = (double)d * d * ws;
+    const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
+    const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     for (int l = 0; l < L; ++l) {
-        launch_rms(x, T, d, xa, wt, stream);
-        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, T, l, T, xa, op_xa, x, d, kEpiResidAdd,
-             "dense_gemm", wbytes_dd);
+        // K3: a = Mix rms(x) as split-K partials; the residual add happens in the next kernel
+        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, T, l, T, xa, op_xa, pmix, d, kEpiStoreF32,
+             "dense_gemm", wbytes_dd, s_mix, pm_stride);
         const int mo = moe_ord[l];
-        const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
         if (mo >= 0) {
             int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
             int* fl = fin_log + ((size_t)log_slot * M + mo) * Tmax * K;
-            GateArgs g{x, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E, xa, wt, rl, fl, wgt,
-                       restricted ? in_draft + (size_t)mo * E : nullptr, draft_sorted + (size_t)mo * E,
+            GateArgs g{x, pmix, s_mix, pm_stride, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E, xa,
+                       wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr, draft_sorted + (size_t)mo * E,
                        rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft, use_aff, mo, row_plen, flags};
-            launch_gate(g, stream);
+            launch_gate(g, stream);  // x += a; K4/K5 on rms(x); xa = rms(x)
             launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
             launch_gather(xa, pos, T, K, d, xperm, wt, stream);
             gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf,
-                 f, kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh, "expert_gemm", ebytes_up);
-            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf,
-                 d, kEpiStoreF32, "expert_gemm", ebytes_dn);
-            launch_combine(x, ybuf, pos, wgt, T, K, d, 0, stream);
+                 f, up_epi, "expert_gemm", ebytes_up);
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
+                 kEpiStoreF32, "expert_gemm", ebytes_dn, s_down, yd_stride);
+            // K9 combine + residual + the next layer's (or the head's) rms
+            launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
         } else {
-            launch_rms(x, T, d, xa, wt, stream);
-            gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, T, dense_slot[l], T, xa, op_xa,
-                 hbuf, f, kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh, "dense_gemm", ebytes_up);
+            launch_resid_rms(x, pmix, s_mix, pm_stride, T, d, xa, wt, stream);
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, T, dense_slot[l], T, xa, op_xa, hbuf,
+                 f, up_epi, "dense_gemm", ebytes_up);
             gemm(down_pool, (long long)d * f, op_down, d, d, f, nullptr, nullptr, 1, T, dense_slot[l], T, hbuf, op_h,
-                 ybuf, d, kEpiStoreF32, "dense_gemm", ebytes_dn);
-            launch_combine(x, ybuf, nullptr, nullptr, T, 1, d, 1, stream);
+                 ybuf, d, kEpiStoreF32, "dense_gemm", ebytes_dn, s_down, yd_stride);
+            launch_combine_rms(x, ybuf, s_down, yd_stride, nullptr, nullptr, T, 1, d, 1, xa, wt, stream);
         }
     }
-    launch_rms(x, T, d, xa, wt, stream);
     gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32, "head_gemm",
          (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
-    launches += 4 + (uint64_t)M * 8 + (uint64_t)n_dense * 6;
+    launches += 3 + (uint64_t)M * 7 + (uint64_t)n_dense * 5;
     alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
+}
+
+// Kernel timed alone: T tokens routed round-robin over all E experts of MoE layer 0 (every expert
+// touched), up-projection then down-projection, `iters` times each with CUDA events.
+void Engine::bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms, double* bytes_up, double* bytes_down) {
+    if (T > Tmax) throw Error(kConfig, "bench_expert_gemm: T exceeds max_batch*(max_gamma+1)");
+    std::vector<int> fin((size_t)T * K);
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < K; ++k) fin[(size_t)t * K + k] = (t * K + k) % E;
+    upload_ints(fin_log, fin.data(), fin.size());
+    launch_route(fin_log, T, K, E, slot_of, group_off, group_slot, pos, stream);
+    const long long yd_stride = (long long)Tmax * K * d;
+    const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
+    cudaEvent_t a, b, c;
+    SMOE_CUDA(cudaEventCreate(&a)); SMOE_CUDA(cudaEventCreate(&b)); SMOE_CUDA(cudaEventCreate(&c));
+    float t_up = 0, t_dn = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // pass 0 = warm-up
+        SMOE_CUDA(cudaEventRecord(a, stream));
+        for (int i = 0; i < iters; ++i)
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf, f,
+                 up_epi, "bench", 0);
+        SMOE_CUDA(cudaEventRecord(b, stream));
+        for (int i = 0; i < iters; ++i)
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
+                 kEpiStoreF32, "bench", 0, s_down, yd_stride);
+        SMOE_CUDA(cudaEventRecord(c, stream));
+        SMOE_CUDA(cudaEventSynchronize(c));
+        SMOE_CUDA(cudaEventElapsedTime(&t_up, a, b));
+        SMOE_CUDA(cudaEventElapsedTime(&t_dn, b, c));
+    }
+    cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
+    const size_t ws = wt == kF32 ? 4 : 2;
+    const int touched = std::min(E, T * K);
+    *up_ms = t_up / iters;
+    *down_ms = t_dn / iters;
+    *bytes_up = (double)touched * U * d * ws + (double)T * K * (d + f) * ws;
+    *bytes_down = (double)touched * d * f * ws + (double)T * K * (f * ws + (double)d * 4 * s_down);
 }
 
 void Engine::reset_sequences(const std::vector<std::vector<int>>& prompts) {

@@ -33,6 +33,9 @@ struct TcGemmArgs {
     void* Y;
     int ldy;
     Epi epi;
+    int splits;               // K splits (kEpiStoreF32 only): partial ks written at Y + ks*split_stride
+    long long split_stride;
+    int* sched;               // device [2] zero-initialised work counter (self-resetting)
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
 
@@ -124,7 +127,9 @@ public:
     int *pos = nullptr, *group_off = nullptr, *group_slot = nullptr;
     void* xperm = nullptr;  // [Tmax*K][d]
     void* hbuf = nullptr;   // [Tmax*K][f]
-    float* ybuf = nullptr;  // [Tmax*K][d]
+    float* ybuf = nullptr;  // [s_down][Tmax*K][d] split-K partials of the down projection
+    float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
+    int s_mix = 1, s_down = 1;
     float* logits = nullptr;  // [Tmax][V]
     int* amax = nullptr;
     uint8_t* in_draft = nullptr;  // [M][E]
@@ -136,6 +141,7 @@ public:
     int* commit_take = nullptr;  // [Bmax]
     int* seqs = nullptr;         // [Bmax]
     int* flags = nullptr;
+    int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
     size_t scratch64_n = 0;
     // pinned host staging
@@ -170,7 +176,8 @@ public:
               int log_slot);
     void gemm(const void* W, long long slot_stride, const TcOperand& aop, long long a_rows_per_slot, int Nout, int Kd,
               const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
-              const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes);
+              const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes,
+              int splits = 1, long long split_stride = 0);
 
     // ---- host<->device helpers
     void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream
@@ -182,6 +189,9 @@ public:
     void forward_one(const std::vector<int>& prefix, const int* restricted, int n_draft, int use_aff,
                      float* logits_out, int* raw_out, int* fin_out);
     void reset_sequences(const std::vector<std::vector<int>>& prompts);
+
+    // isolated expert-GEMM microbenchmark (bench.py roofline, kernel timed alone)
+    void bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms, double* bytes_up, double* bytes_down);
 
     // ---- counters (bench.py): kernel launches, algorithmic HBM bytes, control-path PCIe bytes
     uint64_t launches = 0, ctl_h2d = 0, ctl_d2h = 0;

@@ -77,14 +77,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_gemm_simt(GemmArgs a) {
                 const int n = n0 + i;
                 if (n >= a.Nout) break;
                 float wv[VEC];
-                load_vec<T>(Wb + (long long)n * K + k, wv);
+                load_vec<T>(Wb + (long long)(kGated ? 2 * n : n) * K + k, wv);
 #pragma unroll
                 for (int j = 0; j < kTok; ++j)
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[i][j] += wv[v] * xv[j][v];
-                if (kGated) {
+                if (kGated) {  // SwiGLU slot rows are interleaved: 2n = w1, 2n+1 = w3
                     float w3[VEC];
-                    load_vec<T>(Wb + (long long)(n + a.Nout) * K + k, w3);
+                    load_vec<T>(Wb + (long long)(2 * n + 1) * K + k, w3);
 #pragma unroll
                     for (int j = 0; j < kTok; ++j)
 #pragma unroll

@@ -67,38 +67,122 @@ __global__ void k_rms(const float* __restrict__ x, int d, void* __restrict__ xa)
     for (int i = threadIdx.x; i < d; i += blockDim.x) store_op<OT>(xa, (long long)blockIdx.x * d + i, xr[i] * inv);
 }
 
+// Row kernels below keep one row in shared memory (d floats) and use float4 accesses (d % 4 == 0).
+template <typename OT>
+__device__ __forceinline__ void store_row_op(void* xa, long long base, const float* row, int d, float inv) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) store_op<OT>(xa, base + i, row[i] * inv);
+}
+
+template <typename OT>
+__global__ void k_x0_rms(const double* __restrict__ emb, const double* __restrict__ ssum, const int* __restrict__ slen,
+                         const int* __restrict__ pend, int pstride, const int* __restrict__ row_seq,
+                         const int* __restrict__ row_extra, int extra_u, int d, float* __restrict__ x,
+                         int* __restrict__ row_plen, void* __restrict__ xa) {
+    extern __shared__ float row[];
+    __shared__ float red[33];
+    const int r = blockIdx.x;
+    const int b = row_seq[r];
+    const int e = row_extra ? row_extra[r] : extra_u;
+    const int n = slen[b] + e;
+    const int* toks = pend + (long long)b * pstride;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        double acc = ssum[(long long)b * d + i];
+        for (int j = 0; j < e; ++j) acc += emb[(long long)toks[j] * d + i];
+        const float v = (float)(acc / (double)n);
+        x[(long long)r * d + i] = v;
+        row[i] = v;
+        ss += v * v;
+    }
+    if (threadIdx.x == 0) row_plen[r] = n;
+    ss = block_sum(ss, red);
+    store_row_op<OT>(xa, (long long)r * d, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
+}
+
+template <typename OT>
+__global__ void k_resid_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride, int d,
+                            void* __restrict__ xa) {
+    extern __shared__ float row[];
+    __shared__ float red[33];
+    const long long base = (long long)blockIdx.x * d;
+    float ss = 0.f;
+    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
+        float4 v = *reinterpret_cast<const float4*>(x + base + i4);
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < S; ++s) {
+            const float4 p = *reinterpret_cast<const float4*>(P + s * pstride + base + i4);
+            a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
+        }
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+        *reinterpret_cast<float4*>(x + base + i4) = v;
+        *reinterpret_cast<float4*>(row + i4) = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = block_sum(ss, red);
+    store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
+}
+
 // ------------------------------------------------------------------ K4/K5 gate + remap
 template <typename OT>
 __global__ void k_gate(GateArgs a) {
-    extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[33]
+    extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[8*32 + 33]
     float* xf = sm;
     float* gl = xf + a.d;
     float* red = gl + 2 * a.E;
     const int r = blockIdx.x, d = a.d, E = a.E, K = a.K;
-    const float* xr = a.x + (long long)r * d;
+    const long long base = (long long)r * d;
+    // residual add of the mix GEMM's split-K partials (model.cpp:224), then rms (model.cpp:226)
     float ss = 0.f;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        float v = xr[i];
-        xf[i] = v;
-        ss += v * v;
+    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
+        float4 v = *reinterpret_cast<const float4*>(a.x + base + i4);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < a.s_mix; ++s) {
+            const float4 q = *reinterpret_cast<const float4*>(a.pmix + s * a.pstride + base + i4);
+            acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+        }
+        v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
+        *reinterpret_cast<float4*>(a.x + base + i4) = v;
+        *reinterpret_cast<float4*>(xf + i4) = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
     }
-    ss = block_sum(ss, red);
+    ss = block_sum(ss, red + 8 * 32);
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        float v = xf[i] * inv;
+        const float v = xf[i] * inv;
         xf[i] = v;
-        store_op<OT>(a.xa, (long long)r * d + i, v);
+        store_op<OT>(a.xa, base + i, v);
     }
     __syncthreads();
+    // gate GEMV (model.cpp:229-230): 8 experts at a time, fixed-order block reduction
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int e = w; e < E; e += nw) {
-        const float* gw = a.gate_w + (long long)e * d;
-        float acc = 0.f;
-        for (int i = lane; i < d; i += 32) acc += gw[i] * xf[i];
-        acc = warp_sum(acc);
-        if (lane == 0) gl[e] = acc + a.gate_b[e];
+    for (int e0 = 0; e0 < E; e0 += 8) {
+        const int ne = min(8, E - e0);
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(xf + i4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < ne) {
+                    const float4 g = *reinterpret_cast<const float4*>(a.gate_w + (long long)(e0 + j) * d + i4);
+                    acc[j] += g.x * xv.x + g.y * xv.y + g.z * xv.z + g.w * xv.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float v = warp_sum(acc[j]);
+            if (lane == 0) red[w * 8 + j] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < ne) {
+            float t = 0.f;
+            for (int q = 0; q < nw; ++q) t += red[q * 8 + threadIdx.x];
+            gl[e0 + threadIdx.x] = t + a.gate_b[e0 + threadIdx.x];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (threadIdx.x != 0) return;
     // softmax (model.cpp:145-157), max-subtracted
     float mx = gl[0];
@@ -214,20 +298,40 @@ __global__ void k_gather(const uint4* __restrict__ xa, const int* __restrict__ p
     for (int i = threadIdx.x; i < vecs; i += blockDim.x) dst[i] = src[i];
 }
 
-// ------------------------------------------------------------------ K9 combine
-__global__ void k_combine(float* __restrict__ x, const float* __restrict__ y, const int* __restrict__ pos,
-                          const float* __restrict__ wgt, int K, int d, int dense) {
+// ------------------------------------------------------------------ K9 combine (+ next rms)
+template <typename OT>
+__global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
+                              const int* __restrict__ pos, const float* __restrict__ wgt, int K, int d, int dense,
+                              void* __restrict__ xa) {
+    extern __shared__ float row[];
+    __shared__ float red[33];
     const int t = blockIdx.x;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        float acc;
-        if (dense) {
-            acc = y[(long long)t * d + i];
-        } else {
-            acc = 0.f;
-            for (int k = 0; k < K; ++k) acc += wgt[t * K + k] * y[(long long)pos[t * K + k] * d + i];
+    const long long base = (long long)t * d;
+    float ss = 0.f;
+    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < (dense ? 1 : K); ++k) {
+            const long long src = (dense ? (long long)t : (long long)pos[t * K + k]) * d + i4;
+            float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s = 0; s < S; ++s) {
+                const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src);
+                y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
+            }
+            if (dense) {
+                acc = y;
+            } else {
+                const float wk = wgt[t * K + k];
+                acc.x += wk * y.x; acc.y += wk * y.y; acc.z += wk * y.z; acc.w += wk * y.w;
+            }
         }
-        x[(long long)t * d + i] += acc;
+        float4 v = *reinterpret_cast<const float4*>(x + base + i4);
+        v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
+        *reinterpret_cast<float4*>(x + base + i4) = v;
+        *reinterpret_cast<float4*>(row + i4) = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
     }
+    ss = block_sum(ss, red);
+    store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
 }
 
 // ------------------------------------------------------------------ K10 argmax
@@ -314,7 +418,8 @@ __global__ void k_fill_normal_f64(double* dst, long long n, double sd, uint64_t 
 }
 
 template <typename T>
-__global__ void k_convert_transpose(const double* __restrict__ src, int rows, int cols, T* __restrict__ dst) {
+__global__ void k_convert_transpose(const double* __restrict__ src, int rows, int cols, T* __restrict__ dst, int mul,
+                                    int off) {
     __shared__ double tile[32][33];
     int c = blockIdx.x * 32 + threadIdx.x;
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -325,7 +430,7 @@ __global__ void k_convert_transpose(const double* __restrict__ src, int rows, in
     int r = blockIdx.y * 32 + threadIdx.x;
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         int cc = blockIdx.x * 32 + j;
-        if (r < rows && cc < cols) dst[(long long)cc * rows + r] = from_f<T>((float)tile[threadIdx.x][j]);
+        if (r < rows && cc < cols) dst[((long long)cc * mul + off) * rows + r] = from_f<T>((float)tile[threadIdx.x][j]);
     }
 }
 template <typename T>
@@ -372,6 +477,29 @@ void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, c
                            row_plen);
 }
 
+static int row_threads(int d) { return d >= 4096 ? 512 : 256; }
+
+void launch_x0_rms(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
+                   const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
+                   void* xa, WType op, cudaStream_t s) {
+    if (T <= 0) return;
+    const size_t sm = sizeof(float) * d;
+    if (op == kF32)
+        k_x0_rms<float><<<T, row_threads(d), sm, s>>>(emb64, seq_sum, seq_len, pend, pend_stride, row_seq, row_extra,
+                                                      extra_uniform, d, x, row_plen, xa);
+    else
+        k_x0_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(emb64, seq_sum, seq_len, pend, pend_stride, row_seq,
+                                                              row_extra, extra_uniform, d, x, row_plen, xa);
+}
+
+void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T, int d, void* xa, WType op,
+                      cudaStream_t s) {
+    if (T <= 0) return;
+    const size_t sm = sizeof(float) * d;
+    if (op == kF32) k_resid_rms<float><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, d, xa);
+    else k_resid_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, d, xa);
+}
+
 void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s) {
     if (T <= 0) return;
     if (op == kF32) k_rms<float><<<T, 256, 0, s>>>(x, d, xa);
@@ -380,7 +508,7 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 
 void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
-    size_t smem = sizeof(float) * (a.d + 2 * a.E + 33);
+    size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
     if (a.op == kF32) k_gate<float><<<a.T, 256, smem, s>>>(a);
     else k_gate<__nv_bfloat16><<<a.T, 256, smem, s>>>(a);
 }
@@ -401,10 +529,14 @@ void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xp
     k_gather<<<T * K, 128, 0, s>>>(reinterpret_cast<const uint4*>(xa), pos, K, vecs, reinterpret_cast<uint4*>(xperm));
 }
 
-void launch_combine(float* x, const float* y, const int* pos, const float* wgt, int T, int K, int d, int dense,
-                    cudaStream_t s) {
+void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
+                        int K, int d, int dense, void* xa, WType op, cudaStream_t s) {
     if (T <= 0) return;
-    k_combine<<<T, 256, 0, s>>>(x, y, pos, wgt, K, d, dense);
+    const size_t sm = sizeof(float) * d;
+    if (op == kF32)
+        k_combine_rms<float><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, pos, wgt, K, d, dense, xa);
+    else
+        k_combine_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, pos, wgt, K, d, dense, xa);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
@@ -444,10 +576,11 @@ void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t se
     k_fill_normal_f64<<<grid, 256, 0, s>>>(dst, n, stddev, seed, tensor_id);
 }
 
-void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s) {
+void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s, int mul,
+                              int off) {
     dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32)), block(32, 8);
-    if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst);
-    else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst);
+    if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst, mul, off);
+    else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst, mul, off);
 }
 void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s) {
     int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);

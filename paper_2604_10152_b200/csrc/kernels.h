@@ -15,14 +15,27 @@ void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, c
                const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
                cudaStream_t s);
 
+// K1 + K2 fused: the first layer's rms (model.cpp:19-26) of x0 -> xa (operand type).
+void launch_x0_rms(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
+                   const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
+                   void* xa, WType op, cudaStream_t s);
+
 // K2 (model.cpp:19-26): xa[r] = x[r] * (mean(x^2) + 1e-12)^-1/2 in the operand type.
 void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s);
+
+// Residual add of a split-K GEMM followed by rms (dense layers, model.cpp:222-226):
+//   x[t] += sum_s P[s][t] (s in order);  xa[t] = rms(x[t]).
+void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T, int d, void* xa, WType op,
+                      cudaStream_t s);
 
 // K4+K5 (model.cpp:229-246, drafting.cpp:123-151): fused rms + gate GEMV + bias + softmax +
 // top-K + (restricted) remap.  Writes the normalised row (operand type) for the experts, raw/final
 // picks [T][K] and the combine weight p[raw] [T][K].
 struct GateArgs {
-    const float* x;
+    float* x;                 // residual stream; the mix partials are added first (x += sum_s pmix[s])
+    const float* pmix;
+    int s_mix;
+    long long pstride;
     int T, d, E, K;
     const float* gate_w;  // [E][d]
     const float* gate_b;  // [E]
@@ -52,9 +65,10 @@ void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaS
 // xperm[pos[t*K+k]] = xa[t]
 void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s);
 
-// K9 (model.cpp:248-257): x[t] += sum_k wgt[t,k] * y[pos[t,k]] (k in order); dense: x[t] += y[t].
-void launch_combine(float* x, const float* y, const int* pos, const float* wgt, int T, int K, int d, int dense,
-                    cudaStream_t s);
+// K9 (model.cpp:248-257) + the next rms: y_k = sum_s P[s][pos[t,k]] (split-K partials, s in order),
+// x[t] += sum_k wgt[t,k] * y_k (k in order; dense: x[t] += y), then xa[t] = rms(x[t]).
+void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
+                        int K, int d, int dense, void* xa, WType op, cudaStream_t s);
 
 // K10 (model.cpp:172-176): per-row argmax, first max wins; non-finite -> flag.
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s);
@@ -74,7 +88,7 @@ void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int
 // Grouped skinny GEMM on CUDA cores (f32 or bf16 weights, f32 accumulation):
 //   for group g with slot s = group_slot[g] >= 0 and rows [group_off[g], group_off[g+1]):
 //     acc[r][n] = sum_k W[s][n][k] * X[r][k]       (n < Nout)
-//   epilogue per Epi.  For kEpiSwiglu, W[s] has 2*Nout rows: [0,Nout) w1, [Nout,2Nout) w3.
+//   epilogue per Epi.  For kEpiSwiglu, W[s] has 2*Nout rows, interleaved: 2n = w1, 2n+1 = w3.
 struct GemmArgs {
     const void* W;
     long long slot_stride;  // elements between slots
@@ -96,8 +110,10 @@ void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t
                         cudaStream_t s);
 void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
                             cudaStream_t s);
-// dst[c][r] = (T)src[r][c] for a rows x cols float64 source (reference row-major -> K-major).
-void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s);
+// dst[c*mul+off][r] = (T)src[r][c] for a rows x cols float64 source (reference row-major -> K-major;
+// mul=2 interleaves the SwiGLU w1/w3 rows).
+void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s,
+                              int mul = 1, int off = 0);
 void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s);
 void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
 

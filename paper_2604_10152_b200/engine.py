@@ -27,7 +27,7 @@ PHASES = {0: "speculation", 1: "verification", 2: "baseline-step"}
 EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe_engine_info", "smoe_engine_stream",
            "smoe_init_weights_exact", "smoe_init_weights_device", "smoe_upload_tensor", "smoe_set_affinity",
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
-           "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters",
+           "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters", "smoe_bench_expert_gemm",
            "smoe_profile_reset", "smoe_profile_read"]
 
 
@@ -118,6 +118,7 @@ def lib():
     L.smoe_spec_end.argtypes = [vp, C.POINTER(C.POINTER(RunResultC))]
     L.smoe_counters.argtypes = [vp, C.POINTER(C.c_uint64), dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.c_int]
+    L.smoe_bench_expert_gemm.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp, dp]
     L.smoe_profile_reset.argtypes = [vp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
     _LIB = L
@@ -338,6 +339,13 @@ class Engine:
                                    int(reset)))
         return {"launches": la.value, "alg_expert_bytes": eb.value, "alg_dense_bytes": db.value,
                 "ctl_h2d": h2d.value, "ctl_d2h": d2h.value}
+
+    def bench_expert_gemm(self, T: int, iters: int = 10) -> dict:
+        u, d, bu, bd = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().smoe_bench_expert_gemm(self.h, T, iters, C.byref(u), C.byref(d), C.byref(bu), C.byref(bd)))
+        return {"up_ms": u.value, "down_ms": d.value, "up_bytes": bu.value, "down_bytes": bd.value,
+                "up_GBps": bu.value / (u.value * 1e-3) / 1e9 if u.value else 0.0,
+                "down_GBps": bd.value / (d.value * 1e-3) / 1e9 if d.value else 0.0}
 
     def profile_reset(self):
         _check(lib().smoe_profile_reset(self.h))
