@@ -79,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity)
             : "memory");
         if (done) return;
-        if (clock64() - t0 > 20000000000ll) __trap();
+        if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s
     }
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
@@ -154,15 +154,21 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
     return w.kb0 < w.kb1;
 }
 
-// Consumer side of the unit ring: returns false when the producer published "done".
+// Consumer side of the unit ring: returns false when the producer published "done".  whole_warp:
+// all 32 lanes call this (epilogue warps; lane 0 releases the slot after the warp has read it);
+// otherwise a single lane (the MMA issuer) calls it and releases the slot itself.
 __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full, uint64_t* ring_empty, const int* ring,
-                                          int& cons, bool arrive, Unit& w) {
+                                          int& cons, bool whole_warp, Unit& w) {
     const int r = cons % kRing;
     mbar_wait(&ring_full[r], (uint32_t)((cons / kRing) & 1));
     const int u = ring[r];
     ++cons;
-    __syncwarp();
-    if (arrive) mbar_arrive(&ring_empty[r]);
+    if (whole_warp) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&ring_empty[r]);
+    } else {
+        mbar_arrive(&ring_empty[r]);
+    }
     if (u < 0) return false;
     decode_unit(p, u, w);
     return true;
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
             Unit w;
-            while (next_unit(p, ring_full, ring_empty, ring, cons, true, w)) {
+            while (next_unit(p, ring_full, ring_empty, ring, cons, false, w)) {
                 const int acc = cnt & 1;
                 mbar_wait(&acc_empty[acc], (uint32_t)(((cnt >> 1) & 1) ^ 1));
                 tc_fence_after();
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         int cnt = 0, cons = 0;
         Unit w;
-        while (next_unit(p, ring_full, ring_empty, ring, cons, lane == 0, w)) {
+        while (next_unit(p, ring_full, ring_empty, ring, cons, true, w)) {
             const int acc = cnt & 1;
             mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
             tc_fence_after();
