@@ -93,7 +93,12 @@ Engine::Engine(const smoe_engine_config& c) {
     SMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
 
     const size_t ws = wt == kF32 ? 4 : 2;
-    n_slots = M * E + n_dense;
+    int exp_slots = M * E;
+    if (offload) {
+        exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * E, M * 4 + E);
+        if (exp_slots < E) throw Error(kConfig, "engine: hbm_expert_slots must be >= experts_per_block");
+    }
+    n_slots = exp_slots + n_dense;
     emb64 = dalloc<double>((size_t)V * d);
     mix = dalloc_bytes((size_t)L * d * d * ws);
     gate_w = dalloc<float>((size_t)M * E * d);
@@ -105,8 +110,13 @@ Engine::Engine(const smoe_engine_config& c) {
     for (int i = 0; i < M * E; ++i) h_slot_of[i] = i;
     dense_slot.assign(L, -1);
     for (int l = 0, k = 0; l < L; ++l)
-        if (!mask[l]) dense_slot[l] = M * E + k++;
+        if (!mask[l]) dense_slot[l] = exp_slots + k++;
     slot_of = dalloc<int>((size_t)M * E);
+    if (offload) {
+        stage_up = dalloc_bytes((size_t)U * d * ws);
+        stage_down = dalloc_bytes((size_t)d * f * ws);
+        store_alloc(exp_slots);  // everything starts in host DRAM; slot_of = -1
+    }
     h2d(slot_of, h_slot_of.data(), sizeof(int) * M * E);
     std::vector<float> bias((size_t)M * E);
     for (int m = 0; m < M; ++m)
@@ -181,6 +191,9 @@ Engine::~Engine() {
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
+    if (h_store) cudaFreeHost(h_store);
+    fr(stage_up); fr(stage_down);
+    for (auto& p : h2d_ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     if (host_up) cudaFreeHost(host_up);
     if (host_down) cudaFreeHost(host_down);
     for (auto& kv : prof)
@@ -246,13 +259,32 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     };
     const size_t ws = wt == kF32 ? 4 : 2;
     auto at = [&](void* base, size_t elems) { return static_cast<char*>(base) + elems * ws; };
+    // Destination of an expert matrix: its HBM slot, or (offload) a device staging buffer that is
+    // read-modified-written against the key's region of the pinned host pool.
+    int off_key = -1;
     auto slot_for = [&]() -> int {
         if (layer < 0 || layer >= L) throw Error(kConfig, "upload_tensor: layer out of range");
         if (mask[layer]) {
             if (expert < 0 || expert >= E) throw Error(kConfig, "upload_tensor: expert out of range");
+            if (offload) {
+                off_key = moe_ord[layer] * E + expert;
+                return -1;
+            }
             return h_slot_of[(size_t)moe_ord[layer] * E + expert];
         }
         return dense_slot[layer];
+    };
+    auto up_dst = [&]() -> void* {
+        const int sl = slot_for();
+        if (sl >= 0) return at(up_pool, (size_t)sl * U * d);
+        SMOE_CUDA(cudaMemcpyAsync(stage_up, static_cast<char*>(host_up) + (size_t)off_key * U * d * ws, (size_t)U * d * ws,
+                                  cudaMemcpyHostToDevice, stream));
+        return stage_up;
+    };
+    auto down_dst = [&]() -> void* {
+        const int sl = slot_for();
+        if (sl >= 0) return at(down_pool, (size_t)sl * d * f);
+        return stage_down;
     };
     if (name == "embedding") {
         need((long long)V * d);
@@ -273,19 +305,24 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     } else if (name == "up" || name == "w1") {
         need((long long)d * f);
         // SwiGLU: w1 feature j -> pool row 2j, w3 feature j -> row 2j+1 (one 128-row tile = 64 features)
-        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream,
-                                 kind == kSwiglu3 ? 2 : 1, 0);
+        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, kind == kSwiglu3 ? 2 : 1, 0);
     } else if (name == "w3") {
         need((long long)d * f);
         if (kind != kSwiglu3) throw Error(kConfig, "upload_tensor: w3 needs the swiglu3 expert kind");
-        launch_convert_transpose(stage(n), d, f, at(up_pool, (size_t)slot_for() * U * d), wt, stream, 2, 1);
+        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, 2, 1);
     } else if (name == "down" || name == "w2") {
         need((long long)f * d);
-        launch_convert_transpose(stage(n), f, d, at(down_pool, (size_t)slot_for() * d * f), wt, stream);
+        launch_convert_transpose(stage(n), f, d, down_dst(), wt, stream);
     } else {
         throw Error(kConfig, "upload_tensor: unknown tensor " + name);
     }
     SMOE_CUDA(cudaGetLastError());
+    if (off_key >= 0) {  // write the converted expert matrix back to the pinned host pool
+        const bool is_down = name == "down" || name == "w2";
+        const size_t bytes = is_down ? (size_t)d * f * ws : (size_t)U * d * ws;
+        void* host = static_cast<char*>(is_down ? host_down : host_up) + (size_t)off_key * bytes;
+        SMOE_CUDA(cudaMemcpyAsync(host, is_down ? stage_down : stage_up, bytes, cudaMemcpyDeviceToHost, stream));
+    }
     sync();
 }
 
@@ -349,8 +386,31 @@ void Engine::init_device(uint64_t s) {
     launch_fill_normal_f64(emb64, (long long)V * d, sd, s, tid++, stream);
     launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
     launch_fill_normal(gate_w, kF32, (long long)M * E * d, sd, s, tid++, stream);
-    launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid++, stream);
-    launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid++, stream);
+    const uint64_t tid_up = tid++, tid_down = tid++;
+    if (!offload) {
+        launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid_up, stream);
+        launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid_down, stream);
+    } else {
+        // identical values to the HBM-resident layout (element index = key*U*d + j), staged per expert
+        const size_t ws = wt == kF32 ? 4 : 2;
+        for (int key = 0; key < M * E; ++key) {
+            launch_fill_normal(stage_up, wt, (long long)U * d, sd, s, tid_up, stream, (long long)key * U * d);
+            launch_fill_normal(stage_down, wt, (long long)d * f, sd, s, tid_down, stream, (long long)key * d * f);
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_up) + (size_t)key * U * d * ws, stage_up,
+                                      (size_t)U * d * ws, cudaMemcpyDeviceToHost, stream));
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_down) + (size_t)key * d * f * ws, stage_down,
+                                      (size_t)d * f * ws, cudaMemcpyDeviceToHost, stream));
+        }
+        for (int l = 0, k = 0; l < L; ++l)
+            if (!mask[l]) {
+                const long long gi = (long long)(M * E + k);
+                launch_fill_normal(static_cast<char*>(up_pool) + (size_t)dense_slot[l] * U * d * ws, wt, (long long)U * d,
+                                   sd, s, tid_up, stream, gi * U * d);
+                launch_fill_normal(static_cast<char*>(down_pool) + (size_t)dense_slot[l] * d * f * ws, wt,
+                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f);
+                ++k;
+            }
+    }
     launch_fill_normal(head, wt, (long long)V * d, sd, s, tid++, stream);
     SMOE_CUDA(cudaGetLastError());
     sync();
@@ -368,9 +428,18 @@ void Engine::build_affinity_device() {
     affinity.assign((size_t)M * E * E, 0.0);
     std::vector<double> part(need);
     const size_t ws = wt == kF32 ? 4 : 2;
+    if (offload) store_reset();
+    std::vector<int> ident(E);
+    for (int e = 0; e < E; ++e) ident[e] = e;
     for (int m = 0; m < M; ++m) {
         SMOE_CUDA(cudaMemsetAsync(scratch64, 0, need * sizeof(double), stream));
         const int* slots = slot_of + (size_t)m * E;
+        if (offload) {  // bring the layer's experts into slots 0..E-1 for the pairwise pass
+            for (int e = 0; e < E; ++e) store_copy_in(m * E + e, e);
+            SMOE_CUDA(cudaStreamSynchronize(copy_stream));
+            upload_ints(group_slot, ident.data(), E);
+            slots = group_slot;
+        }
         launch_pairwise_sqdist(up_pool, wt, (long long)U * d, (long long)U * d, slots, E, scratch64, stream);
         launch_pairwise_sqdist(down_pool, wt, (long long)d * f, (long long)d * f, slots, E, scratch64, stream);
         (void)ws;
@@ -384,6 +453,7 @@ void Engine::build_affinity_device() {
                 D[(size_t)i * E + j] = D[(size_t)j * E + i] = std::sqrt(s);
             }
     }
+    if (offload) h2d_bytes = 0;
     have_affinity = true;
 }
 
@@ -502,11 +572,14 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                        rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft, use_aff, mo, row_plen, flags};
             launch_gate(g, stream);  // x += a; K4/K5 on rms(x); xa = rms(x)
             launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
+            const bool fetch = offload && !restricted;
+            if (fetch) store_fetch_layer(mo, T, rl);  // expert store: migrate this layer's missing experts
             launch_gather(xa, pos, T, K, d, xperm, wt, stream);
             gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf,
                  f, up_epi, "expert_gemm", ebytes_up);
             gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
                  kEpiStoreF32, "expert_gemm", ebytes_dn, s_down, yd_stride);
+            if (fetch) store_finish_layer(mo);
             // K9 combine + residual + the next layer's (or the head's) rms
             launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
         } else {
@@ -529,6 +602,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
 // Kernel timed alone: T tokens routed round-robin over all E experts of MoE layer 0 (every expert
 // touched), up-projection then down-projection, `iters` times each with CUDA events.
 void Engine::bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms, double* bytes_up, double* bytes_down) {
+    if (offload) throw Error(kConfig, "bench_expert_gemm: HBM-resident engines only");
     if (T > Tmax) throw Error(kConfig, "bench_expert_gemm: T exceeds max_batch*(max_gamma+1)");
     std::vector<int> fin((size_t)T * K);
     for (int t = 0; t < T; ++t)
@@ -595,6 +669,9 @@ void Engine::forward_one(const std::vector<int>& prefix, const int* restricted, 
         std::vector<std::vector<int>> sets(M);
         for (int m = 0; m < M; ++m) sets[m].assign(restricted + (size_t)m * n_draft, restricted + (size_t)(m + 1) * n_draft);
         set_draft_sets(sets, n_draft);
+        store_pin_sets(sets);
+    } else if (offload) {
+        store_reset();
     }
     reset_sequences({prefix});
     int zero = 0;

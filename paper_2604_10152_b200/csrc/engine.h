@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -110,9 +111,31 @@ public:
     std::vector<double> affinity;  // [M][E][E]
     bool have_affinity = false;
 
-    // ---- expert store (offload mode): pinned host pools, slots
+    // ---- expert store (offload mode, store.cpp): pinned host pools, HBM slot pool
     void* host_up = nullptr;    // [M*E][U][d] pinned
     void* host_down = nullptr;  // [M*E][d][f] pinned
+    void* stage_up = nullptr;   // device staging of one expert (offload init)
+    void* stage_down = nullptr;
+    int n_exp_slots = 0;
+    std::vector<int> slot_key;       // slot -> key (moe_layer*E + expert) or -1
+    std::vector<uint8_t> key_pinned;
+    std::vector<int> free_slots;
+    int* h_store = nullptr;          // pinned: slot_of mirror [M*E], group sizes, group slots, raw picks
+    int store_last_T = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev;
+    // hot_temporal re-pin decided per layer during a verify pass: (layer, raw picks [T][K], T) -> next set
+    std::function<bool(int, const int*, int, std::vector<int>&)> repin_hook;
+    void store_alloc(int exp_slots);
+    void store_reset();
+    void upload_slot_rows(int m0, int m1);
+    size_t expert_bytes(int which) const;
+    void store_copy_in(int key, int slot);
+    int store_take_slot(int key);
+    void store_release(int key);
+    void store_pin_sets(const std::vector<std::vector<int>>& sets);
+    void store_fetch_layer(int mo, int T, const int* raw_dev);
+    void store_finish_layer(int mo);
+    void collect_h2d();
 
     // ---- per-sequence state / buffers (device)
     double* seq_sum = nullptr;  // [Bmax][d]

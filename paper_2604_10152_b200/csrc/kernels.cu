@@ -408,9 +408,9 @@ __device__ __forceinline__ double normal_at(uint64_t seed, uint64_t tid, long lo
 }
 
 template <typename T>
-__global__ void k_fill_normal(T* dst, long long n, double sd, uint64_t seed, uint64_t tid) {
+__global__ void k_fill_normal(T* dst, long long n, double sd, uint64_t seed, uint64_t tid, long long idx0) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        dst[i] = from_f<T>((float)(sd * normal_at(seed, tid, i)));
+        dst[i] = from_f<T>((float)(sd * normal_at(seed, tid, idx0 + i)));
 }
 __global__ void k_fill_normal_f64(double* dst, long long n, double sd, uint64_t seed, uint64_t tid) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -563,11 +563,11 @@ void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int
 }
 
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
-                        cudaStream_t s) {
+                        cudaStream_t s, long long index0) {
     int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
     if (grid <= 0) return;
-    if (t == kF32) k_fill_normal<float><<<grid, 256, 0, s>>>((float*)dst, n, stddev, seed, tensor_id);
-    else k_fill_normal<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst, n, stddev, seed, tensor_id);
+    if (t == kF32) k_fill_normal<float><<<grid, 256, 0, s>>>((float*)dst, n, stddev, seed, tensor_id, index0);
+    else k_fill_normal<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst, n, stddev, seed, tensor_id, index0);
 }
 void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
                             cudaStream_t s) {

@@ -106,8 +106,10 @@ struct GemmArgs {
 void launch_gemm_simt(const GemmArgs& a, WType wt, cudaStream_t s);
 
 // Device init / conversion helpers.
+// Counter-based N(0, stddev) fill; element i of dst draws the variate of global index index0 + i, so
+// a tensor filled in pieces equals the tensor filled at once.
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
-                        cudaStream_t s);
+                        cudaStream_t s, long long index0 = 0);
 void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
                             cudaStream_t s);
 // dst[c*mul+off][r] = (T)src[r][c] for a rows x cols float64 source (reference row-major -> K-major;

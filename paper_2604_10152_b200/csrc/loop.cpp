@@ -125,6 +125,25 @@ private:
 // ------------------------------------------------------------------ drafting replica (drafting.cpp:153-227)
 double unif(std::mt19937_64& r) { return (double)(r() >> 11) * 0x1.0p-53; }
 
+// hot_* selection for one layer (drafting.cpp:191-226): top-N by (count desc, index asc) among
+// activated experts, filled from the current set in its order, sorted.
+std::vector<int> select_layer_hot(const uint64_t* c, int E, const std::vector<int>* current, int n) {
+    std::vector<int> idx(E);
+    for (int i = 0; i < E; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return c[a] > c[b]; });
+    std::vector<int> picked;
+    for (int i = 0; i < std::min(n, E); ++i)
+        if (c[idx[i]] > 0) picked.push_back(idx[i]);
+    if ((int)picked.size() < n && current)
+        for (int e : *current) {
+            if ((int)picked.size() == n) break;
+            if (std::find(picked.begin(), picked.end(), e) == picked.end()) picked.push_back(e);
+        }
+    if ((int)picked.size() != n) throw Error(kInvariant, "select_draft_experts: cannot assemble N draft experts");
+    std::sort(picked.begin(), picked.end());
+    return picked;
+}
+
 std::vector<std::vector<int>> select_sets(int policy, const std::vector<uint64_t>& counts, int M, int E,
                                           const std::vector<std::vector<int>>& current, int n, std::mt19937_64& rng) {
     if (n > E) throw Error(kConfig, "select_draft_experts: n_draft > experts_per_block");
@@ -142,21 +161,7 @@ std::vector<std::vector<int>> select_sets(int policy, const std::vector<uint64_t
             out[l] = pool;
             continue;
         }
-        const uint64_t* c = counts.data() + (size_t)l * E;
-        std::vector<int> idx(E);
-        for (int i = 0; i < E; ++i) idx[i] = i;
-        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return c[a] > c[b]; });
-        std::vector<int> picked;
-        for (int i = 0; i < std::min(n, E); ++i)
-            if (c[idx[i]] > 0) picked.push_back(idx[i]);
-        if ((int)picked.size() < n && l < (int)current.size())
-            for (int e : current[l]) {
-                if ((int)picked.size() == n) break;
-                if (std::find(picked.begin(), picked.end(), e) == picked.end()) picked.push_back(e);
-            }
-        if ((int)picked.size() != n) throw Error(kInvariant, "select_draft_experts: cannot assemble N draft experts");
-        std::sort(picked.begin(), picked.end());
-        out[l] = picked;
+        out[l] = select_layer_hot(counts.data() + (size_t)l * E, E, l < (int)current.size() ? &current[l] : nullptr, n);
     }
     return out;
 }
@@ -236,6 +241,7 @@ static void hot_global_warmup(Engine& e, SpecState& S, const std::vector<std::ve
     std::vector<uint64_t> wc((size_t)M * E, 0);
     Ledger wl;
     Residency wr(M, E, S.c);
+    if (e.offload) e.store_reset();  // the profiling pass starts from an empty device (no pins)
     e.reset_sequences(prompts);
     std::vector<int> rs(B), one(B, 1), raw, am(B);
     for (int b = 0; b < B; ++b) rs[b] = b;
@@ -288,6 +294,11 @@ void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>&
     S->res->pin(S->sets, S->led, 1, -1);
     S->out.setup_bytes = S->led.total;
     S->led.reset();
+    if (e.offload) {  // initial pin = model setup, excluded like the reference's setup_bytes
+        e.store_reset();
+        e.store_pin_sets(S->sets);
+        e.collect_h2d();
+    }
     e.reset_sequences(prompts);
     S->gen.assign(S->B, 0);
     e.h2d_bytes = 0;
@@ -333,8 +344,24 @@ int spec_step(Engine& e, int* accepted_tokens) {
         e.pass(na, drows, nullptr, t, true, S.c.use_affinity, t);
         launch_scatter_tokens(e.amax, drows, nullptr, t, na, e.drafts, e.stride, e.stream);
     }
-    // (b) verification: one pass over all gamma+1 positions of every active sequence
-    e.pass(TV, e.row_seq, e.row_extra, 0, false, 0, g);
+    // (b) verification: one pass over all gamma+1 positions of every active sequence.  Offloaded
+    // experts are migrated layer by layer inside the pass; hot_temporal re-pins each layer as soon as
+    // its routing over all verify rows is known (same rule and inputs as the phase-end selection).
+    if (e.offload && S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
+        e.repin_hook = [&S, E, K](int mo, const int* raw, int T, std::vector<int>& next) {
+            std::vector<uint64_t> cnt(E, 0);
+            for (int q = 0; q < T * K; ++q) cnt[raw[q]]++;
+            next = select_layer_hot(cnt.data(), E, &S.sets[mo], S.nd);
+            return true;
+        };
+    }
+    try {
+        e.pass(TV, e.row_seq, e.row_extra, 0, false, 0, g);
+    } catch (...) {
+        e.repin_hook = nullptr;
+        throw;
+    }
+    e.repin_hook = nullptr;
     launch_scatter_tokens(e.amax, e.row_seq, e.row_extra, 0, TV, e.vam, e.stride, e.stream);
     // (c) accept
     launch_accept(e.drafts, e.vam, e.seqs, na, g, e.stride, e.acc, e.corr, e.stream);
@@ -440,6 +467,12 @@ int spec_step(Engine& e, int* accepted_tokens) {
     if (S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
         auto next = select_sets(SMOE_POLICY_HOT_TEMPORAL, S.pc, M, E, S.sets, S.nd, S.prng);
         S.res->pin(next, S.led, 1, S.phase);
+        if (e.offload)  // the store re-pinned layer by layer during verify: it must agree
+            for (int m = 0; m < M; ++m)
+                for (int ex = 0; ex < E; ++ex)
+                    if ((e.key_pinned[(size_t)m * E + ex] != 0) !=
+                        (std::find(next[m].begin(), next[m].end(), ex) != next[m].end()))
+                        throw Error(kInvariant, "expert store: per-layer re-pin diverged from the phase selection");
         if (next != S.sets) S.sets_dirty = true;
         S.sets = std::move(next);
     }
@@ -481,6 +514,7 @@ RunOut spec_end(Engine& e) {
                        ? (S.spec_s / ((double)S.phase * S.g)) / (S.step_s / (double)S.phase)
                        : 0.0;
     R.ledger = S.led.e;
+    e.collect_h2d();
     R.h2d_expert_bytes = e.h2d_bytes;
     R.h2d_s = e.h2d_ms * 1e-3;
     RunOut out = std::move(R);
@@ -518,6 +552,9 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     R.B = B; R.max_new = c.max_new_tokens; R.gamma = 0;
     R.tokens.assign(B, {});
     R.hotness.assign((size_t)M * E, 0);
+    if (e.offload) e.store_reset();
+    e.h2d_bytes = 0;
+    e.h2d_ms = 0;
     e.reset_sequences(prompts);
     std::vector<int> rs(B), one(B, 1), raw, am(B);
     for (int b = 0; b < B; ++b) rs[b] = b;
@@ -569,6 +606,9 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     R.lambda = 1.0;
     R.c_measured = 0.0;
     R.ledger = led.e;
+    e.collect_h2d();
+    R.h2d_expert_bytes = e.h2d_bytes;
+    R.h2d_s = e.h2d_ms * 1e-3;
     return R;
 }
 

@@ -162,3 +162,56 @@ def test_bf16_lossless_and_batch_invariant(kind):
     one = e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=24), prompts[2:3])
     assert one.tokens[0] == sp.tokens[2]
     assert sp.metrics["bytes_spec"] == 0
+
+
+# ---------------------------------------------------------------- C3: expert store (pinned host -> HBM)
+@pytest.mark.parametrize("i", [1, 4])
+def test_offload_store_f32_equals_reference(i):
+    """Experts in pinned host DRAM, migrated per layer during verify: tokens/ledger still equal the
+    reference, and the bytes physically copied == ledger bytes (fp32 tanh2: real bytes per expert ==
+    the reference's 2*d*f*4)."""
+    g = gold("toy")[i]
+    s = spec_of(g["spec"])
+    e = Engine(s, weight_type=F32, max_batch=8, max_gamma=10, offload=1, hbm_expert_slots=40).init_exact()
+    assert e.affinity().tolist() == g["affinity"]
+    cfg = RunCfg(**g["cfg"])
+    r = e.run_specmoe(cfg, g["prompts"])
+    got = run_dict(r)
+    for key in ("tokens", "outcomes", "trace", "ledger", "metrics"):
+        assert got[key] == g["specmoe"][key], key
+    assert r.metrics["h2d_expert_bytes"] == r.metrics["bytes_total"]
+    od = e.run_ondemand(cfg, g["prompts"])
+    assert run_dict(od) == g["ondemand"]
+    assert od.metrics["h2d_expert_bytes"] == od.metrics["bytes_total"]
+
+
+@pytest.mark.parametrize("policy", ["hot_temporal", "random", "hot_global"])
+def test_offload_bf16_matches_resident(policy):
+    """Same device-initialised weights, HBM-resident vs offloaded store: identical tokens and
+    ledger; migrated bytes == ledger entries x real bytes per expert."""
+    s = _c1_like(SWIGLU3, skew=1.0)
+    a = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4).init_device(9)
+    b = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4, offload=1).init_device(9)
+    a.build_affinity_device()
+    b.build_affinity_device()
+    assert np.array_equal(a.affinity(), b.affinity())
+    prompts = make_prompts(2, 4, 8, s.vocab)
+    cfg = RunCfg(gamma=4, n_draft=4, max_new_tokens=16, policy=policy, warmup_steps=4)
+    ra, rb = a.run_specmoe(cfg, prompts), b.run_specmoe(cfg, prompts)
+    assert ra.tokens == rb.tokens and ra.ledger == rb.ledger and ra.outcomes == rb.outcomes
+    bpe = b.info()["bytes_per_expert"]
+    assert rb.metrics["h2d_expert_bytes"] == len(rb.ledger) * bpe
+    assert rb.metrics["h2d_s"] > 0
+    oa, ob = a.run_ondemand(cfg, prompts), b.run_ondemand(cfg, prompts)
+    assert oa.tokens == ob.tokens == ra.tokens
+    assert ob.metrics["h2d_expert_bytes"] == len(ob.ledger) * bpe
+
+
+def test_offload_slot_exhaustion_is_reported():
+    s = _c1_like(TANH2)
+    e = Engine(s, weight_type=BF16, max_batch=2, max_gamma=4, offload=1, hbm_expert_slots=8).init_device(1)
+    e.build_affinity_device()
+    from paper_2604_10152_b200.engine import EngineError
+    with pytest.raises(EngineError) as ei:
+        e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=8), make_prompts(0, 2, 8, s.vocab))
+    assert ei.value.code == 2
