@@ -49,6 +49,10 @@ def args_parse():
     p.add_argument("--e2e-tokens", type=int, default=12)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--offload", action="store_true", help="headline = C3 (experts in pinned host DRAM)")
+    p.add_argument("--no-offload-section", action="store_true", help="skip the C3 section of the default run")
+    p.add_argument("--offload-batch", type=int, default=32)
+    p.add_argument("--offload-steps", type=int, default=2)
     return p.parse_args()
 
 
@@ -158,6 +162,79 @@ def ncu_traffic():
         return None
 
 
+def measure_pcie(dev: int) -> float:
+    """Pinned host->device cudaMemcpyAsync bandwidth, 1 GiB, best of 10 (the migration roofline)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", dev))
+    best = 0.0
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        d.copy_(h, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+    del h, d
+    return best
+
+
+def offload_section(a, dev: int, batch: int, steps: int, warmup: int, gammas=(4,)) -> dict:
+    """C3: experts in pinned host DRAM, migrated over PCIe per layer during verify.  Reports accepted
+    tokens/s, PCIe bytes/token, achieved H2D GB/s vs the measured pinned-copy peak, and the on-demand
+    comparator (baselines.cpp:29-105) on the same engine."""
+    import torch
+    from paper_2604_10152_b200.engine import BF16, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    pcie = measure_pcie(dev)
+    spec = ModelSpec(**SHAPES[a.shape], seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
+    t0 = time.time()
+    eng = Engine(spec, weight_type=BF16, max_batch=batch, max_gamma=max(gammas), device=dev, offload=1)
+    eng.init_device(0)
+    eng.build_affinity_device()
+    setup_s = time.time() - t0
+    prompts = make_prompts(2000, batch, 8, spec.vocab)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", dev))
+    out = {"workload": f"{SHAPE_NAMES[a.shape]}, {a.expert} experts in pinned host DRAM (C3), B={batch}, N={a.n_draft}",
+           "pcie_peak_gbs": pcie, "pcie_peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 10, measured in this run",
+           "setup_s": setup_s, "gamma": {}}
+    for g in gammas:
+        eng.spec_begin(RunCfg(gamma=g, n_draft=a.n_draft, max_new_tokens=1 << 30), prompts)
+        for _ in range(warmup):
+            eng.spec_step()
+        eng.counters(reset=True)
+        base_bytes = eng.spec_end().metrics["h2d_expert_bytes"]
+        eng.spec_begin(RunCfg(gamma=g, n_draft=a.n_draft, max_new_tokens=1 << 30), prompts)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        tokens = 0
+        for _ in range(steps):
+            tokens += eng.spec_step()[0]
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        r = eng.spec_end()
+        hb, hs = r.metrics["h2d_expert_bytes"], r.metrics["h2d_s"]
+        out["gamma"][str(g)] = {
+            "tokens_per_s": tokens / (ms * 1e-3), "tau": r.metrics["tau_mean"], "ms_per_step": ms / steps,
+            "pcie_bytes_per_token": hb / max(1, tokens), "h2d_gbs": hb / hs / 1e9 if hs else None,
+            "h2d_frac_of_measured": (hb / hs / 1e9) / pcie if hs else None,
+            "pcie_busy_frac": (hs * 1e3) / ms if ms else None,
+            "ledger_bytes_per_token_reference_units": r.metrics["bytes_total"] / max(1, r.metrics["tokens_total"])}
+        del base_bytes
+    od = eng.run_ondemand(RunCfg(gamma=max(gammas), n_draft=a.n_draft, max_new_tokens=max(2, steps)), prompts)
+    od_tps = od.metrics["tokens_total"] / od.metrics["gpu_s"]
+    out["ondemand"] = {"tokens_per_s": od_tps, "pcie_bytes_per_token": od.metrics["h2d_expert_bytes"] / max(1, od.metrics["tokens_total"]),
+                       "h2d_gbs": od.metrics["h2d_expert_bytes"] / od.metrics["h2d_s"] / 1e9 if od.metrics["h2d_s"] else None}
+    for g, v in out["gamma"].items():
+        v["speedup_vs_ondemand"] = v["tokens_per_s"] / od_tps if od_tps else None
+        v["transfer_reduction_vs_ondemand"] = 1.0 - v["pcie_bytes_per_token"] / max(1e-9, out["ondemand"]["pcie_bytes_per_token"])
+    eng.close()
+    return out
+
+
 def run_b200(a) -> None:
     import torch
     rank, world, local = dist_env()
@@ -168,6 +245,18 @@ def run_b200(a) -> None:
     from paper_2604_10152_b200.engine import BF16, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
 
+    if a.offload:
+        if rank == 0:
+            sec = offload_section(a, local, a.batch, a.steps, a.warmup, gammas=(a.gamma,))
+            gv = sec["gamma"][str(a.gamma)]
+            line = {"metric": METRIC, "value": gv["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "steps": a.steps,
+                    "warmup": a.warmup, "ms_per_step": gv["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                    "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": {"workload": sec["workload"]},
+                    "roofline": {"bound": "pcie", "achieved": gv["h2d_gbs"], "peak": sec["pcie_peak_gbs"],
+                                 "unit": "GB/s", "frac": gv["h2d_frac_of_measured"], "traffic": None},
+                    "offload": sec}
+            print(json.dumps(line), flush=True)
+        return
     shp = dict(SHAPES[a.shape])
     spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
     eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local)
@@ -266,6 +355,12 @@ def run_b200(a) -> None:
         "breakdown_ms": {"expert_gemm": prof["ms"], "dense_gemm": dense["ms"], "head_gemm": head["ms"], "step_total": ms},
         "clocks": clocks,
     }
+    if not a.no_offload_section and world == 1:
+        eng.close()
+        try:
+            line["offload_c3"] = offload_section(a, local, a.offload_batch, a.offload_steps, 1, gammas=(2, 4, 8))
+        except Exception as ex:
+            line["offload_c3"] = {"error": str(ex)[:300]}
     if not a.no_cpu_baseline and world == 1:
         thr = a.cpu_threads or os.cpu_count()
         try:
