@@ -215,3 +215,70 @@ def test_offload_slot_exhaustion_is_reported():
     with pytest.raises(EngineError) as ei:
         e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=8), make_prompts(0, 2, 8, s.vocab))
     assert ei.value.code == 2
+
+
+# ---------------------------------------------------------------- breadth: configs and edge cases vs the oracle
+CASES = [
+    # (spec overrides, run cfg overrides, batch)
+    (dict(num_layers=3, moe_mask=[0, 1, 1], experts=64, top_k=6, hidden=64, ffn=32, vocab=128, seed=5),
+     dict(gamma=4, n_draft=8, max_new_tokens=14), 3),                                  # C4-like: E64 K6, dense layer 0
+    (dict(num_layers=2, experts=8, top_k=2, hidden=32, ffn=64, vocab=64, seed=6),
+     dict(gamma=1, n_draft=2, max_new_tokens=1), 2),                                   # gamma=1, N=K, 1 new token
+    (dict(num_layers=4, experts=16, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.5, seed=7),
+     dict(gamma=5, n_draft=4, max_new_tokens=17, use_affinity=False), 2),             # hash-surrogate remap
+    (dict(num_layers=4, experts=16, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.5, seed=8),
+     dict(gamma=3, n_draft=4, max_new_tokens=13, policy="hot_global", warmup_steps=5), 2),
+    (dict(num_layers=4, experts=16, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.5, seed=9),
+     dict(gamma=3, n_draft=4, max_new_tokens=13, policy="random"), 3),
+    (dict(num_layers=3, experts=8, top_k=3, hidden=48, ffn=40, vocab=96, gate_skew=0.5, seed=10),
+     dict(gamma=6, n_draft=3, max_new_tokens=20), 4),                                  # K=3, N=K, odd dims
+    (dict(num_layers=4, experts=8, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.0, seed=11),
+     dict(gamma=4, n_draft=2, max_new_tokens=16, device_capacity_bytes=(4 * 2 + 3) * 2 * 32 * 64 * 4), 2),  # eviction
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_f32_configs_equal_oracle(case, port):
+    from oracle.oracle import ModelSpec as OSpec, OracleError, RunCfg as ORun
+    sp, rc, B = CASES[case]
+    ospec = OSpec(**sp)
+    m = port.build(ospec)
+    prompts = make_prompts(100 + case, B, 6, sp["vocab"])
+    cfg = dict(rc, collect_trace=True, run_seed=case)
+    try:
+        want = m.run_specmoe(ORun(**cfg), prompts)
+    except OracleError as ex:
+        want = ex
+    e = Engine(spec_of(sp), weight_type=F32, max_batch=B, max_gamma=cfg["gamma"]).init_exact()
+    if isinstance(want, Exception):
+        from paper_2604_10152_b200.engine import EngineError
+        with pytest.raises(EngineError) as ei:
+            e.run_specmoe(RunCfg(**cfg), prompts)
+        assert ei.value.code == want.code
+        return
+    got = e.run_specmoe(RunCfg(**cfg), prompts)
+    assert got.tokens == want.tokens
+    assert got.outcomes == want.outcomes
+    assert got.trace == want.trace
+    assert got.ledger == want.ledger
+    assert got.hotness.tolist() == want.hotness.tolist()
+    for k, v in want.metrics.items():
+        if k != "wall_s":
+            assert got.metrics[k] == v, k
+    od_w = m.run_ondemand(ORun(**cfg), prompts)
+    od_g = e.run_ondemand(RunCfg(**cfg), prompts)
+    assert od_g.tokens == od_w.tokens and od_g.ledger == od_w.ledger and od_g.trace == od_w.trace
+
+
+def test_bf16_fine_grained_lossless():
+    """C4-like shape on the tcgen05 path (E=64, K=6, dense first layer): lossless + batch invariant."""
+    s = ModelSpec(num_layers=3, moe_mask=[0, 1, 1], experts=64, top_k=6, hidden=256, ffn=128, vocab=512, seed=4,
+                  expert_kind=SWIGLU3)
+    e = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4).init_device(4)
+    e.build_affinity_device()
+    prompts = make_prompts(9, 4, 8, s.vocab)
+    sp = e.run_specmoe(RunCfg(gamma=4, n_draft=8, max_new_tokens=20), prompts)
+    od = e.run_ondemand(RunCfg(gamma=4, max_new_tokens=20), prompts)
+    assert sp.tokens == od.tokens
+    one = e.run_specmoe(RunCfg(gamma=4, n_draft=8, max_new_tokens=20), prompts[1:2])
+    assert one.tokens[0] == sp.tokens[1]
