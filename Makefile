@@ -8,10 +8,10 @@ SRC := paper_2604_10152_b200/csrc
 OUT := paper_2604_10152_b200/lib
 OBJ := build/obj
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
-CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -Wno-unused-parameter -I$(CUDA)/include
+CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -Wno-unused-parameter -I$(CUDA)/include -Iinclude
 CU := $(wildcard $(SRC)/*.cu)
 CPP := $(wildcard $(SRC)/*.cpp)
-HDR := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/specmoe_b200.h
+HDR := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/specmoe_b200.h include/specmoe/api.hpp
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP))
 
 all: $(OUT)/libspecmoe_b200.so oracle-port

@@ -1,0 +1,3 @@
+// specmoe/model.hpp -- drop-in header name of the reference module; the declarations live in api.hpp.
+#pragma once
+#include "specmoe/api.hpp"

@@ -463,14 +463,19 @@ void Engine::build_affinity_device() {
 // list and takes the first member not already chosen, so no float64 compare happens on the GPU.
 void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft) {
     if ((int)sets.size() != M) throw Error(kInvariant, "forward: restricted set count != MoE layer count");
-    if (n_draft < K) throw Error(kInvariant, "forward: restricted set smaller than top_k");
+    // per-layer sizes may differ (RestrictedExperts allows it); rows are padded with -1 to the widest
+    int nmax = 0;
+    for (const auto& st : sets) {
+        if ((int)st.size() < K) throw Error(kInvariant, "forward: restricted set smaller than top_k");
+        nmax = std::max(nmax, (int)st.size());
+    }
+    (void)n_draft;
     std::vector<uint8_t> ind((size_t)M * E, 0);
-    std::vector<int> sorted((size_t)M * E, 0), rk((size_t)M * E * n_draft, 0);
+    std::vector<int> sorted((size_t)M * E, -1), rk((size_t)M * E * nmax, -1);
     for (int m = 0; m < M; ++m) {
         std::vector<int> srt(sets[m]);
-        if ((int)srt.size() != n_draft) throw Error(kInvariant, "forward: restricted set size mismatch");
         std::sort(srt.begin(), srt.end());
-        for (int i = 0; i < n_draft; ++i) {
+        for (size_t i = 0; i < srt.size(); ++i) {
             if (srt[i] < 0 || srt[i] >= E) throw Error(kInvariant, "forward: draft expert out of range");
             ind[(size_t)m * E + srt[i]] = 1;
             sorted[(size_t)m * E + i] = srt[i];
@@ -484,13 +489,13 @@ void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_dra
                     return a < b;
                 });
             }
-            std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * n_draft);
+            std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * nmax);
         }
     }
     h2d(in_draft, ind.data(), ind.size());
     upload_ints(draft_sorted, sorted.data(), sorted.size());
     upload_ints(rank, rk.data(), rk.size());
-    cur_n_draft = n_draft;
+    cur_n_draft = nmax;
 }
 
 // ------------------------------------------------------------------ profiling

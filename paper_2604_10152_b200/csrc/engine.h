@@ -46,6 +46,7 @@ struct RunCfg {
     uint64_t run_seed = 0;
     uint64_t device_capacity_bytes = 0, bytes_per_expert = 0;
     double host_bandwidth = 64e9, ssd_bandwidth = 0.0, compute_rate = 1e6, compute_cost_per_expert = 2e-6;
+    int overlap = 0;  // baselines: oracle overlap timing, total = max(compute, migration) (baselines.cpp:101-111)
 };
 
 struct LedgerEntry { int phase, step, layer, expert; uint64_t bytes; };
@@ -68,6 +69,7 @@ struct RunOut {
     double lambda = 1.0, c_measured = 0.0;
     double wall_s = 0, gpu_s = 0, h2d_s = 0;
     uint64_t h2d_expert_bytes = 0;
+    std::vector<uint64_t> lambda_inputs;  // 4 per phase: verify tokens, verify experts, step tokens, step experts
 };
 
 struct SpecState;  // stepped loop state (loop.cpp)
@@ -231,7 +233,13 @@ public:
 
 // loop.cpp
 RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
-RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
+// pinned_sets != nullptr: MoE-Caching (baselines.cpp:117-145) -- those experts are pinned before the
+// run (setup bytes, excluded from the ledger) and cost zero bytes afterwards.
+RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts,
+                    const std::vector<std::vector<int>>* pinned_sets = nullptr);
+// baselines.cpp:117-145: greedy on-demand warmup profile -> top ceil(fraction*E) per layer.
+std::vector<std::vector<int>> caching_sets(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts,
+                                           double cache_fraction, uint64_t* warmup_bytes);
 void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);
 int spec_step(Engine& e, int* accepted_tokens);  // returns number of active sequences after the step
 RunOut spec_end(Engine& e);

@@ -216,13 +216,14 @@ __global__ void k_gate(GateArgs a) {
                 if (a.use_affinity) {  // nearest by (distance, index): first non-excluded rank
                     for (int j = 0; j < a.N && ex < 0; ++j) {
                         int c = a.rank[pick * a.N + j];
+                        if (c < 0) break;  // padded row (smaller set on this layer)
                         bool ex_c = false;
                         for (int q = 0; q < k; ++q) ex_c |= chosen[q] == c;
                         if (!ex_c) ex = c;
                     }
                 } else {  // hash surrogate (drafting.cpp:140-151)
                     int cnt = 0;
-                    for (int j = 0; j < a.N; ++j) {
+                    for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
                         bool ex_c = false;
                         for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
                         cnt += !ex_c;
@@ -232,7 +233,7 @@ __global__ void k_gate(GateArgs a) {
                                                ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
                                                (uint64_t)a.row_plen[r]);
                         int want = (int)(h % (uint64_t)cnt);
-                        for (int j = 0; j < a.N; ++j) {
+                        for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
                             bool ex_c = false;
                             for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
                             if (!ex_c && want-- == 0) { ex = a.draft_sorted[j]; break; }

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cmath>
 #include <random>
 
 #include "engine.h"
@@ -510,6 +511,7 @@ RunOut spec_end(Engine& e) {
         if (ss <= 0.0) throw Error(kInvariant, "measure_lambda: zero single-step latency");
         R.lambda = vs / ss;
     }
+    R.lambda_inputs = S.lam;
     R.c_measured = (S.phase > 0 && S.step_s > 0.0)
                        ? (S.spec_s / ((double)S.phase * S.g)) / (S.step_s / (double)S.phase)
                        : 0.0;
@@ -535,7 +537,8 @@ RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int
 }
 
 // baselines.cpp:29-99 (greedy, no pinned set, no overlap)
-RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts) {
+RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts,
+                    const std::vector<std::vector<int>>* pinned_sets) {
     const int plen = prompt_len_of(prompts);
     const int B = (int)prompts.size();
     if (c.gamma < 1) throw Error(kConfig, "spec: gamma >= 1 violated");
@@ -553,6 +556,12 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     R.tokens.assign(B, {});
     R.hotness.assign((size_t)M * E, 0);
     if (e.offload) e.store_reset();
+    if (pinned_sets) {  // MoE-Caching: cached experts pinned up front (baselines.cpp:60-65)
+        res.pin(*pinned_sets, led, 2, -1);
+        R.setup_bytes = led.total;
+        led.reset();
+        if (e.offload) e.store_pin_sets(*pinned_sets);
+    }
     e.h2d_bytes = 0;
     e.h2d_ms = 0;
     e.reset_sequences(prompts);
@@ -589,7 +598,7 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
                 }
         }
         const uint64_t bytes = res.ensure(need, 2, step, led);
-        modeled += step_cost((uint64_t)B, n_need, bytes, c, false);
+        modeled += step_cost((uint64_t)B, n_need, bytes, c, c.overlap != 0);
         res.flush();
     }
     tm.stop(e.stream, &R.gpu_s, &R.wall_s);
@@ -610,6 +619,22 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     R.h2d_expert_bytes = e.h2d_bytes;
     R.h2d_s = e.h2d_ms * 1e-3;
     return R;
+}
+
+std::vector<std::vector<int>> caching_sets(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts,
+                                           double cache_fraction, uint64_t* warmup_bytes) {
+    if (cache_fraction <= 0.0 || cache_fraction >= 1.0) throw Error(kConfig, "baseline: 0 < cache_fraction < 1 violated");
+    if (c.warmup_steps < 1) throw Error(kConfig, "baseline: warmup_steps >= 1 violated");
+    SpecState S;
+    S.c = c;
+    S.B = (int)prompts.size();
+    S.M = e.M; S.E = e.E; S.K = e.K;
+    S.nd = (int)std::ceil(cache_fraction * e.E);
+    const uint64_t cache_bytes = (uint64_t)S.nd * e.M * c.bytes_per_expert;
+    hot_global_warmup(e, S, prompts);  // fills S.sets from the warmup counts (empty current set)
+    if (cache_bytes > c.device_capacity_bytes) throw Error(kConfig, "caching: cached experts exceed device capacity");
+    if (warmup_bytes) *warmup_bytes = S.out.warmup_bytes;
+    return S.sets;
 }
 
 }  // namespace smoe

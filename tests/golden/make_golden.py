@@ -74,6 +74,14 @@ def main():
                   "forward_logits": lg.tolist(), "forward_raw": raw.tolist(),
                   "affinity": m.affinity().tolist(), "weights": weights_digest(m, s)}
 
+    # the reference-API caller (tests/cpp/caller.cpp) compiled against the reference itself
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "caller_ref")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I/root/reference/proj/core/include",
+                    os.path.join(ROOT, "tests", "cpp", "caller.cpp")] +
+                   sorted(__import__("glob").glob("/root/reference/proj/core/src/*.cpp")) + ["-o", exe], check=True)
+    gold["cpp_caller"] = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+
     for k, v in gold.items():
         with open(os.path.join(OUT, f"{k}.json"), "w") as f:
             json.dump(v, f)
