@@ -38,6 +38,8 @@ typedef struct {
     int device;
     int offload;             /* 0: all experts HBM-resident; 1: pinned host pool + HBM slots (C3) */
     int hbm_expert_slots;    /* offload: HBM slot count (0 = pinned draft sets + one layer's transients) */
+    int ep_rank, ep_world;   /* expert parallelism: this rank holds experts [r*E/G, (r+1)*E/G) of every layer
+                                (0, 0 or 0, 1 = single GPU); attach a transport before running */
 } smoe_engine_config;
 
 /* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy/seed (greedy). */
@@ -113,6 +115,17 @@ void smoe_free_result(smoe_run_result* r);
 int smoe_spec_begin(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len);
 int smoe_spec_step(smoe_engine* e, int* tokens_accepted_out, int* active_out);
 int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
+
+/* Expert parallelism.  Tokens are replicated, experts sharded; per MoE layer the ranks'
+ * disjoint expert outputs are summed (exact in any order -> bit-identical results at any G).
+ * NCCL: rank 0 calls smoe_ep_nccl_unique_id, the id is broadcast out of band, every rank attaches.
+ * Loopback: G engines on one device driven by G host threads (validation without a multi-GPU box). */
+typedef struct smoe_ep_loopback smoe_ep_loopback;
+int smoe_ep_nccl_unique_id(void* out, int len);
+int smoe_ep_attach_nccl(smoe_engine* e, const void* id, int len);
+smoe_ep_loopback* smoe_ep_loopback_create(int world);
+void smoe_ep_loopback_destroy(smoe_ep_loopback* g);
+int smoe_ep_attach_loopback(smoe_engine* e, smoe_ep_loopback* g);
 
 /* Counters since the last reset: hot-path kernel launches, algorithmic HBM bytes of the expert GEMMs
  * (distinct experts touched per pass x bytes per expert) and of the dense GEMMs, and control-path

@@ -228,6 +228,32 @@ int smoe_bench_expert_gemm(smoe_engine* h, int T, int iters, double* up_ms, doub
     return guarded([&] { h->e->bench_expert_gemm(T, iters, up_ms, down_ms, bytes_up, bytes_down); });
 }
 
+int smoe_ep_nccl_unique_id(void* out, int len) {
+    int n = 0;
+    int rc = guarded([&] { n = smoe::nccl_unique_id(out, len); });
+    return rc ? -rc : n;
+}
+int smoe_ep_attach_nccl(smoe_engine* h, const void* id, int len) {
+    return guarded([&] {
+        auto& e = *h->e;
+        if (e.ep_world < 2) throw smoe::Error(SMOE_CONFIG, "engine was not created with ep_world > 1");
+        e.comm = smoe::make_nccl_comm(e.ep_rank, e.ep_world, id, len, e.device);
+    });
+}
+smoe_ep_loopback* smoe_ep_loopback_create(int world) {
+    smoe::LoopbackGroup* g = nullptr;
+    guarded([&] { g = smoe::loopback_create(world); });
+    return reinterpret_cast<smoe_ep_loopback*>(g);
+}
+void smoe_ep_loopback_destroy(smoe_ep_loopback* g) { smoe::loopback_destroy(reinterpret_cast<smoe::LoopbackGroup*>(g)); }
+int smoe_ep_attach_loopback(smoe_engine* h, smoe_ep_loopback* g) {
+    return guarded([&] {
+        auto& e = *h->e;
+        if (e.ep_world < 2) throw smoe::Error(SMOE_CONFIG, "engine was not created with ep_world > 1");
+        e.comm = smoe::make_loopback_comm(reinterpret_cast<smoe::LoopbackGroup*>(g), e.ep_rank);
+    });
+}
+
 int smoe_profile_reset(smoe_engine* h) {
     return guarded([&] {
         h->e->prof_collect();

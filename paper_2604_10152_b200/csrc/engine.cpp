@@ -93,7 +93,14 @@ Engine::Engine(const smoe_engine_config& c) {
     SMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
 
     const size_t ws = wt == kF32 ? 4 : 2;
-    int exp_slots = M * E;
+    ep_world = std::max(1, c.ep_world);
+    ep_rank = c.ep_rank;
+    if (ep_rank < 0 || ep_rank >= ep_world) throw Error(kConfig, "engine: ep_rank outside [0, ep_world)");
+    if (E % ep_world) throw Error(kConfig, "engine: experts_per_block must be divisible by ep_world");
+    if (ep_world > 1 && offload) throw Error(kConfig, "engine: expert parallelism with the offloaded store is not supported");
+    e_lo = ep_rank * (E / ep_world);
+    e_hi = e_lo + E / ep_world;
+    int exp_slots = M * (E / ep_world);
     if (offload) {
         exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * E, M * 4 + E);
         if (exp_slots < E) throw Error(kConfig, "engine: hbm_expert_slots must be >= experts_per_block");
@@ -106,8 +113,9 @@ Engine::Engine(const smoe_engine_config& c) {
     up_pool = dalloc_bytes((size_t)n_slots * U * d * ws);
     down_pool = dalloc_bytes((size_t)n_slots * d * f * ws);
     head = dalloc_bytes((size_t)V * d * ws);
-    h_slot_of.resize((size_t)M * E);
-    for (int i = 0; i < M * E; ++i) h_slot_of[i] = i;
+    h_slot_of.assign((size_t)M * E, -1);  // experts of other EP ranks stay -1 (their GEMM groups are skipped)
+    for (int m = 0; m < M; ++m)
+        for (int e = e_lo; e < e_hi; ++e) h_slot_of[(size_t)m * E + e] = m * (e_hi - e_lo) + (e - e_lo);
     dense_slot.assign(L, -1);
     for (int l = 0, k = 0; l < L; ++l)
         if (!mask[l]) dense_slot[l] = exp_slots + k++;
@@ -154,6 +162,7 @@ Engine::Engine(const smoe_engine_config& c) {
         s_down = pick(nkb_f, 4);
     }
     ybuf = dalloc<float>((size_t)s_down * Tmax * K * d);
+    if (ep_world > 1) yred = dalloc<float>((size_t)Tmax * K * d);
     pmix = dalloc<float>((size_t)s_mix * Tmax * d);
     logits = dalloc<float>((size_t)Tmax * V);
     amax = dalloc<int>(Tmax);
@@ -187,7 +196,7 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
-    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);
+    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
@@ -262,6 +271,11 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     // Destination of an expert matrix: its HBM slot, or (offload) a device staging buffer that is
     // read-modified-written against the key's region of the pinned host pool.
     int off_key = -1;
+    if ((name == "up" || name == "w1" || name == "w3" || name == "down" || name == "w2") && layer >= 0 && layer < L &&
+        mask[layer] && expert >= 0 && expert < E && (expert < e_lo || expert >= e_hi)) {
+        if (n != (long long)d * f) throw Error(kConfig, "upload_tensor: " + name + " size mismatch");
+        return;  // another EP rank owns this expert
+    }
     auto slot_for = [&]() -> int {
         if (layer < 0 || layer >= L) throw Error(kConfig, "upload_tensor: layer out of range");
         if (mask[layer]) {
@@ -387,7 +401,28 @@ void Engine::init_device(uint64_t s) {
     launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
     launch_fill_normal(gate_w, kF32, (long long)M * E * d, sd, s, tid++, stream);
     const uint64_t tid_up = tid++, tid_down = tid++;
-    if (!offload) {
+    dev_rng = true;
+    dev_seed = s;
+    if (!offload && ep_world > 1) {  // this rank's experts, same values as the single-GPU layout
+        const size_t ws = wt == kF32 ? 4 : 2;
+        for (int m = 0; m < M; ++m)
+            for (int e = e_lo; e < e_hi; ++e) {
+                const int key = m * E + e, slot = h_slot_of[key];
+                launch_fill_normal(static_cast<char*>(up_pool) + (size_t)slot * U * d * ws, wt, (long long)U * d, sd, s,
+                                   tid_up, stream, (long long)key * U * d);
+                launch_fill_normal(static_cast<char*>(down_pool) + (size_t)slot * d * f * ws, wt, (long long)d * f, sd,
+                                   s, tid_down, stream, (long long)key * d * f);
+            }
+        for (int l = 0, k = 0; l < L; ++l)
+            if (!mask[l]) {
+                const long long gi = (long long)(M * E + k);
+                launch_fill_normal(static_cast<char*>(up_pool) + (size_t)dense_slot[l] * U * d * ws, wt, (long long)U * d,
+                                   sd, s, tid_up, stream, gi * U * d);
+                launch_fill_normal(static_cast<char*>(down_pool) + (size_t)dense_slot[l] * d * f * ws, wt,
+                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f);
+                ++k;
+            }
+    } else if (!offload) {
         launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid_up, stream);
         launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid_down, stream);
     } else {
@@ -431,6 +466,13 @@ void Engine::build_affinity_device() {
     if (offload) store_reset();
     std::vector<int> ident(E);
     for (int e = 0; e < E; ++e) ident[e] = e;
+    void *tmp_up = nullptr, *tmp_down = nullptr;
+    if (ep_world > 1) {  // experts of other ranks are not resident: regenerate each layer's E experts
+        if (!dev_rng)
+            throw Error(kConfig, "expert parallelism: build the affinity on the host (smoe_set_affinity) for uploaded weights");
+        tmp_up = dalloc_bytes((size_t)E * U * d * ws);
+        tmp_down = dalloc_bytes((size_t)E * d * f * ws);
+    }
     for (int m = 0; m < M; ++m) {
         SMOE_CUDA(cudaMemsetAsync(scratch64, 0, need * sizeof(double), stream));
         const int* slots = slot_of + (size_t)m * E;
@@ -440,8 +482,22 @@ void Engine::build_affinity_device() {
             upload_ints(group_slot, ident.data(), E);
             slots = group_slot;
         }
-        launch_pairwise_sqdist(up_pool, wt, (long long)U * d, (long long)U * d, slots, E, scratch64, stream);
-        launch_pairwise_sqdist(down_pool, wt, (long long)d * f, (long long)d * f, slots, E, scratch64, stream);
+        if (tmp_up) {
+            const double sd = 1.0 / std::sqrt((double)d);
+            for (int e = 0; e < E; ++e) {
+                const long long key = (long long)m * E + e;
+                launch_fill_normal(static_cast<char*>(tmp_up) + (size_t)e * U * d * ws, wt, (long long)U * d, sd, dev_seed,
+                                   4, stream, key * U * d);
+                launch_fill_normal(static_cast<char*>(tmp_down) + (size_t)e * d * f * ws, wt, (long long)d * f, sd,
+                                   dev_seed, 5, stream, key * d * f);
+            }
+            upload_ints(group_slot, ident.data(), E);
+            slots = group_slot;
+        }
+        const void* pool_up = tmp_up ? tmp_up : up_pool;
+        const void* pool_down = tmp_down ? tmp_down : down_pool;
+        launch_pairwise_sqdist(pool_up, wt, (long long)U * d, (long long)U * d, slots, E, scratch64, stream);
+        launch_pairwise_sqdist(pool_down, wt, (long long)d * f, (long long)d * f, slots, E, scratch64, stream);
         (void)ws;
         SMOE_CUDA(cudaMemcpyAsync(part.data(), scratch64, need * sizeof(double), cudaMemcpyDeviceToHost, stream));
         sync();
@@ -453,6 +509,8 @@ void Engine::build_affinity_device() {
                 D[(size_t)i * E + j] = D[(size_t)j * E + i] = std::sqrt(s);
             }
     }
+    if (tmp_up) SMOE_CUDA(cudaFree(tmp_up));
+    if (tmp_down) SMOE_CUDA(cudaFree(tmp_down));
     if (offload) h2d_bytes = 0;
     have_affinity = true;
 }
@@ -585,8 +643,15 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
                  kEpiStoreF32, "expert_gemm", ebytes_dn, s_down, yd_stride);
             if (fetch) store_finish_layer(mo);
-            // K9 combine + residual + the next layer's (or the head's) rms
-            launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
+            if (ep_world > 1) {  // EP: this rank's rows (zeros elsewhere), summed across ranks -- exact
+                if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
+                launch_ep_pack(ybuf, s_down, yd_stride, group_off, e_lo, e_hi, T * K, d, yred, stream);
+                comm->allreduce_sum(yred, (size_t)T * K * d, stream);
+                launch_combine_rms(x, yred, 1, 0, pos, wgt, T, K, d, 0, xa, wt, stream);
+            } else {
+                // K9 combine + residual + the next layer's (or the head's) rms
+                launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
+            }
         } else {
             launch_resid_rms(x, pmix, s_mix, pm_stride, T, d, xa, wt, stream);
             gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, T, dense_slot[l], T, xa, op_xa, hbuf,
@@ -607,7 +672,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
 // Kernel timed alone: T tokens routed round-robin over all E experts of MoE layer 0 (every expert
 // touched), up-projection then down-projection, `iters` times each with CUDA events.
 void Engine::bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms, double* bytes_up, double* bytes_down) {
-    if (offload) throw Error(kConfig, "bench_expert_gemm: HBM-resident engines only");
+    if (offload || ep_world > 1) throw Error(kConfig, "bench_expert_gemm: single-GPU HBM-resident engines only");
     if (T > Tmax) throw Error(kConfig, "bench_expert_gemm: T exceeds max_batch*(max_gamma+1)");
     std::vector<int> fin((size_t)T * K);
     for (int t = 0; t < T; ++t)

@@ -12,6 +12,7 @@
 
 #include "../../include/specmoe_b200.h"
 #include "common.cuh"
+#include "ep.h"
 #include "kernels.h"
 
 namespace smoe {
@@ -96,6 +97,12 @@ public:
     int n_dense;
     int offload, n_slots;
     int U;                        // rows per slot in the up pool (f or 2f)
+    // expert parallelism: this rank owns experts [e_lo, e_hi) of every MoE layer
+    int ep_rank = 0, ep_world = 1, e_lo = 0, e_hi = 0;
+    std::unique_ptr<Comm> comm;
+    float* yred = nullptr;        // [Tmax*K][d] this rank's expert outputs, summed across ranks
+    bool dev_rng = false;         // weights came from init_device (regenerable anywhere)
+    uint64_t dev_seed = 0;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     int device = 0;
 

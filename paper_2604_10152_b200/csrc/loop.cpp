@@ -379,17 +379,19 @@ int spec_step(Engine& e, int* accepted_tokens) {
     e.launches += (uint64_t)g + 2;  // scatters + accept (commit counted below)
     e.ctl_d2h += sizeof(int) * ((size_t)2 * na + (size_t)e.Bmax * e.stride + (size_t)M * K * (TV + (size_t)g * na));
     {  // algorithmic expert bytes: every distinct (layer, expert) a pass touches streams its weights once
+        // (this rank's experts only under expert parallelism)
         const double bpe = (double)e.real_bytes_per_expert();
+        const uint64_t mine = (e.e_hi - e.e_lo >= 64 ? ~0ull : ((1ull << (e.e_hi - e.e_lo)) - 1)) << e.e_lo;
         for (int t = 0; t < g; ++t)
             for (int m = 0; m < M; ++m) {
                 uint64_t seen = 0;
                 for (int q = 0; q < na * K; ++q) seen |= 1ull << dfin[t][(size_t)m * na * K + q];
-                e.alg_expert_bytes += bpe * __builtin_popcountll(seen);
+                e.alg_expert_bytes += bpe * __builtin_popcountll(seen & mine);
             }
         for (int m = 0; m < M; ++m) {
             uint64_t seen = 0;
             for (int q = 0; q < TV * K; ++q) seen |= 1ull << S.vraw[(size_t)m * TV * K + q];
-            e.alg_expert_bytes += bpe * __builtin_popcountll(seen);
+            e.alg_expert_bytes += bpe * __builtin_popcountll(seen & mine);
         }
     }
 

@@ -28,7 +28,8 @@ EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe
            "smoe_init_weights_exact", "smoe_init_weights_device", "smoe_upload_tensor", "smoe_set_affinity",
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
            "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters", "smoe_bench_expert_gemm",
-           "smoe_profile_reset", "smoe_profile_read"]
+           "smoe_profile_reset", "smoe_profile_read", "smoe_ep_nccl_unique_id", "smoe_ep_attach_nccl",
+           "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback"]
 
 
 class EngineError(RuntimeError):
@@ -42,7 +43,7 @@ class EngineConfig(C.Structure):
                 ("ffn", C.c_int), ("vocab", C.c_int), ("gate_skew", C.c_double), ("seed", C.c_uint64),
                 ("moe_mask", C.POINTER(C.c_uint8)), ("expert_kind", C.c_int), ("weight_type", C.c_int),
                 ("max_batch", C.c_int), ("max_gamma", C.c_int), ("gemm_backend", C.c_int), ("device", C.c_int),
-                ("offload", C.c_int), ("hbm_expert_slots", C.c_int)]
+                ("offload", C.c_int), ("hbm_expert_slots", C.c_int), ("ep_rank", C.c_int), ("ep_world", C.c_int)]
 
 
 class RunConfig(C.Structure):
@@ -119,6 +120,12 @@ def lib():
     L.smoe_counters.argtypes = [vp, C.POINTER(C.c_uint64), dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.c_int]
     L.smoe_bench_expert_gemm.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp, dp]
+    L.smoe_ep_nccl_unique_id.argtypes = [vp, C.c_int]
+    L.smoe_ep_attach_nccl.argtypes = [vp, vp, C.c_int]
+    L.smoe_ep_loopback_create.restype = vp
+    L.smoe_ep_loopback_create.argtypes = [C.c_int]
+    L.smoe_ep_loopback_destroy.argtypes = [vp]
+    L.smoe_ep_attach_loopback.argtypes = [vp, vp]
     L.smoe_profile_reset.argtypes = [vp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
     _LIB = L
@@ -211,6 +218,28 @@ def _collect(rp) -> RunResult:
         lib().smoe_free_result(rp)
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(256)
+    n = lib().smoe_ep_nccl_unique_id(buf, 256)
+    if n <= 0:
+        raise EngineError(-n if n < 0 else 3, lib().smoe_last_error().decode(errors="replace"))
+    return buf.raw[:n]
+
+
+class LoopbackGroup:
+    """G virtual EP ranks on one device (each rank: an Engine driven by its own thread)."""
+
+    def __init__(self, world: int):
+        self.h = lib().smoe_ep_loopback_create(world)
+        if not self.h:
+            raise EngineError(1, lib().smoe_last_error().decode(errors="replace"))
+
+    def close(self):
+        if self.h:
+            lib().smoe_ep_loopback_destroy(self.h)
+            self.h = None
+
+
 def _iarr(x):
     a = np.ascontiguousarray(np.asarray(x, dtype=np.int32))
     return a, a.ctypes.data_as(C.POINTER(C.c_int))
@@ -220,7 +249,8 @@ class Engine:
     """One B200 engine: device-resident weights + state for one model (specmoe::ModelWeights analogue)."""
 
     def __init__(self, spec: ModelSpec, weight_type: int = F32, max_batch: int = 8, max_gamma: int = 10,
-                 gemm: int = GEMM_AUTO, device: int = 0, offload: int = 0, hbm_expert_slots: int = 0):
+                 gemm: int = GEMM_AUTO, device: int = 0, offload: int = 0, hbm_expert_slots: int = 0,
+                 ep_rank: int = 0, ep_world: int = 1):
         self.spec = spec
         L = lib()
         self._mask = None
@@ -229,7 +259,7 @@ class Engine:
         cfg = EngineConfig(spec.num_layers, spec.experts, spec.top_k, spec.hidden, spec.ffn, spec.vocab, spec.gate_skew,
                            spec.seed, C.cast(self._mask, C.POINTER(C.c_uint8)) if self._mask is not None else None,
                            spec.expert_kind, weight_type, max_batch, max_gamma, gemm, device, offload,
-                           hbm_expert_slots)
+                           hbm_expert_slots, ep_rank, ep_world)
         h = C.c_void_p()
         _check(L.smoe_engine_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -331,6 +361,14 @@ class Engine:
         out = C.POINTER(RunResultC)()
         _check(lib().smoe_spec_end(self.h, C.byref(out)))
         return _collect(out)
+
+    # ---- expert parallelism
+    def attach_nccl(self, unique_id: bytes):
+        buf = C.create_string_buffer(unique_id, len(unique_id))
+        _check(lib().smoe_ep_attach_nccl(self.h, buf, len(unique_id)))
+
+    def attach_loopback(self, group: "LoopbackGroup"):
+        _check(lib().smoe_ep_attach_loopback(self.h, group.h))
 
     def counters(self, reset: bool = False) -> dict:
         la, h2d, d2h = C.c_uint64(), C.c_uint64(), C.c_uint64()
