@@ -53,11 +53,39 @@ def args_parse():
     p.add_argument("--no-offload-section", action="store_true", help="skip the C3 section of the default run")
     p.add_argument("--offload-batch", type=int, default=32)
     p.add_argument("--offload-steps", type=int, default=2)
+    p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallelism")
     return p.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def reduce_over_ranks(ms: float, tokens: int, sum_tokens: bool):
+    """Max of the device-timed ms over ranks; tokens summed (replicas) or taken from rank 0 (expert
+    parallel: every rank decodes the same global batch)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return ms, tokens
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    k = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
+    if sum_tokens:
+        dist.all_reduce(k, op=dist.ReduceOp.SUM)
+    else:
+        dist.broadcast(k, 0)
+    return float(t.item()), int(k.item())
+
+
+def share_nccl_id(rank: int):
+    """Rank 0 creates the engine-side NCCL unique id; every rank receives it (torch.distributed)."""
+    import torch.distributed as dist
+    from paper_2604_10152_b200.engine import nccl_unique_id
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 # ---------------------------------------------------------------- clocks (B200_PROFILING.md)
@@ -259,11 +287,16 @@ def run_b200(a) -> None:
         return
     shp = dict(SHAPES[a.shape])
     spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
-    eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local)
+    ep = world > 1 and not a.replicas  # N > 1: experts sharded over the GPUs (NCCL), tokens replicated
+    eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local,
+                 ep_rank=rank if ep else 0, ep_world=world if ep else 1)
+    if ep:
+        eng.attach_nccl(share_nccl_id(rank))
     eng.init_device(0)
     eng.build_affinity_device()
-    prompts = make_prompts(1000 + rank, a.batch, 8, spec.vocab)
-    cfg = RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30, run_seed=rank)
+    seq_seed = 1000 if ep else 1000 + rank
+    prompts = make_prompts(seq_seed, a.batch, 8, spec.vocab)
+    cfg = RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30, run_seed=0 if ep else rank)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
 
     eng.spec_begin(cfg, prompts)
@@ -292,29 +325,20 @@ def run_b200(a) -> None:
     dense = eng.profile_read("dense_gemm")
     head = eng.profile_read("head_gemm")
     res = eng.spec_end()
-    if world > 1:
-        t = torch.tensor([ms, float(tokens)], device="cuda")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms, tokens = float(mx[0].item()), int(t[1].item())
+    ms, tokens = reduce_over_ranks(ms, tokens, sum_tokens=not ep)
 
     # ---- e2e through the public API (host prompts in, host tokens out; per-phase H2D/D2H inside)
     eng.counters(reset=True)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
-    r2 = eng.run_specmoe(RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=a.e2e_tokens, run_seed=rank),
-                         prompts)
+    r2 = eng.run_specmoe(RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=a.e2e_tokens,
+                                run_seed=0 if ep else rank), prompts)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
     c2 = eng.counters()
     e2e_tokens = r2.metrics["tokens_total"]
-    if world > 1:
-        t = torch.tensor([e2e_s, float(e2e_tokens)], device="cuda")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        e2e_s, e2e_tokens = float(mx[0].item()), int(t[1].item())
+    e2e_ms, e2e_tokens = reduce_over_ranks(e2e_s * 1e3, e2e_tokens, sum_tokens=not ep)
+    e2e_s = e2e_ms * 1e-3
     phases2 = max(1, r2.metrics["phases"])
 
     if rank != 0:
@@ -326,18 +350,21 @@ def run_b200(a) -> None:
     achieved = cnt["alg_expert_bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] > 0 else 0.0
     line = {
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init N(0,1/sqrt(d)) weights, synthetic prompts)",
-        "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert} experts HBM-resident, B={a.batch}/GPU, "
+        "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert} experts HBM-resident, "
+                               f"B={a.batch}{'' if ep else '/GPU'}{f', experts sharded over {world} GPUs (NCCL)' if ep else ''}, "
                                f"gamma={a.gamma}, N={a.n_draft}, hot_temporal+affinity, greedy",
                    "model": f"{a.shape} L{spec.num_layers} E{spec.experts} K{spec.top_k} d{spec.hidden} f{spec.ffn} "
                             f"V{spec.vocab}",
-                   "global_batch": a.batch * world, "seq_len": 8, "parallelism": f"replicas{world}",
+                   "global_batch": a.batch if ep else a.batch * world, "seq_len": 8,
+                   "parallelism": f"ep{world}" if ep else f"replicas{world}",
                    "l2": "inputs larger than L2: every verify pass streams all touched expert weights "
                          "(>= 10 GB) from HBM"},
         "tau": res.metrics["tau_mean"],
         "expert_bytes_per_token": {
-            "hbm": cnt["alg_expert_bytes"] * world / max(1, tokens),
+            "hbm": cnt["alg_expert_bytes"] * world / max(1, tokens),  # rank 0's share x G (experts split evenly)
             "pcie": 0, "pcie_note": "HBM-resident config: no migration (see C3 offload)",
             "ledger_reference_units": res.metrics["bytes_total"] / max(1, res.metrics["tokens_total"])},
         "e2e": {"value": e2e_tokens / e2e_s, "unit": "tokens/s",
