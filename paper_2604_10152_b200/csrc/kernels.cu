@@ -478,7 +478,7 @@ void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, c
                            row_plen);
 }
 
-static int row_threads(int d) { return d >= 4096 ? 512 : 256; }
+static int row_threads(int d) { return d >= 4096 ? 1024 : d >= 1024 ? 512 : 256; }
 
 void launch_x0_rms(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
                    const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,
@@ -510,8 +510,9 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
-    if (a.op == kF32) k_gate<float><<<a.T, 256, smem, s>>>(a);
-    else k_gate<__nv_bfloat16><<<a.T, 256, smem, s>>>(a);
+    const int threads = row_threads(a.d);  // one row per block: enough loads in flight for the partials
+    if (a.op == kF32) k_gate<float><<<a.T, threads, smem, s>>>(a);
+    else k_gate<__nv_bfloat16><<<a.T, threads, smem, s>>>(a);
 }
 
 void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot, int* pos,
