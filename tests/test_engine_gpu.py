@@ -343,3 +343,18 @@ def test_expert_parallel_f32_equals_reference():
             assert got[key] == g["specmoe"][key], key
     od = _run_ep(2, s, lambda e: e.init_exact(), cfg, g["prompts"], weight_type=F32, ondemand=True)
     assert run_dict(od[0]) == g["ondemand"]
+
+
+@pytest.mark.slow
+def test_mixtral_shape_lossless_b64():
+    """The benchmark configuration itself (Mixtral-8x7B shape, SwiGLU bf16, B=64, gamma=4): the
+    speculative token stream equals plain greedy decoding on the same engine, token for token."""
+    s = ModelSpec(num_layers=32, experts=8, top_k=2, hidden=4096, ffn=14336, vocab=32000, expert_kind=SWIGLU3)
+    e = Engine(s, weight_type=BF16, max_batch=64, max_gamma=4).init_device(0)
+    e.build_affinity_device()
+    prompts = make_prompts(1000, 64, 8, s.vocab)
+    sp = e.run_specmoe(RunCfg(gamma=4, n_draft=4, max_new_tokens=6), prompts)
+    od = e.run_ondemand(RunCfg(gamma=4, max_new_tokens=6), prompts)
+    assert sp.tokens == od.tokens
+    assert sp.metrics["tokens_total"] == 64 * 6
+    e.close()
