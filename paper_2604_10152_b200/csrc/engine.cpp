@@ -176,8 +176,8 @@ Engine::Engine(const smoe_engine_config& c) {
     seqs = dalloc<int>(Bmax);
     flags = dalloc<int>(1);
     SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
-    sched = dalloc<int>(2);
-    SMOE_CUDA(cudaMemset(sched, 0, 2 * sizeof(int)));
+    sched = dalloc<int>(4);  // two counter slots: consecutive GEMM launches may overlap under PDL
+    SMOE_CUDA(cudaMemset(sched, 0, 4 * sizeof(int)));
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
@@ -598,7 +598,7 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
     if (use_tc) {
         if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
         TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound,
-                     Y, ldy, epi, splits, split_stride, sched};
+                     Y, ldy, epi, splits, split_stride, sched + 2 * (gemm_launches++ & 1)};
         launch_gemm_tc(a, stream);
     } else {
         if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");

@@ -173,7 +173,8 @@ public:
     int* commit_take = nullptr;  // [Bmax]
     int* seqs = nullptr;         // [Bmax]
     int* flags = nullptr;
-    int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters
+    int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][2]
+    unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
     size_t scratch64_n = 0;
     // pinned host staging

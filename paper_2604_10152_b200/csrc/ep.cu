@@ -18,6 +18,8 @@ namespace {
 
 __global__ void k_ep_pack(const float* __restrict__ P, int S, long long pstride, const int* __restrict__ off, int e0,
                           int e1, int d, float* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     const bool mine = r >= off[e0] && r < off[e1];
     const long long base = (long long)r * d;
@@ -186,7 +188,7 @@ std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank) {
 void launch_ep_pack(const float* P, int S, long long pstride, const int* group_off, int e0, int e1, int rows, int d,
                     float* y_red, cudaStream_t s) {
     if (rows <= 0) return;
-    k_ep_pack<<<rows, 256, 0, s>>>(P, S, pstride, group_off, e0, e1, d, y_red);
+    launch_k(k_ep_pack, rows, 256, 0, s, P, S, pstride, group_off, e0, e1, d, y_red);
 }
 
 }  // namespace smoe

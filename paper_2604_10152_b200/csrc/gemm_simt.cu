@@ -40,6 +40,8 @@ template <typename T, int EPI>
 __global__ void __launch_bounds__(kWarps * 32) k_gemm_simt(GemmArgs a) {
     constexpr int VEC = 16 / sizeof(T);
     constexpr bool kGated = EPI == kEpiSwiglu;
+    pdl_wait();
+    pdl_trigger();
     const int g = blockIdx.y;
     const int slot = a.group_off ? a.group_slot[g] : a.single_slot;
     if (slot < 0) return;
@@ -127,10 +129,10 @@ template <typename T>
 void dispatch(const GemmArgs& a, cudaStream_t s) {
     dim3 grid(ceil_div(a.Nout, kWarps * kRPW), a.G);
     switch (a.epi) {
-        case kEpiStoreF32: k_gemm_simt<T, kEpiStoreF32><<<grid, kWarps * 32, 0, s>>>(a); break;
-        case kEpiResidAdd: k_gemm_simt<T, kEpiResidAdd><<<grid, kWarps * 32, 0, s>>>(a); break;
-        case kEpiTanh: k_gemm_simt<T, kEpiTanh><<<grid, kWarps * 32, 0, s>>>(a); break;
-        case kEpiSwiglu: k_gemm_simt<T, kEpiSwiglu><<<grid, kWarps * 32, 0, s>>>(a); break;
+        case kEpiStoreF32: launch_k(k_gemm_simt<T, kEpiStoreF32>, grid, kWarps * 32, 0, s, a); break;
+        case kEpiResidAdd: launch_k(k_gemm_simt<T, kEpiResidAdd>, grid, kWarps * 32, 0, s, a); break;
+        case kEpiTanh: launch_k(k_gemm_simt<T, kEpiTanh>, grid, kWarps * 32, 0, s, a); break;
+        case kEpiSwiglu: launch_k(k_gemm_simt<T, kEpiSwiglu>, grid, kWarps * 32, 0, s, a); break;
     }
 }
 

@@ -220,12 +220,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) pdl_trigger();  // let the next kernel's CTAs take SMs as ours retire
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- scheduler + TMA producer
             int it = 0;
+            bool first = true;
             for (int pub = 0;; ++pub) {
-                // dynamic work distribution: claim the next non-empty unit
+                // dynamic work distribution: claim the next non-empty unit (unit geometry comes from the
+                // routing kernels, which completed before the kernel preceding this one could trigger)
                 int u;
                 Unit w;
                 do {
@@ -239,7 +242,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int arow = (int)((long long)w.slot * p.a_rows_per_slot + w.m0);
                 const int nb = (w.n_valid + BOX_N - 1) / BOX_N;
                 const uint32_t bytes = kABytes + nb * kBoxBytes;
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
+                int kb = w.kb0;
+                if (first) {
+                    // PDL: weights do not depend on the previous kernel -- stream the first stages' weight
+                    // boxes while it drains, then wait for it before loading its activations.
+                    const int pre = min(stages, w.kb1 - w.kb0);
+                    for (int j = 0; j < pre; ++j) {
+                        const int s = (it + j) % stages;
+                        mbar_expect_tx(&full[s], bytes);
+                        tma_load_2d(&mapA, &full[s], smem + s * stage_bytes, (kb + j) * BK, arow);
+                    }
+                    pdl_wait();
+                    for (int j = 0; j < pre; ++j) {
+                        const int s = (it + j) % stages;
+                        uint8_t* st = smem + s * stage_bytes;
+                        for (int q = 0; q < nb; ++q)
+                            tma_load_2d(&mapB, &full[s], st + kABytes + q * kBoxBytes, (kb + j) * BK, w.n0 + q * BOX_N);
+                    }
+                    it += pre;
+                    kb += pre;
+                    first = false;
+                }
+                for (; kb < w.kb1; ++kb, ++it) {
                     const int s = it % stages;
                     mbar_wait(&empty[s], (uint32_t)(((it / stages) & 1) ^ 1));
                     uint8_t* st = smem + s * stage_bytes;
@@ -249,8 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_2d(&mapB, &full[s], st + kABytes + j * kBoxBytes, kb * BK, w.n0 + j * BOX_N);
                 }
             }
+            if (first) pdl_wait();
         }
     } else if (warp == 1) {
+        pdl_wait();
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
             Unit w;
@@ -279,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
+        pdl_wait();
         const int q = warp & 3;
         int cnt = 0, cons = 0;
         Unit w;
@@ -424,7 +451,7 @@ void launch_epi(const TcGemmArgs& a, cudaStream_t s) {
     const CUtensorMap& mb = tensor_map(a.B, BOX_N);
     const int units = p.G * p.n_tiles * p.m_tiles * p.splits;
     const int grid = std::max(1, std::min(units, sm_count()));
-    k_gemm_tc<EPI><<<grid, kThreads, smem, s>>>(ma, mb, p);
+    launch_k(k_gemm_tc<EPI>, grid, kThreads, smem, s, ma, mb, p);
 }
 
 }  // namespace

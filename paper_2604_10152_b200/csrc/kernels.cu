@@ -3,9 +3,16 @@
 // are latency-bound; they are written as single-pass, coalesced, 16-byte-vectorised kernels.
 #include <math.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace smoe {
+
+bool g_use_pdl = [] {
+    const char* v = std::getenv("SMOE_PDL");
+    return !(v && v[0] == '0');
+}();
 
 namespace {
 
@@ -58,6 +65,8 @@ __global__ void k_x0(const double* __restrict__ emb, const double* __restrict__ 
 // ------------------------------------------------------------------ K2 rms
 template <typename OT>
 __global__ void k_rms(const float* __restrict__ x, int d, void* __restrict__ xa) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[33];
     const float* xr = x + (long long)blockIdx.x * d;
     float ss = 0.f;
@@ -78,6 +87,8 @@ __global__ void k_x0_rms(const double* __restrict__ emb, const double* __restric
                          const int* __restrict__ pend, int pstride, const int* __restrict__ row_seq,
                          const int* __restrict__ row_extra, int extra_u, int d, float* __restrict__ x,
                          int* __restrict__ row_plen, void* __restrict__ xa) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float row[];
     __shared__ float red[33];
     const int r = blockIdx.x;
@@ -102,6 +113,8 @@ __global__ void k_x0_rms(const double* __restrict__ emb, const double* __restric
 template <typename OT>
 __global__ void k_resid_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride, int d,
                             void* __restrict__ xa) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float row[];
     __shared__ float red[33];
     const long long base = (long long)blockIdx.x * d;
@@ -125,6 +138,8 @@ __global__ void k_resid_rms(float* __restrict__ x, const float* __restrict__ P, 
 // ------------------------------------------------------------------ K4/K5 gate + remap
 template <typename OT>
 __global__ void k_gate(GateArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[8*32 + 33]
     float* xf = sm;
     float* gl = xf + a.d;
@@ -256,6 +271,8 @@ __global__ void k_gate(GateArgs a) {
 // ------------------------------------------------------------------ K6 permutation
 __global__ void k_route(const int* __restrict__ fin, int n, int E, const int* __restrict__ slot_of,
                         int* __restrict__ off, int* __restrict__ gslot, int* __restrict__ pos) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int s[];  // fin[n], cnt[E+1]
     int* f = s;
     int* cnt = s + n;
@@ -292,6 +309,8 @@ __global__ void k_single_group(int T, int slot, int* off, int* gslot) {
 
 __global__ void k_gather(const uint4* __restrict__ xa, const int* __restrict__ pos, int K, int vecs,
                          uint4* __restrict__ xp) {
+    pdl_wait();
+    pdl_trigger();
     const int p = blockIdx.x;
     const int t = p / K;
     const uint4* src = xa + (long long)t * vecs;
@@ -304,6 +323,8 @@ template <typename OT>
 __global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
                               const int* __restrict__ pos, const float* __restrict__ wgt, int K, int d, int dense,
                               void* __restrict__ xa) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float row[];
     __shared__ float red[33];
     const int t = blockIdx.x;
@@ -337,6 +358,8 @@ __global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P
 
 // ------------------------------------------------------------------ K10 argmax
 __global__ void k_argmax(const float* __restrict__ lg, int V, int* __restrict__ out, int* flags) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float sv[32];
     __shared__ int si[32];
     const float* row = lg + (long long)blockIdx.x * V;
@@ -367,6 +390,8 @@ __global__ void k_argmax(const float* __restrict__ lg, int V, int* __restrict__ 
 
 __global__ void k_scatter_tokens(const int* src, const int* row_seq, const int* row_extra, int extra_u, int T,
                                  int* dst, int stride) {
+    pdl_wait();
+    pdl_trigger();
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= T) return;
     int e = row_extra ? row_extra[r] : extra_u;
@@ -375,6 +400,8 @@ __global__ void k_scatter_tokens(const int* src, const int* row_seq, const int* 
 
 __global__ void k_accept(const int* drafts, const int* vam, const int* seqs, int na, int gamma, int stride, int* acc,
                          int* corr) {
+    pdl_wait();
+    pdl_trigger();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
     const int b = seqs[i];
@@ -388,6 +415,8 @@ __global__ void k_accept(const int* drafts, const int* vam, const int* seqs, int
 
 __global__ void k_commit(double* ssum, int* slen, const double* emb, const int* seqs, const int* toks, int tstride,
                          const int* take, int d) {
+    pdl_wait();
+    pdl_trigger();
     const int j = blockIdx.x;
     const int b = seqs[j];
     const int n = take[j];
@@ -486,19 +515,19 @@ void launch_x0_rms(const double* emb64, const double* seq_sum, const int* seq_le
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
     if (op == kF32)
-        k_x0_rms<float><<<T, row_threads(d), sm, s>>>(emb64, seq_sum, seq_len, pend, pend_stride, row_seq, row_extra,
-                                                      extra_uniform, d, x, row_plen, xa);
+        launch_k(k_x0_rms<float>, T, row_threads(d), sm, s, emb64, seq_sum, seq_len, pend, pend_stride, row_seq,
+                 row_extra, extra_uniform, d, x, row_plen, xa);
     else
-        k_x0_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(emb64, seq_sum, seq_len, pend, pend_stride, row_seq,
-                                                              row_extra, extra_uniform, d, x, row_plen, xa);
+        launch_k(k_x0_rms<__nv_bfloat16>, T, row_threads(d), sm, s, emb64, seq_sum, seq_len, pend, pend_stride,
+                 row_seq, row_extra, extra_uniform, d, x, row_plen, xa);
 }
 
 void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T, int d, void* xa, WType op,
                       cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
-    if (op == kF32) k_resid_rms<float><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, d, xa);
-    else k_resid_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, d, xa);
+    if (op == kF32) launch_k(k_resid_rms<float>, T, row_threads(d), sm, s, x, P, S, pstride, d, xa);
+    else launch_k(k_resid_rms<__nv_bfloat16>, T, row_threads(d), sm, s, x, P, S, pstride, d, xa);
 }
 
 void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s) {
@@ -511,14 +540,14 @@ void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
     const int threads = row_threads(a.d);  // one row per block: enough loads in flight for the partials
-    if (a.op == kF32) k_gate<float><<<a.T, threads, smem, s>>>(a);
-    else k_gate<__nv_bfloat16><<<a.T, threads, smem, s>>>(a);
+    if (a.op == kF32) launch_k(k_gate<float>, a.T, threads, smem, s, a);
+    else launch_k(k_gate<__nv_bfloat16>, a.T, threads, smem, s, a);
 }
 
 void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot, int* pos,
                   cudaStream_t s) {
     const int n = T * K;
-    k_route<<<1, 1024, sizeof(int) * (n + E + 1), s>>>(fin, n, E, slot_of, group_off, group_slot, pos);
+    launch_k(k_route, 1, 1024, sizeof(int) * (n + E + 1), s, fin, n, E, slot_of, group_off, group_slot, pos);
 }
 
 void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaStream_t s) {
@@ -528,7 +557,8 @@ void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaS
 void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s) {
     if (T <= 0) return;
     const int vecs = d * (op == kF32 ? 4 : 2) / 16;
-    k_gather<<<T * K, 128, 0, s>>>(reinterpret_cast<const uint4*>(xa), pos, K, vecs, reinterpret_cast<uint4*>(xperm));
+    launch_k(k_gather, T * K, 128, 0, s, reinterpret_cast<const uint4*>(xa), pos, K, vecs,
+             reinterpret_cast<uint4*>(xperm));
 }
 
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
@@ -536,32 +566,32 @@ void launch_combine_rms(float* x, const float* P, int S, long long pstride, cons
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
     if (op == kF32)
-        k_combine_rms<float><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_k(k_combine_rms<float>, T, row_threads(d), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
     else
-        k_combine_rms<__nv_bfloat16><<<T, row_threads(d), sm, s>>>(x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_k(k_combine_rms<__nv_bfloat16>, T, row_threads(d), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
     if (T <= 0) return;
-    k_argmax<<<T, 512, 0, s>>>(logits, V, out, flags);
+    launch_k(k_argmax, T, 512, 0, s, logits, V, out, flags);
 }
 
 void launch_scatter_tokens(const int* src, const int* row_seq, const int* row_extra, int extra_uniform, int T, int* dst,
                            int stride, cudaStream_t s) {
     if (T <= 0) return;
-    k_scatter_tokens<<<ceil_div(T, 128), 128, 0, s>>>(src, row_seq, row_extra, extra_uniform, T, dst, stride);
+    launch_k(k_scatter_tokens, ceil_div(T, 128), 128, 0, s, src, row_seq, row_extra, extra_uniform, T, dst, stride);
 }
 
 void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, int gamma, int stride, int* acc,
                    int* corr, cudaStream_t s) {
     if (na <= 0) return;
-    k_accept<<<ceil_div(na, 128), 128, 0, s>>>(drafts, vam, seqs, na, gamma, stride, acc, corr);
+    launch_k(k_accept, ceil_div(na, 128), 128, 0, s, drafts, vam, seqs, na, gamma, stride, acc, corr);
 }
 
 void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
                    int tok_stride, const int* take, int na, int d, cudaStream_t s) {
     if (na <= 0) return;
-    k_commit<<<na, 256, 0, s>>>(seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
+    launch_k(k_commit, na, 256, 0, s, seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
 }
 
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
