@@ -20,7 +20,6 @@ for B in batches:
     for _ in range(2):
         e.spec_step()
     e.counters(reset=True)
-    e.profile_reset()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     a.record(st)
@@ -28,6 +27,11 @@ for B in batches:
     b.record(st)
     b.synchronize()
     ms = a.elapsed_time(b)
+    # profiled copy of the region: per-launch events around the expert GEMMs (serialises PDL overlap)
+    e.counters(reset=True)
+    e.profile_reset()
+    for _ in range(4):
+        e.spec_step()
     c = e.counters()
     p = e.profile_read("expert_gemm")
     r = e.spec_end()
