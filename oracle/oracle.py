@@ -248,6 +248,22 @@ class OracleModel:
             raise OracleError(rc, err.value.decode())
         return logits, raw.reshape(sp.moe_layers, sp.top_k), fin.reshape(sp.moe_layers, sp.top_k)
 
+    def forward_gates(self, prefix):
+        """Port only: (logits [V], gate logits + bias [moe_layers][E]) of one forward."""
+        sp = self.spec
+        p, pp = _iarr(prefix)
+        lg = np.empty(sp.vocab, dtype=np.float64)
+        gates = np.empty(sp.moe_layers * sp.experts, dtype=np.float64)
+        err = C.create_string_buffer(256)
+        f = self.o.lib.om_forward_gates
+        f.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                      C.c_char_p, C.c_int]
+        rc = f(self.h, pp, len(p), lg.ctypes.data_as(C.POINTER(C.c_double)),
+               gates.ctypes.data_as(C.POINTER(C.c_double)), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return lg, gates.reshape(sp.moe_layers, sp.experts)
+
     def time_forward(self, prefix, threads: int = 1, iters: int = 1) -> float:
         """Wall seconds for `threads` concurrent threads x `iters` forward() calls each."""
         p, pp = _iarr(prefix)

@@ -84,6 +84,11 @@ int om_affinity_get(void* aff, double* out, long long cap);
 int om_forward(void* model, const int* prefix, int n, const int* restricted, int n_draft, void* aff,
                double* logits_out, int* raw_out, int* final_out, char* err, int errlen);
 
+/* Port only: forward() plus every MoE layer's gate logits (+ bias) [moe_layers*E] -- the decision
+ * margins for the bf16 agreement tests. */
+int om_forward_gates(void* model, const int* prefix, int n, double* logits_out, double* gates_out, char* err,
+                     int errlen);
+
 /* run_specmoe (specdec.hpp:122-124) and run_ondemand (baselines.hpp:24-26). prompts [B*prompt_len]. */
 om_result* om_run_specmoe(void* model, const om_run_cfg* cfg, const int* prompts, int B, int prompt_len,
                           void* aff, char* err, int errlen);

@@ -370,6 +370,8 @@ static int surrogate_(int layer, int raw, size_t plen, const int* ds, int nd, co
 typedef struct { double* dist; int E, M; } oaff; /* drafting.hpp:14-19 */
 
 /* model.cpp:192-263.  restricted: [M*nd] or NULL. */
+static __thread double* g_gate_dump;  /* om_forward_gates: per-layer gate logits destination */
+
 static void fwd(const omodel* m, const int* prefix, int n, const int* restricted, int nd, const oaff* aff,
                 double* logits, int* raw_out, int* fin_out) {
     const int d = m->d, E = m->E, K = m->K;
@@ -403,6 +405,7 @@ static void fwd(const omodel* m, const int* prefix, int n, const int* restricted
         if (ly->is_moe) {
             mtv(ly->gate, xn, d, E, gl);
             for (int e = 0; e < E; ++e) gl[e] += ly->bias[e];
+            if (g_gate_dump) memcpy(g_gate_dump + (size_t)mo * E, gl, sizeof(double) * E);
             softmax_(gl, E, pr);
             topk_(gl, E, K, raw);
             for (int k = 0; k < K; ++k) {
@@ -433,6 +436,15 @@ int om_forward(void* model, const int* prefix, int n, const int* restricted, int
                int* raw_out, int* final_out, char* err, int errlen) {
     ENTER(err, errlen, g_code);
     fwd((omodel*)model, prefix, n, restricted, nd, (oaff*)aff, logits, raw_out, final_out);
+    LEAVE();
+    return 0;
+}
+
+int om_forward_gates(void* model, const int* prefix, int n, double* logits, double* gates, char* err, int errlen) {
+    ENTER(err, errlen, (g_gate_dump = NULL, g_code));
+    g_gate_dump = gates;
+    fwd((omodel*)model, prefix, n, NULL, 0, NULL, logits, NULL, NULL);
+    g_gate_dump = NULL;
     LEAVE();
     return 0;
 }

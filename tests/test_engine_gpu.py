@@ -358,3 +358,38 @@ def test_mixtral_shape_lossless_b64():
     assert sp.tokens == od.tokens
     assert sp.metrics["tokens_total"] == 64 * 6
     e.close()
+
+
+def test_bf16_agreement_with_oracle_margin_aware(port):
+    """P3 (ii)/(iii): the bf16 tcgen05 engine on the reference's own weights (C1 shape) agrees with the
+    float64 oracle on every routing decision whose oracle gate margin (K-th minus (K+1)-th gate
+    logit) exceeds 0.05, and on every greedy token whose logit margin exceeds 0.1; logits within 3% of
+    the logit scale.  The near-tie rates are reported (bf16 rounding can flip genuine near-ties)."""
+    from oracle.oracle import ModelSpec as OSpec
+    sp = dict(num_layers=4, experts=8, top_k=2, hidden=512, ffn=1024, vocab=1024, seed=0)
+    m = port.build(OSpec(**sp))
+    e = Engine(spec_of(sp), weight_type=BF16, max_batch=1, max_gamma=1).init_exact()
+    rng = np.random.RandomState(1)
+    route_total = route_big = route_bad = tok_big = tok_bad = 0
+    worst = 0.0
+    for trial in range(60):
+        prefix = rng.randint(0, sp["vocab"], size=rng.randint(1, 24)).tolist()
+        lg, raw, _ = e.forward(prefix)
+        rl, gates = m.forward_gates(prefix)
+        rr = m.forward(prefix)[1]
+        worst = max(worst, float(np.max(np.abs(lg - rl)) / np.max(np.abs(rl))))
+        for l in range(gates.shape[0]):
+            srt = np.sort(gates[l])[::-1]
+            margin = srt[sp["top_k"] - 1] - srt[sp["top_k"]]
+            route_total += 1
+            if margin > 0.05:
+                route_big += 1
+                route_bad += set(raw[l].tolist()) != set(rr[l].tolist())
+        s2 = np.sort(rl)[::-1]
+        if s2[0] - s2[1] > 0.1:
+            tok_big += 1
+            tok_bad += int(np.argmax(lg)) != int(np.argmax(rl))
+    print(f"bf16 vs oracle: worst logit err {worst:.4f}; routing near-tie rate {1 - route_big / route_total:.3f}; "
+          f"token near-tie rate {1 - tok_big / 60:.3f}")
+    assert worst <= 0.03
+    assert route_bad == 0 and tok_bad == 0
