@@ -3,7 +3,7 @@
 
 Default workload (BASELINE.json configs[1], the metric's config): Mixtral-8x7B shape
 (L32 E8 K2 d4096 f14336 V32000, SwiGLU experts, bf16 weights, random init), all experts
-HBM-resident, batch 32, gamma 4, N 4 draft experts, hot_temporal + affinity, greedy.
+HBM-resident, batch 64, gamma 4, N 4 draft experts, hot_temporal + affinity, greedy.
 A "step" = one speculative phase over the batch: gamma restricted draft passes, one batched verify
 pass over B*(gamma+1) positions, accept/rollback, hotness + re-pin + ledger.
 
@@ -43,7 +43,7 @@ def args_parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--shape", default="c2", choices=sorted(SHAPES))
     p.add_argument("--expert", default="swiglu3", choices=["swiglu3", "tanh2"])
-    p.add_argument("--batch", type=int, default=32)
+    p.add_argument("--batch", type=int, default=64)
     p.add_argument("--gamma", type=int, default=4)
     p.add_argument("--n-draft", type=int, default=4)
     p.add_argument("--e2e-tokens", type=int, default=12)
@@ -51,7 +51,7 @@ def args_parse():
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--offload", action="store_true", help="headline = C3 (experts in pinned host DRAM)")
     p.add_argument("--no-offload-section", action="store_true", help="skip the C3 section of the default run")
-    p.add_argument("--offload-batch", type=int, default=32)
+    p.add_argument("--offload-batch", type=int, default=64)
     p.add_argument("--offload-steps", type=int, default=2)
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallelism")
     return p.parse_args()
