@@ -178,6 +178,9 @@ Engine::Engine(const smoe_engine_config& c) {
     SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
     sched = dalloc<int>(4);  // two counter slots: consecutive GEMM launches may overlap under PDL
     SMOE_CUDA(cudaMemset(sched, 0, 4 * sizeof(int)));
+    moe_done = dalloc<int>(128);
+    SMOE_CUDA(cudaMemset(moe_done, 0, 128 * sizeof(int)));
+    if (const char* v = getenv("SMOE_FUSED_MOE")) fuse_moe = atoi(v) != 0;
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
@@ -198,7 +201,7 @@ Engine::~Engine() {
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
     fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
-    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(scratch64);
+    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
     fr(stage_up); fr(stage_down);
@@ -608,6 +611,29 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
     prof_end(cls, ev, bytes);
 }
 
+// Grouped expert FFN of the current MoE layer: xperm -> hbuf (up) -> ybuf split partials (down).
+void Engine::expert_ffn(int T, const char* cls) {
+    const size_t ws = wt == kF32 ? 4 : 2;
+    const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
+    const long long yd_stride = (long long)Tmax * K * d;
+    if (!(use_tc && fuse_moe && E <= 64)) {
+        gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf, f,
+             up_epi, cls, (double)U * d * ws);
+        gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
+             kEpiStoreF32, cls, (double)d * f * ws, s_down, yd_stride);
+        return;
+    }
+    cudaEvent_t ev;
+    prof_begin(cls, &ev);
+    const unsigned slot = gemm_launches++ & 1;
+    TcGemmArgs up{op_up, U, op_xperm, f, d, group_off, group_slot, E, 0, 0, T, hbuf, f, up_epi, 1, 0,
+                  sched + 2 * slot, moe_done + 64 * slot};
+    TcGemmArgs dn{op_down, d, op_h, d, f, group_off, group_slot, E, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
+                  sched + 2 * slot, moe_done + 64 * slot};
+    launch_moe_tc(up, dn, stream);
+    prof_end(cls, ev, (double)(U + d) * f * ws);
+}
+
 // ------------------------------------------------------------------ the batched forward pass
 // One pass over T rows (model.cpp:192-263 applied to every row at once).
 void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
@@ -638,10 +664,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             const bool fetch = offload && !restricted;
             if (fetch) store_fetch_layer(mo, T, rl);  // expert store: migrate this layer's missing experts
             launch_gather(xa, pos, T, K, d, xperm, wt, stream);
-            gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf,
-                 f, up_epi, "expert_gemm", ebytes_up);
-            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
-                 kEpiStoreF32, "expert_gemm", ebytes_dn, s_down, yd_stride);
+            expert_ffn(T, "expert_gemm");
             if (fetch) store_finish_layer(mo);
             if (ep_world > 1) {  // EP: this rank's rows (zeros elsewhere), summed across ranks -- exact
                 if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
@@ -665,7 +688,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
          (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
-    launches += 3 + (uint64_t)M * 7 + (uint64_t)n_dense * 5;
+    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 6 : 7) + (uint64_t)n_dense * 5;
     alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
 }
 

@@ -38,8 +38,12 @@ struct TcGemmArgs {
     int splits;               // K splits (kEpiStoreF32 only): partial ks written at Y + ks*split_stride
     long long split_stride;
     int* sched;               // device [2] zero-initialised work counter (self-resetting)
+    int* done = nullptr;      // device [64] zeroed per-group completion counters (fused launches)
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
+// One launch for a MoE layer's grouped up- (tanh / SwiGLU) and down-projection (f32 split partials):
+// down units of expert g start once g's up units have published (gemm_tc.cu).
+void launch_moe_tc(const TcGemmArgs& up, const TcGemmArgs& down, cudaStream_t s);
 
 struct RunCfg {
     int gamma = 10, n_draft = 4, max_new_tokens = 32, use_affinity = 1, warmup_steps = 64, policy = 2,
@@ -174,6 +178,8 @@ public:
     int* seqs = nullptr;         // [Bmax]
     int* flags = nullptr;
     int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][2]
+    int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
+    int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
     unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
     size_t scratch64_n = 0;
@@ -211,6 +217,8 @@ public:
               const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
               const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes,
               int splits = 1, long long split_stride = 0);
+    // a MoE layer's expert FFN (grouped up + down projection), fused into one launch on tcgen05
+    void expert_ffn(int T, const char* cls);
 
     // ---- host<->device helpers
     void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream

@@ -4,19 +4,28 @@
 // Decode-size expert GEMMs have few tokens per expert (n_e = 1..160) and large weight matrices, so
 // the weights take the MMA M slot (128 rows per tile) and the tokens the N slot:
 //   D[row m][token n] (TMEM, f32) = sum_k W[slot][m][k] * X[row n][k]
-// Work unit = (group g, 128-row tile, token tile of <=256 rows, K split).  One CTA per SM walks the
-// units round-robin; its roles run decoupled through mbarrier rings:
-//   warp 0     TMA producer: one 128x64 bf16 weight box + ceil(n/32) 32x64 token boxes per stage
-//              (token boxes sized by the group's real row count, 128B swizzle), multi-stage ring;
+// Work unit = (phase, group g, 128-row tile, token tile of <=256 rows, K split).  One CTA per SM
+// claims units dynamically (global atomic counter); its roles run decoupled through mbarrier rings:
+//   warp 0     scheduler + TMA producer: one 128x64 bf16 weight box + ceil(n/32) 32x64 token boxes per
+//              stage (token boxes sized by the group's real row count, 128B swizzle);
 //   warp 1     owns TMEM (2 x 256 columns: double-buffered accumulator); one lane issues
 //              tcgen05.mma.cta_group::1.kind::f16 with M=128, N=round16(n) (runtime instruction
 //              descriptor), K=16, four per stage, and commits stages / finished accumulators;
 //   warps 2-5  epilogue: tcgen05.ld.32x32b.x16 -> tanh | SwiGLU (w1/w3 rows interleaved, pairs
 //              combined with one shuffle) | f32 store (optionally into a split-K partial) | residual
 //              add, 32 consecutive rows per warp per token (coalesced), then release the accumulator.
-// The epilogue of unit i overlaps the loads and MMAs of unit i+1.  The K order inside a unit and the
-// split count are fixed per GEMM shape (never T-dependent) and a D column never depends on other
-// columns, so every token row gets bit-identical results in draft, verify and on-demand passes.
+// The epilogue of unit i overlaps the loads and MMAs of unit i+1.
+//
+// Two-phase launches fuse a MoE layer's up- and down-projection: every phase-0 (up) unit precedes
+// the phase-1 (down) units in claim order; a down unit of expert g streams its weights into the ring
+// at once and loads its activations (g's up output H) when all of g's up units have published
+// completion through a per-expert counter (release / acquire + async-proxy fence).  The up->down
+// kernel boundary and the up projection's tail disappear.  Programmatic dependent launch is handled
+// the same way for a CTA's first unit: weights first, then griddepcontrol.wait, then activations.
+//
+// The K order inside a unit and the split count are fixed per GEMM shape (never T-dependent) and a D
+// column never depends on other columns, so every token row gets bit-identical results in draft,
+// verify and on-demand passes (batch invariance).
 #include <cuda.h>
 
 #include <map>
@@ -38,22 +47,29 @@ constexpr int kABytes = BM * BK * 2;
 constexpr int kBoxBytes = BOX_N * BK * 2;
 constexpr int kTmemCols = 512;  // 2 accumulators x BN_MAX
 
-struct TcParams {
+constexpr int kRing = 8;        // unit ids published by the producer to the MMA / epilogue roles
+constexpr int kMaxGroups = 64;  // completion counters per two-phase launch
+
+struct Phase {
     int Nrows;  // valid weight rows per slot to compute (Nout, or 2*Nout for SwiGLU)
-    int K;
     long long a_rows_per_slot;
-    const int* group_off;
-    const int* group_slot;
-    int G, single_rows, single_slot;
-    int m_tiles, n_tiles, splits, kb_per_split, num_kb;
+    int m_tiles, splits, kb_per_split, num_kb;
     void* Y;
     int ldy;
     long long split_stride;  // elements between split-K partial outputs
-    int stages, b_region;    // b_region = bytes of token boxes per stage
-    int* sched;              // [2]: next-unit counter, finished-CTA counter (self-resetting)
 };
 
-constexpr int kRing = 8;  // unit ids published by the producer to the MMA / epilogue roles
+struct TcParams {
+    Phase ph[2];
+    int nphase;
+    const int* group_off;
+    const int* group_slot;
+    int G, single_rows, single_slot;
+    int n_tiles;
+    int stages, b_region;  // b_region = bytes of token boxes per stage
+    int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
+    int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -91,6 +107,12 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // K-major operand tile, 128-byte swizzle: 128-B rows, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
@@ -122,18 +144,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Unit u -> (group, token tile, row tile, split); returns false for units with no rows.
 struct Unit {
-    int slot, n0, n_valid, m0, kb0, kb1, ks;
+    int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks;
 };
-__device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
-    int ks = u % p.splits;
-    u /= p.splits;
-    const int mt = u % p.m_tiles;
-    u /= p.m_tiles;
-    const int g = u % p.G;
-    const int nt = u / p.G;
-    int slot, r0, r1;
+
+__device__ __forceinline__ int units_of_phase(const TcParams& p, int ph) {
+    return p.G * p.n_tiles * p.ph[ph].m_tiles * p.ph[ph].splits;
+}
+
+__device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, int& r0, int& r1) {
     if (p.group_off) {
         slot = p.group_slot[g];
         r0 = p.group_off[g];
@@ -143,15 +162,44 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
         r0 = 0;
         r1 = p.single_rows;
     }
+}
+
+// Unit u -> (phase, group, token tile, row tile, split); returns false for units with no rows.
+__device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
+    int ph = 0;
+    const int u0 = units_of_phase(p, 0);
+    if (u >= u0) {
+        ph = 1;
+        u -= u0;
+    }
+    const Phase& P = p.ph[ph];
+    const int ks = u % P.splits;
+    u /= P.splits;
+    const int mt = u % P.m_tiles;
+    u /= P.m_tiles;
+    const int g = u % p.G;
+    const int nt = u / p.G;
+    int slot, r0, r1;
+    group_rows(p, g, slot, r0, r1);
     w.n0 = r0 + nt * BN_MAX;
     if (slot < 0 || w.n0 >= r1) return false;
+    w.phase = ph;
+    w.g = g;
     w.slot = slot;
     w.n_valid = min(BN_MAX, r1 - w.n0);
     w.m0 = mt * BM;
     w.ks = ks;
-    w.kb0 = ks * p.kb_per_split;
-    w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+    w.kb0 = ks * P.kb_per_split;
+    w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
     return w.kb0 < w.kb1;
+}
+
+// Phase-0 units a phase-1 unit of group g waits for (every token tile x row tile x split of g).
+__device__ __forceinline__ int phase0_units_of_group(const TcParams& p, int g) {
+    int slot, r0, r1;
+    group_rows(p, g, slot, r0, r1);
+    if (slot < 0 || r1 <= r0) return 0;
+    return (r1 - r0 + BN_MAX - 1) / BN_MAX * p.ph[0].m_tiles * p.ph[0].splits;
 }
 
 // Consumer side of the unit ring: returns false when the producer published "done".  whole_warp:
@@ -174,13 +222,46 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
     return true;
 }
 
+// One 16-column TMEM chunk of a finished accumulator -> the phase's output.
 template <int EPI>
+__device__ __forceinline__ void epilogue_store(const Phase& P, const Unit& w, int row, int lane, int c,
+                                               const uint32_t* v) {
+    if (EPI == kEpiSwiglu) {
+        // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float mine = __uint_as_float(v[j]);
+            const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+            if (!(lane & 1) && row < P.Nrows && c + j < w.n_valid) {
+                const float h = mine / (1.0f + expf(-mine)) * other;
+                reinterpret_cast<__nv_bfloat16*>(P.Y)[(long long)(w.n0 + c + j) * P.ldy + (row >> 1)] =
+                    __float2bfloat16_rn(h);
+            }
+        }
+    } else if (row < P.Nrows) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (c + j >= w.n_valid) break;
+            const long long o = (long long)(w.n0 + c + j) * P.ldy + row;
+            const float a = __uint_as_float(v[j]);
+            if (EPI == kEpiStoreF32)
+                reinterpret_cast<float*>(P.Y)[o + (long long)w.ks * P.split_stride] = a;
+            else if (EPI == kEpiResidAdd)
+                reinterpret_cast<float*>(P.Y)[o] += a;
+            else
+                reinterpret_cast<__nv_bfloat16*>(P.Y)[o] = __float2bfloat16_rn(tanhf(a));
+        }
+    }
+}
+
+template <int EPI0, int EPI1>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapB0,
+              const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapB1, TcParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int stages = p.stages;
     const int stage_bytes = kABytes + p.b_region;
-    const int total_units = p.G * p.n_tiles * p.m_tiles * p.splits;
+    const int total_units = units_of_phase(p, 0) + (p.nphase > 1 ? units_of_phase(p, 1) : 0);
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -207,8 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&ring_empty[r], 5);  // MMA lane + 4 epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB0) : "memory");
+        if (p.nphase > 1) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB1) : "memory");
+        }
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -225,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // ---------------- scheduler + TMA producer
             int it = 0;
-            bool first = true;
+            bool kernel_dep = false;  // griddepcontrol.wait done: the previous kernel's outputs are visible
             for (int pub = 0;; ++pub) {
                 // dynamic work distribution: claim the next non-empty unit (unit geometry comes from the
                 // routing kernels, which completed before the kernel preceding this one could trigger)
@@ -239,41 +324,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ring[r] = u < total_units ? u : -1;
                 mbar_arrive(&ring_full[r]);
                 if (u >= total_units) break;
-                const int arow = (int)((long long)w.slot * p.a_rows_per_slot + w.m0);
+                const CUtensorMap* mA = w.phase ? &mapA1 : &mapA0;
+                const CUtensorMap* mB = w.phase ? &mapB1 : &mapB0;
+                const int arow = (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0);
                 const int nb = (w.n_valid + BOX_N - 1) / BOX_N;
                 const uint32_t bytes = kABytes + nb * kBoxBytes;
-                int kb = w.kb0;
-                if (first) {
-                    // PDL: weights do not depend on the previous kernel -- stream the first stages' weight
-                    // boxes while it drains, then wait for it before loading its activations.
-                    const int pre = min(stages, w.kb1 - w.kb0);
-                    for (int j = 0; j < pre; ++j) {
-                        const int s = (it + j) % stages;
-                        mbar_expect_tx(&full[s], bytes);
-                        tma_load_2d(&mapA, &full[s], smem + s * stage_bytes, (kb + j) * BK, arow);
-                    }
-                    pdl_wait();
-                    for (int j = 0; j < pre; ++j) {
-                        const int s = (it + j) % stages;
-                        uint8_t* st = smem + s * stage_bytes;
-                        for (int q = 0; q < nb; ++q)
-                            tma_load_2d(&mapB, &full[s], st + kABytes + q * kBoxBytes, (kb + j) * BK, w.n0 + q * BOX_N);
-                    }
-                    it += pre;
-                    kb += pre;
-                    first = false;
-                }
-                for (; kb < w.kb1; ++kb, ++it) {
+                // Activations may be read once (a) the previous kernel is complete (PDL) and (b) for a
+                // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
+                // boxes are issued; at most `stages` of them are held back.
+                const int need = w.phase ? phase0_units_of_group(p, w.g) : 0;
+                bool ready = kernel_dep && (w.phase == 0 || ld_acquire(&p.done[w.g]) >= need);
+                if (ready && w.phase) proxy_fence_async();
+                const int pend_it = it;
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
                     const int s = it % stages;
                     mbar_wait(&empty[s], (uint32_t)(((it / stages) & 1) ^ 1));
                     uint8_t* st = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], bytes);
-                    tma_load_2d(&mapA, &full[s], st, kb * BK, arow);
-                    for (int j = 0; j < nb; ++j)
-                        tma_load_2d(&mapB, &full[s], st + kABytes + j * kBoxBytes, kb * BK, w.n0 + j * BOX_N);
+                    tma_load_2d(mA, &full[s], st, kb * BK, arow);
+                    if (ready) {
+                        for (int j = 0; j < nb; ++j)
+                            tma_load_2d(mB, &full[s], st + kABytes + j * kBoxBytes, kb * BK, w.n0 + j * BOX_N);
+                        continue;
+                    }
+                    if (it + 1 - pend_it < stages && kb + 1 < w.kb1) continue;  // keep streaming weights
+                    if (!kernel_dep) {
+                        pdl_wait();
+                        kernel_dep = true;
+                    }
+                    if (w.phase) {
+                        const long long t0 = clock64();
+                        while (ld_acquire(&p.done[w.g]) < need) {
+                            __nanosleep(100);
+                            if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s: a lost publication
+                        }
+                        proxy_fence_async();  // generic-proxy stores of H before async-proxy (TMA) reads
+                    }
+                    ready = true;
+                    for (int j2 = pend_it; j2 <= it; ++j2) {  // activations of the held-back stages
+                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + kABytes;
+                        const int k2 = w.kb0 + (j2 - pend_it);
+                        for (int j = 0; j < nb; ++j)
+                            tma_load_2d(mB, &full[j2 % stages], sp + j * kBoxBytes, k2 * BK, w.n0 + j * BOX_N);
+                    }
                 }
             }
-            if (first) pdl_wait();
+            if (!kernel_dep) pdl_wait();
         }
     } else if (warp == 1) {
         pdl_wait();
@@ -315,38 +411,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int row = w.m0 + q * 32 + lane;  // weight row within the slot
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX);
+            const Phase& P = p.ph[w.phase];
             for (int c = 0; c < w.n_valid; c += 16) {
                 uint32_t v[16];
                 tmem_ld16(taddr + c, v);
                 tmem_wait_ld();
-                if (EPI == kEpiSwiglu) {
-                    // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const float mine = __uint_as_float(v[j]);
-                        const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-                        if (!(lane & 1) && row < p.Nrows && c + j < w.n_valid) {
-                            const float h = mine / (1.0f + expf(-mine)) * other;
-                            reinterpret_cast<__nv_bfloat16*>(p.Y)[(long long)(w.n0 + c + j) * p.ldy + (row >> 1)] =
-                                __float2bfloat16_rn(h);
-                        }
-                    }
-                } else if (row < p.Nrows) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        if (c + j >= w.n_valid) break;
-                        const long long o = (long long)(w.n0 + c + j) * p.ldy + row;
-                        const float a = __uint_as_float(v[j]);
-                        if (EPI == kEpiStoreF32)
-                            reinterpret_cast<float*>(p.Y)[o + (long long)w.ks * p.split_stride] = a;
-                        else if (EPI == kEpiResidAdd)
-                            reinterpret_cast<float*>(p.Y)[o] += a;
-                        else
-                            reinterpret_cast<__nv_bfloat16*>(p.Y)[o] = __float2bfloat16_rn(tanhf(a));
-                    }
-                }
+                if (w.phase == 0) epilogue_store<EPI0>(P, w, row, lane, c, v);
+                else epilogue_store<EPI1>(P, w, row, lane, c, v);
             }
             tc_fence_before();
+            if (p.nphase > 1 && w.phase == 0) {
+                // publish: all four warps' stores of this unit, then one counter increment
+                __threadfence();
+                proxy_fence_async();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (warp == 2 && lane == 0) atomicAdd(&p.done[w.g], 1);
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
             ++cnt;
@@ -354,10 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) {  // last CTA out resets the scheduler for the next launch on this stream
+    if (threadIdx.x == 0) {  // last CTA out resets the scheduler (and counters) for the next launch
         __threadfence();
         if (atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1) {
             p.sched[0] = 0;
+            if (p.nphase > 1)
+                for (int g = 0; g < p.G; ++g) p.done[g] = 0;
             p.sched[1] = 0;
             __threadfence();
         }
@@ -416,42 +498,55 @@ int sm_count() {
     return n;
 }
 
-template <int EPI>
-void launch_epi(const TcGemmArgs& a, cudaStream_t s) {
+Phase make_phase(const TcGemmArgs& a) {
+    Phase P{};
+    P.Nrows = a.epi == kEpiSwiglu ? 2 * a.Nout : a.Nout;
+    P.a_rows_per_slot = a.a_rows_per_slot;
+    P.m_tiles = (P.Nrows + BM - 1) / BM;
+    P.num_kb = (a.K + BK - 1) / BK;
+    P.splits = std::max(1, std::min(a.splits, P.num_kb));
+    P.kb_per_split = (P.num_kb + P.splits - 1) / P.splits;
+    // every split must own K blocks: a consumer sums exactly `splits` partials
+    if ((P.splits - 1) * P.kb_per_split >= P.num_kb) throw Error(kInvariant, "tcgen05 GEMM: empty K split");
+    P.Y = a.Y;
+    P.ldy = a.ldy;
+    P.split_stride = a.split_stride;
+    return P;
+}
+
+template <int EPI0, int EPI1>
+void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     constexpr int kSmemBudget = 220 * 1024;
     static bool configured = false;
     if (!configured) {
-        SMOE_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        SMOE_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI0, EPI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         configured = true;
     }
     TcParams p{};
-    p.Nrows = EPI == kEpiSwiglu ? 2 * a.Nout : a.Nout;
-    p.K = a.K;
-    p.a_rows_per_slot = a.a_rows_per_slot;
+    p.ph[0] = make_phase(a);
+    p.nphase = b ? 2 : 1;
+    if (b) p.ph[1] = make_phase(*b);
     p.group_off = a.group_off;
     p.group_slot = a.group_slot;
     p.G = a.group_off ? a.G : 1;
     p.single_rows = a.single_rows;
     p.single_slot = a.single_slot;
-    p.m_tiles = (p.Nrows + BM - 1) / BM;
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
-    p.num_kb = (a.K + BK - 1) / BK;
-    p.splits = std::max(1, std::min(a.splits, p.num_kb));
-    p.kb_per_split = (p.num_kb + p.splits - 1) / p.splits;
-    p.Y = a.Y;
-    p.ldy = a.ldy;
-    p.split_stride = a.split_stride;
     const int nb_max = (std::min(a.rows_bound, BN_MAX) + BOX_N - 1) / BOX_N;
     p.b_region = nb_max * kBoxBytes;
     const int stage_bytes = kABytes + p.b_region;
     p.stages = std::max(2, std::min(kMaxStages, (kSmemBudget - 1024 - 512) / stage_bytes));
     p.sched = a.sched;
+    p.done = a.done;
     const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
-    const CUtensorMap& ma = tensor_map(a.A, BM);
-    const CUtensorMap& mb = tensor_map(a.B, BOX_N);
-    const int units = p.G * p.n_tiles * p.m_tiles * p.splits;
-    const int grid = std::max(1, std::min(units, sm_count()));
-    launch_k(k_gemm_tc<EPI>, grid, kThreads, smem, s, ma, mb, p);
+    const CUtensorMap& ma0 = tensor_map(a.A, BM);
+    const CUtensorMap& mb0 = tensor_map(a.B, BOX_N);
+    const CUtensorMap& ma1 = b ? tensor_map(b->A, BM) : ma0;
+    const CUtensorMap& mb1 = b ? tensor_map(b->B, BOX_N) : mb0;
+    long long units = (long long)p.G * p.n_tiles * p.ph[0].m_tiles * p.ph[0].splits;
+    if (b) units += (long long)p.G * p.n_tiles * p.ph[1].m_tiles * p.ph[1].splits;
+    const int grid = (int)std::max(1ll, std::min(units, (long long)sm_count()));
+    launch_k(k_gemm_tc<EPI0, EPI1>, grid, kThreads, smem, s, ma0, mb0, ma1, mb1, p);
 }
 
 }  // namespace
@@ -459,11 +554,22 @@ void launch_epi(const TcGemmArgs& a, cudaStream_t s) {
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s) {
     if (a.Nout <= 0 || a.rows_bound <= 0) return;
     switch (a.epi) {
-        case kEpiStoreF32: launch_epi<kEpiStoreF32>(a, s); break;
-        case kEpiResidAdd: launch_epi<kEpiResidAdd>(a, s); break;
-        case kEpiTanh: launch_epi<kEpiTanh>(a, s); break;
-        case kEpiSwiglu: launch_epi<kEpiSwiglu>(a, s); break;
+        case kEpiStoreF32: launch_phases<kEpiStoreF32, kEpiStoreF32>(a, nullptr, s); break;
+        case kEpiResidAdd: launch_phases<kEpiResidAdd, kEpiStoreF32>(a, nullptr, s); break;
+        case kEpiTanh: launch_phases<kEpiTanh, kEpiStoreF32>(a, nullptr, s); break;
+        case kEpiSwiglu: launch_phases<kEpiSwiglu, kEpiStoreF32>(a, nullptr, s); break;
     }
+}
+
+void launch_moe_tc(const TcGemmArgs& up, const TcGemmArgs& down, cudaStream_t s) {
+    if (up.Nout <= 0 || up.rows_bound <= 0) return;
+    if (!up.group_off || !up.done || up.G > kMaxGroups)
+        throw Error(kInvariant, "fused expert GEMM: needs <= 64 groups and completion counters");
+    if (down.epi != kEpiStoreF32 || down.group_off != up.group_off || down.rows_bound != up.rows_bound)
+        throw Error(kInvariant, "fused expert GEMM: down projection must share the up projection's groups");
+    if (up.epi == kEpiSwiglu) launch_phases<kEpiSwiglu, kEpiStoreF32>(up, &down, s);
+    else if (up.epi == kEpiTanh) launch_phases<kEpiTanh, kEpiStoreF32>(up, &down, s);
+    else throw Error(kInvariant, "fused expert GEMM: up projection epilogue must be tanh or SwiGLU");
 }
 
 }  // namespace smoe
