@@ -158,8 +158,12 @@ Engine::Engine(const smoe_engine_config& c) {
             const int per = (nkb + want - 1) / want;
             return (nkb + per - 1) / per;
         };
-        s_mix = pick(nkb_d, std::max(1, 296 / std::max(1, (d + 127) / 128)));
-        s_down = pick(nkb_f, 4);
+        // mix: about one unit per SM at T <= 256 (measured best on the C2 shape: s_mix 4 > 8 > 2);
+        // down: 2 splits (measured best vs 1/4 with the fused up+down launch)
+        s_mix = pick(nkb_d, std::max(1, 148 / std::max(1, (d + 127) / 128)));
+        s_down = pick(nkb_f, 2);
+        if (const char* v = getenv("SMOE_S_MIX")) s_mix = pick(nkb_d, atoi(v));    // tuning overrides
+        if (const char* v = getenv("SMOE_S_DOWN")) s_down = pick(nkb_f, atoi(v));
     }
     ybuf = dalloc<float>((size_t)s_down * Tmax * K * d);
     if (ep_world > 1) yred = dalloc<float>((size_t)Tmax * K * d);
@@ -634,6 +638,15 @@ void Engine::expert_ffn(int T, const char* cls) {
     prof_end(cls, ev, (double)(U + d) * f * ws);
 }
 
+// Event scope for the non-GEMM kernel classes (profiling runs only).
+struct ProfScope {
+    Engine& e;
+    const char* cls;
+    cudaEvent_t ev;
+    ProfScope(Engine& eng, const char* c) : e(eng), cls(c) { e.prof_begin(c, &ev); }
+    ~ProfScope() { e.prof_end(cls, ev, 0); }
+};
+
 // ------------------------------------------------------------------ the batched forward pass
 // One pass over T rows (model.cpp:192-263 applied to every row at once).
 void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
@@ -659,11 +672,20 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             GateArgs g{x, pmix, s_mix, pm_stride, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E, xa,
                        wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr, draft_sorted + (size_t)mo * E,
                        rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft, use_aff, mo, row_plen, flags};
-            launch_gate(g, stream);  // x += a; K4/K5 on rms(x); xa = rms(x)
-            launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
+            {
+                ProfScope ps(*this, "gate");
+                launch_gate(g, stream);  // x += a; K4/K5 on rms(x); xa = rms(x)
+            }
+            {
+                ProfScope ps(*this, "route");
+                launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
+            }
             const bool fetch = offload && !restricted;
             if (fetch) store_fetch_layer(mo, T, rl);  // expert store: migrate this layer's missing experts
-            launch_gather(xa, pos, T, K, d, xperm, wt, stream);
+            {
+                ProfScope ps(*this, "gather");
+                launch_gather(xa, pos, T, K, d, xperm, wt, stream);
+            }
             expert_ffn(T, "expert_gemm");
             if (fetch) store_finish_layer(mo);
             if (ep_world > 1) {  // EP: this rank's rows (zeros elsewhere), summed across ranks -- exact
@@ -673,6 +695,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                 launch_combine_rms(x, yred, 1, 0, pos, wgt, T, K, d, 0, xa, wt, stream);
             } else {
                 // K9 combine + residual + the next layer's (or the head's) rms
+                ProfScope ps(*this, "combine");
                 launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
             }
         } else {

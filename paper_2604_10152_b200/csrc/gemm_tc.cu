@@ -69,6 +69,9 @@ struct TcParams {
     int stages, b_region;  // b_region = bytes of token boxes per stage
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
+#ifdef SMOE_TC_BULK_A
+    const uint8_t* a_ptr[2];
+#endif
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -341,7 +344,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], (uint32_t)(((it / stages) & 1) ^ 1));
                     uint8_t* st = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], bytes);
+#ifdef SMOE_TC_BULK_A
+                    {
+                        const uint8_t* src = p.a_ptr[w.phase] + ((long long)arow / BM * p.ph[w.phase].num_kb + kb) * kABytes;
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(st)), "l"(src), "r"(kABytes), "r"(smem_u32(&full[s])) : "memory");
+                    }
+#else
                     tma_load_2d(mA, &full[s], st, kb * BK, arow);
+#endif
                     if (ready) {
                         for (int j = 0; j < nb; ++j)
                             tma_load_2d(mB, &full[s], st + kABytes + j * kBoxBytes, kb * BK, w.n0 + j * BOX_N);
@@ -538,6 +548,10 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.stages = std::max(2, std::min(kMaxStages, (kSmemBudget - 1024 - 512) / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
+#ifdef SMOE_TC_BULK_A
+    p.a_ptr[0] = (const uint8_t*)a.A.base;
+    p.a_ptr[1] = b ? (const uint8_t*)b->A.base : nullptr;
+#endif
     const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
     const CUtensorMap& ma0 = tensor_map(a.A, BM);
     const CUtensorMap& mb0 = tensor_map(a.B, BOX_N);

@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libspecmoe_b200.so")
+LIB_PATH = os.environ.get("SMOE_LIB") or os.path.join(HERE, "lib", "libspecmoe_b200.so")  # override: A/B builds
 
 F32, BF16 = 0, 1
 TANH2, SWIGLU3 = 0, 1

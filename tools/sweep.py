@@ -34,10 +34,11 @@ for B in batches:
         e.spec_step()
     c = e.counters()
     p = e.profile_read("expert_gemm")
+    other = {k: round(e.profile_read(k)["ms"] / 4, 3) for k in ("dense_gemm", "head_gemm", "gate", "route", "gather", "combine")}
     r = e.spec_end()
     row = {"B": B, "gamma": gamma, "tokens_per_s": toks / ms * 1e3, "ms_per_step": ms / 4, "tau": r.metrics["tau_mean"],
            "expert_gemm_ms_per_step": p["ms"] / 4, "expert_hbm_GBps": c["alg_expert_bytes"] / (p["ms"] * 1e-3) / 1e9,
-           "hbm_bytes_per_token": c["alg_expert_bytes"] / max(1, toks)}
+           "hbm_bytes_per_token": c["alg_expert_bytes"] / max(1, toks), "other_ms_per_step": other}
     rows.append(row)
     print(json.dumps(row), flush=True)
 json.dump(rows, open(f"gpurun_out/sweep_g{gamma}.json", "w"), indent=1)
