@@ -11,10 +11,11 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-r
 CXXFLAGS := -O2 -std=c++20 -fPIC -Wall -Wextra -Wno-unused-parameter -I$(CUDA)/include -Iinclude
 CU := $(wildcard $(SRC)/*.cu)
 CPP := $(wildcard $(SRC)/*.cpp)
-HDR := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/specmoe_b200.h include/specmoe/api.hpp
+HDR := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/specmoe_b200.h include/specmoe/api.hpp include/specmoe/harness.hpp
+BIN := paper_2604_10152_b200/bin
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP))
 
-all: $(OUT)/libspecmoe_b200.so oracle-port
+all: $(OUT)/libspecmoe_b200.so $(BIN)/specmoe oracle-port
 
 $(OBJ)/%.cu.o: $(SRC)/%.cu $(HDR)
 	@mkdir -p $(OBJ)
@@ -28,11 +29,16 @@ $(OUT)/libspecmoe_b200.so: $(OBJS)
 	@mkdir -p $(OUT)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -ldl -lpthread -lrt
 
+# CLI (harness verbs); finds the library through its rpath
+$(BIN)/specmoe: paper_2604_10152_b200/cli/specmoe_main.cpp $(OUT)/libspecmoe_b200.so include/specmoe/harness.hpp
+	@mkdir -p $(BIN)
+	g++ $(CXXFLAGS) $< -o $@ -L$(OUT) -lspecmoe_b200 -Wl,-rpath,'$$ORIGIN/../lib'
+
 oracle-port:
 	$(MAKE) -s -C oracle port
 oracle-ref:
 	$(MAKE) -s -C oracle ref
 
 clean:
-	rm -rf build $(OUT)/libspecmoe_b200.so
+	rm -rf build $(OUT)/libspecmoe_b200.so $(BIN)
 .PHONY: all clean oracle-port oracle-ref

@@ -144,6 +144,10 @@ int smoe_profile_reset(smoe_engine* e);
 int smoe_profile_read(smoe_engine* e, const char* kernel_class, double* total_ms, long long* launches,
                       double* bytes);
 
+/* Harness prompts (reference harness.hpp:60-62): prompt b = floor(uniform01 * V) draws from
+ * mt19937_64(substream(seed, "prom", b)); out is [batch][prompt_len].  Host only (no device). */
+int smoe_make_prompts(uint64_t seed, int batch, int prompt_len, int vocab, int* out);
+
 #ifdef __cplusplus
 }
 #endif

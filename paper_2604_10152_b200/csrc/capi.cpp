@@ -5,6 +5,7 @@
 #include <string>
 
 #include "engine.h"
+#include "specmoe/harness.hpp"
 
 struct smoe_engine {
     std::unique_ptr<smoe::Engine> e;
@@ -276,3 +277,17 @@ int smoe_profile_read(smoe_engine* h, const char* cls, double* total_ms, long lo
 }
 
 }  // extern "C"
+
+int smoe_make_prompts(uint64_t seed, int batch, int prompt_len, int vocab, int* out) {
+    try {
+        const auto p = specmoe::make_prompts(seed, batch, prompt_len, vocab);
+        for (int b = 0; b < batch; ++b) std::memcpy(out + (size_t)b * prompt_len, p[b].data(), sizeof(int) * prompt_len);
+        return SMOE_OK;
+    } catch (const specmoe::ConfigError& x) {
+        g_err = x.what();
+        return SMOE_CONFIG;
+    } catch (const std::exception& x) {
+        g_err = x.what();
+        return SMOE_INVARIANT;
+    }
+}

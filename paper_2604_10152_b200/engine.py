@@ -29,7 +29,7 @@ EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
            "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters", "smoe_bench_expert_gemm",
            "smoe_profile_reset", "smoe_profile_read", "smoe_ep_nccl_unique_id", "smoe_ep_attach_nccl",
-           "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback"]
+           "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback", "smoe_make_prompts"]
 
 
 class EngineError(RuntimeError):
@@ -128,6 +128,7 @@ def lib():
     L.smoe_ep_attach_loopback.argtypes = [vp, vp]
     L.smoe_profile_reset.argtypes = [vp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
+    L.smoe_make_prompts.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, ip]
     _LIB = L
     return L
 
@@ -135,6 +136,13 @@ def lib():
 def _check(rc: int) -> None:
     if rc != 0:
         raise EngineError(rc, lib().smoe_last_error().decode(errors="replace"))
+
+
+def make_prompts_native(seed: int, batch: int, prompt_len: int, vocab: int) -> list[list[int]]:
+    """The harness's make_prompts (C++, harness.cpp) through the C ABI; host only."""
+    out = (C.c_int * max(1, batch * prompt_len))()
+    _check(lib().smoe_make_prompts(seed, batch, prompt_len, vocab, out))
+    return [list(out[b * prompt_len:(b + 1) * prompt_len]) for b in range(batch)]
 
 
 @dataclass
