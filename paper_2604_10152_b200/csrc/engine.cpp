@@ -146,10 +146,12 @@ Engine::Engine(const smoe_engine_config& c) {
     fin_log = dalloc<int>((size_t)(Gmax + 1) * M * Tmax * K);
     wgt = dalloc<float>((size_t)Tmax * K);
     pos = dalloc<int>((size_t)Tmax * K);
-    group_off = dalloc<int>(E + 1);
     group_slot = dalloc<int>(E);
-    xperm = dalloc_bytes((size_t)Tmax * K * d * ws);
-    hbuf = dalloc_bytes((size_t)Tmax * K * f * ws);
+    grp_cnt = dalloc<int>((size_t)std::max(1, M) * E);
+    SMOE_CUDA(cudaMemset(grp_cnt, 0, sizeof(int) * std::max(1, M) * E));
+    const size_t seg_rows = (size_t)E * Tmax;  // expert segments of Tmax rows (gate dispatch)
+    xperm = dalloc_bytes(seg_rows * d * ws);
+    hbuf = dalloc_bytes(seg_rows * f * ws);
     // split-K counts are fixed per GEMM shape (never T-dependent) so results stay batch invariant
     if (use_tc) {
         const int nkb_d = (d + 63) / 64, nkb_f = (f + 63) / 64;
@@ -165,7 +167,7 @@ Engine::Engine(const smoe_engine_config& c) {
         if (const char* v = getenv("SMOE_S_MIX")) s_mix = pick(nkb_d, atoi(v));    // tuning overrides
         if (const char* v = getenv("SMOE_S_DOWN")) s_down = pick(nkb_f, atoi(v));
     }
-    ybuf = dalloc<float>((size_t)s_down * Tmax * K * d);
+    ybuf = dalloc<float>((size_t)s_down * seg_rows * d);
     if (ep_world > 1) yred = dalloc<float>((size_t)Tmax * K * d);
     pmix = dalloc<float>((size_t)s_mix * Tmax * d);
     logits = dalloc<float>((size_t)Tmax * V);
@@ -193,8 +195,8 @@ Engine::Engine(const smoe_engine_config& c) {
     op_down = {down_pool, (long long)n_slots * d, f};
     op_head = {head, (long long)V, d};
     op_xa = {xa, (long long)Tmax, d};
-    op_xperm = {xperm, (long long)Tmax * K, d};
-    op_h = {hbuf, (long long)Tmax * K, f};
+    op_xperm = {xperm, (long long)seg_rows, d};
+    op_h = {hbuf, (long long)seg_rows, f};
     SMOE_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets above vs. the non-blocking engine stream
 }
 
@@ -203,7 +205,7 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
-    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_off); fr(group_slot); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
+    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
@@ -597,42 +599,44 @@ void Engine::prof_collect() {
 
 // ------------------------------------------------------------------ GEMM dispatch
 void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, long long a_rows_per_slot, int Nout,
-                  int Kd, const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
+                  int Kd, const int* gcnt, const int* gslot, int G, int seg, int single_rows, int single_slot,
+                  int rows_bound,
                   const void* X, const TcOperand& bmap, void* Y, int ldy, Epi epi, const char* cls, double bytes,
                   int splits, long long split_stride) {
     cudaEvent_t ev;
     prof_begin(cls, &ev);
     if (use_tc) {
         if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
-        TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound,
+        TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, gcnt, gslot, G, seg, single_rows, single_slot, rows_bound,
                      Y, ldy, epi, splits, split_stride, sched + 2 * (gemm_launches++ & 1)};
         launch_gemm_tc(a, stream);
     } else {
         if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");
-        GemmArgs a{W, slot_stride, Nout, Kd, goff, gslot, G, single_rows, single_slot, rows_bound, X, Y, ldy, epi};
+        GemmArgs a{W, slot_stride, Nout, Kd, gcnt, gslot, G, seg, single_rows, single_slot, rows_bound, X, Y, ldy, epi};
         launch_gemm_simt(a, wt, stream);
     }
     prof_end(cls, ev, bytes);
 }
 
-// Grouped expert FFN of the current MoE layer: xperm -> hbuf (up) -> ybuf split partials (down).
-void Engine::expert_ffn(int T, const char* cls) {
+// Grouped expert FFN of the current MoE layer: xperm segments -> hbuf (up) -> ybuf split partials
+// (down).  Group e = rows [e*T, e*T + cnt[e]) in weight slot slots[e].
+void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls) {
     const size_t ws = wt == kF32 ? 4 : 2;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
-    const long long yd_stride = (long long)Tmax * K * d;
+    const long long yd_stride = (long long)E * Tmax * d;
     if (!(use_tc && fuse_moe && E <= 64)) {
-        gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf, f,
-             up_epi, cls, (double)U * d * ws);
-        gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
+        gemm(up_pool, (long long)U * d, op_up, U, f, d, cnt, slots, E, T, 0, 0, T, xperm, op_xperm, hbuf, f, up_epi,
+             cls, (double)U * d * ws);
+        gemm(down_pool, (long long)d * f, op_down, d, d, f, cnt, slots, E, T, 0, 0, T, hbuf, op_h, ybuf, d,
              kEpiStoreF32, cls, (double)d * f * ws, s_down, yd_stride);
         return;
     }
     cudaEvent_t ev;
     prof_begin(cls, &ev);
     const unsigned slot = gemm_launches++ & 1;
-    TcGemmArgs up{op_up, U, op_xperm, f, d, group_off, group_slot, E, 0, 0, T, hbuf, f, up_epi, 1, 0,
-                  sched + 2 * slot, moe_done + 64 * slot};
-    TcGemmArgs dn{op_down, d, op_h, d, f, group_off, group_slot, E, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
+    TcGemmArgs up{op_up, U, op_xperm, f, d, cnt, slots, E, T, 0, 0, T, hbuf, f, up_epi, 1, 0, sched + 2 * slot,
+                  moe_done + 64 * slot};
+    TcGemmArgs dn{op_down, d, op_h, d, f, cnt, slots, E, T, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
                   sched + 2 * slot, moe_done + 64 * slot};
     launch_moe_tc(up, dn, stream);
     prof_end(cls, ev, (double)(U + d) * f * ws);
@@ -654,7 +658,8 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     if (T <= 0) return;
     if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
     const size_t ws = wt == kF32 ? 4 : 2;
-    const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)Tmax * K * d;
+    const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)E * Tmax * d;
+    if (M > 0) SMOE_CUDA(cudaMemsetAsync(grp_cnt, 0, sizeof(int) * (size_t)M * E, stream));  // dispatch counters
     // K1+K2: x0 and the first rms
     launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
                   stream);
@@ -663,36 +668,32 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     for (int l = 0; l < L; ++l) {
         // K3: a = Mix rms(x) as split-K partials; the residual add happens in the next kernel
-        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, T, l, T, xa, op_xa, pmix, d, kEpiStoreF32,
-             "dense_gemm", wbytes_dd, s_mix, pm_stride);
+        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, 0, T, l, T, xa, op_xa, pmix, d,
+             kEpiStoreF32, "dense_gemm", wbytes_dd, s_mix, pm_stride);
         const int mo = moe_ord[l];
         if (mo >= 0) {
             int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
             int* fl = fin_log + ((size_t)log_slot * M + mo) * Tmax * K;
-            GateArgs g{x, pmix, s_mix, pm_stride, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E, xa,
-                       wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr, draft_sorted + (size_t)mo * E,
-                       rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft, use_aff, mo, row_plen, flags};
+            int* cnt = grp_cnt + (size_t)mo * E;
+            GateArgs g{x, pmix, s_mix, pm_stride, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E,
+                       xperm, cnt, pos, wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr,
+                       draft_sorted + (size_t)mo * E, rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft,
+                       use_aff, mo, row_plen, flags};
             {
                 ProfScope ps(*this, "gate");
-                launch_gate(g, stream);  // x += a; K4/K5 on rms(x); xa = rms(x)
-            }
-            {
-                ProfScope ps(*this, "route");
-                launch_route(fl, T, K, E, slot_of + (size_t)mo * E, group_off, group_slot, pos, stream);
+                launch_gate(g, stream);  // x += a; rms; gate, top-K, remap; dispatch rows into xperm
             }
             const bool fetch = offload && !restricted;
-            if (fetch) store_fetch_layer(mo, T, rl);  // expert store: migrate this layer's missing experts
-            {
-                ProfScope ps(*this, "gather");
-                launch_gather(xa, pos, T, K, d, xperm, wt, stream);
-            }
-            expert_ffn(T, "expert_gemm");
+            if (fetch) store_fetch_layer(mo, T, rl, cnt);  // expert store: migrate this layer's missing experts
+            // weight slots: the store's table for this layer's fetch, else the resident slot map (draft
+            // passes touch only pinned draft experts)
+            expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
             if (fetch) store_finish_layer(mo);
-            if (ep_world > 1) {  // EP: this rank's rows (zeros elsewhere), summed across ranks -- exact
+            if (ep_world > 1) {  // EP: this rank's picks (zeros elsewhere), summed across ranks -- exact
                 if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
-                launch_ep_pack(ybuf, s_down, yd_stride, group_off, e_lo, e_hi, T * K, d, yred, stream);
+                launch_ep_pack(ybuf, s_down, yd_stride, pos, fl, e_lo, e_hi, T * K, d, yred, stream);
                 comm->allreduce_sum(yred, (size_t)T * K * d, stream);
-                launch_combine_rms(x, yred, 1, 0, pos, wgt, T, K, d, 0, xa, wt, stream);
+                launch_combine_rms(x, yred, 1, 0, nullptr, wgt, T, K, d, 0, xa, wt, stream);
             } else {
                 // K9 combine + residual + the next layer's (or the head's) rms
                 ProfScope ps(*this, "combine");
@@ -700,18 +701,19 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             }
         } else {
             launch_resid_rms(x, pmix, s_mix, pm_stride, T, d, xa, wt, stream);
-            gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, T, dense_slot[l], T, xa, op_xa, hbuf,
-                 f, up_epi, "dense_gemm", ebytes_up);
-            gemm(down_pool, (long long)d * f, op_down, d, d, f, nullptr, nullptr, 1, T, dense_slot[l], T, hbuf, op_h,
-                 ybuf, d, kEpiStoreF32, "dense_gemm", ebytes_dn, s_down, yd_stride);
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, 0, T, dense_slot[l], T, xa, op_xa,
+                 hbuf, f, up_epi, "dense_gemm", ebytes_up);
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, nullptr, nullptr, 1, 0, T, dense_slot[l], T, hbuf,
+                 op_h, ybuf, d, kEpiStoreF32, "dense_gemm", ebytes_dn, s_down, yd_stride);
             launch_combine_rms(x, ybuf, s_down, yd_stride, nullptr, nullptr, T, 1, d, 1, xa, wt, stream);
         }
     }
-    gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32, "head_gemm",
-         (double)V * d * ws);
+    gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, 0, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32,
+         "head_gemm", (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
-    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 6 : 7) + (uint64_t)n_dense * 5;
+    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 4 : 5) + (uint64_t)n_dense * 5 +
+                (ep_world > 1 ? (uint64_t)M : 0);
     alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
 }
 
@@ -720,12 +722,11 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
 void Engine::bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms, double* bytes_up, double* bytes_down) {
     if (offload || ep_world > 1) throw Error(kConfig, "bench_expert_gemm: single-GPU HBM-resident engines only");
     if (T > Tmax) throw Error(kConfig, "bench_expert_gemm: T exceeds max_batch*(max_gamma+1)");
-    std::vector<int> fin((size_t)T * K);
-    for (int t = 0; t < T; ++t)
-        for (int k = 0; k < K; ++k) fin[(size_t)t * K + k] = (t * K + k) % E;
-    upload_ints(fin_log, fin.data(), fin.size());
-    launch_route(fin_log, T, K, E, slot_of, group_off, group_slot, pos, stream);
-    const long long yd_stride = (long long)Tmax * K * d;
+    // round-robin routing: expert e gets the picks (t,k) with (t*K+k) % E == e
+    std::vector<int> cnt(E, 0);
+    for (int j = 0; j < T * K; ++j) ++cnt[j % E];
+    upload_ints(grp_cnt, cnt.data(), E);
+    const long long yd_stride = (long long)E * Tmax * d;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     cudaEvent_t a, b, c;
     SMOE_CUDA(cudaEventCreate(&a)); SMOE_CUDA(cudaEventCreate(&b)); SMOE_CUDA(cudaEventCreate(&c));
@@ -733,11 +734,11 @@ void Engine::bench_expert_gemm(int T, int iters, double* up_ms, double* down_ms,
     for (int pass = 0; pass < 2; ++pass) {  // pass 0 = warm-up
         SMOE_CUDA(cudaEventRecord(a, stream));
         for (int i = 0; i < iters; ++i)
-            gemm(up_pool, (long long)U * d, op_up, U, f, d, group_off, group_slot, E, 0, 0, T, xperm, op_xperm, hbuf, f,
+            gemm(up_pool, (long long)U * d, op_up, U, f, d, grp_cnt, slot_of, E, T, 0, 0, T, xperm, op_xperm, hbuf, f,
                  up_epi, "bench", 0);
         SMOE_CUDA(cudaEventRecord(b, stream));
         for (int i = 0; i < iters; ++i)
-            gemm(down_pool, (long long)d * f, op_down, d, d, f, group_off, group_slot, E, 0, 0, T, hbuf, op_h, ybuf, d,
+            gemm(down_pool, (long long)d * f, op_down, d, d, f, grp_cnt, slot_of, E, T, 0, 0, T, hbuf, op_h, ybuf, d,
                  kEpiStoreF32, "bench", 0, s_down, yd_stride);
         SMOE_CUDA(cudaEventRecord(c, stream));
         SMOE_CUDA(cudaEventSynchronize(c));

@@ -28,9 +28,10 @@ struct TcGemmArgs {
     long long a_rows_per_slot;
     TcOperand B;        // activations [rows, K]
     int Nout, K;
-    const int* group_off;  // nullptr -> single group {0, single_rows} with slot single_slot
+    const int* group_cnt;  // nullptr -> single group {0, single_rows} with slot single_slot
     const int* group_slot;
-    int G, single_rows, single_slot;
+    int G, seg;            // group g = rows [g*seg, g*seg + group_cnt[g]) of B / Y
+    int single_rows, single_slot;
     int rows_bound;
     void* Y;
     int ldy;
@@ -146,7 +147,7 @@ public:
     int store_take_slot(int key);
     void store_release(int key);
     void store_pin_sets(const std::vector<std::vector<int>>& sets);
-    void store_fetch_layer(int mo, int T, const int* raw_dev);
+    void store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt_dev);
     void store_finish_layer(int mo);
     void collect_h2d();
 
@@ -160,10 +161,11 @@ public:
     void* xa = nullptr;
     int *raw_log = nullptr, *fin_log = nullptr;  // [Gmax+1][M][Tmax][K]
     float* wgt = nullptr;
-    int *pos = nullptr, *group_off = nullptr, *group_slot = nullptr;
-    void* xperm = nullptr;  // [Tmax*K][d]
-    void* hbuf = nullptr;   // [Tmax*K][f]
-    float* ybuf = nullptr;  // [s_down][Tmax*K][d] split-K partials of the down projection
+    int *pos = nullptr, *group_slot = nullptr;
+    int* grp_cnt = nullptr;  // [M][E] rows dispatched to each expert in the current pass (zeroed per pass)
+    void* xperm = nullptr;  // [E*Tmax][d] expert segments of T rows (gate dispatch)
+    void* hbuf = nullptr;   // [E*Tmax][f]
+    float* ybuf = nullptr;  // [s_down][E*Tmax][d] split-K partials of the down projection
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
     int s_mix = 1, s_down = 1;
     float* logits = nullptr;  // [Tmax][V]
@@ -214,11 +216,11 @@ public:
     void pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
               int log_slot);
     void gemm(const void* W, long long slot_stride, const TcOperand& aop, long long a_rows_per_slot, int Nout, int Kd,
-              const int* goff, const int* gslot, int G, int single_rows, int single_slot, int rows_bound,
+              const int* gcnt, const int* gslot, int G, int seg, int single_rows, int single_slot, int rows_bound,
               const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes,
               int splits = 1, long long split_stride = 0);
     // a MoE layer's expert FFN (grouped up + down projection), fused into one launch on tcgen05
-    void expert_ffn(int T, const char* cls);
+    void expert_ffn(int T, const int* cnt, const int* slots, const char* cls);
 
     // ---- host<->device helpers
     void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream

@@ -16,21 +16,24 @@ namespace smoe {
 
 namespace {
 
-__global__ void k_ep_pack(const float* __restrict__ P, int S, long long pstride, const int* __restrict__ off, int e0,
-                          int e1, int d, float* __restrict__ y) {
+// y[j] = sum_s P[s][pos[j]] for picks j of this rank's experts (fin[j] in [e0, e1)), else 0: the
+// rank's contribution in pick order, so the sum over ranks is exact and feeds the combine directly.
+__global__ void k_ep_pack(const float* __restrict__ P, int S, long long pstride, const int* __restrict__ pos,
+                          const int* __restrict__ fin, int e0, int e1, int d, float* __restrict__ y) {
     pdl_wait();
     pdl_trigger();
-    const int r = blockIdx.x;
-    const bool mine = r >= off[e0] && r < off[e1];
-    const long long base = (long long)r * d;
+    const int j = blockIdx.x;
+    const int e = fin[j];
+    const bool mine = e >= e0 && e < e1;
+    const long long src = (long long)pos[j] * d, dst = (long long)j * d;
     for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
         if (mine)
             for (int s = 0; s < S; ++s) {
-                const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + base + i);
+                const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src + i);
                 a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
             }
-        *reinterpret_cast<float4*>(y + base + i) = a;
+        *reinterpret_cast<float4*>(y + dst + i) = a;
     }
 }
 
@@ -185,10 +188,10 @@ std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank) {
     return std::make_unique<LoopbackComm>(g, rank);
 }
 
-void launch_ep_pack(const float* P, int S, long long pstride, const int* group_off, int e0, int e1, int rows, int d,
-                    float* y_red, cudaStream_t s) {
-    if (rows <= 0) return;
-    launch_k(k_ep_pack, rows, 256, 0, s, P, S, pstride, group_off, e0, e1, d, y_red);
+void launch_ep_pack(const float* P, int S, long long pstride, const int* pos, const int* fin, int e0, int e1, int picks,
+                    int d, float* y_red, cudaStream_t s) {
+    if (picks <= 0) return;
+    launch_k(k_ep_pack, picks, 256, 0, s, P, S, pstride, pos, fin, e0, e1, d, y_red);
 }
 
 }  // namespace smoe

@@ -2,7 +2,7 @@
 //
 // Experts are sharded across G ranks in contiguous blocks (owner(e) = e / (E/G)); every rank runs the
 // dense path and the routing for all rows, computes only its own experts' rows, and the per-layer
-// expert outputs -- disjoint row supports, zeros elsewhere -- are summed across ranks.  A sum in
+// expert outputs -- one row per pick, zeros for other ranks' picks -- are summed across ranks.  A sum in
 // which every element has one non-zero term is exact in any order, so the token stream, routing and
 // ledger are bit-identical at G = 1, 2, 4, 8 (tested with the loopback transport on one GPU).
 #pragma once
@@ -32,8 +32,8 @@ LoopbackGroup* loopback_create(int world);
 void loopback_destroy(LoopbackGroup* g);
 std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank);
 
-// y_red[r] = (off[e0] <= r < off[e1]) ? sum_s P[s][r] : 0   (rows of this rank's experts are contiguous)
-void launch_ep_pack(const float* P, int S, long long pstride, const int* group_off, int e0, int e1, int rows, int d,
-                    float* y_red, cudaStream_t s);
+// y_red[j] = (e0 <= fin[j] < e1) ? sum_s P[s][pos[j]] : 0 for the T*K picks j (pick order)
+void launch_ep_pack(const float* P, int S, long long pstride, const int* pos, const int* fin, int e0, int e1, int picks,
+                    int d, float* y_red, cudaStream_t s);
 
 }  // namespace smoe

@@ -43,10 +43,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_gemm_simt(GemmArgs a) {
     pdl_wait();
     pdl_trigger();
     const int g = blockIdx.y;
-    const int slot = a.group_off ? a.group_slot[g] : a.single_slot;
+    const int slot = a.group_cnt ? a.group_slot[g] : a.single_slot;
     if (slot < 0) return;
-    const int r0 = a.group_off ? a.group_off[g] : 0;
-    const int r1 = a.group_off ? a.group_off[g + 1] : a.single_rows;
+    const int r0 = a.group_cnt ? g * a.seg : 0;
+    const int r1 = a.group_cnt ? r0 + a.group_cnt[g] : a.single_rows;
     if (r1 <= r0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = (blockIdx.x * kWarps + warp) * kRPW;

@@ -62,9 +62,9 @@ struct Phase {
 struct TcParams {
     Phase ph[2];
     int nphase;
-    const int* group_off;
+    const int* group_cnt;  // nullptr: single group {0, single_rows} -> single_slot
     const int* group_slot;
-    int G, single_rows, single_slot;
+    int G, seg, single_rows, single_slot;  // group g: rows [g*seg, g*seg + group_cnt[g])
     int n_tiles;
     int stages, b_region;  // b_region = bytes of token boxes per stage
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
@@ -156,10 +156,10 @@ __device__ __forceinline__ int units_of_phase(const TcParams& p, int ph) {
 }
 
 __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, int& r0, int& r1) {
-    if (p.group_off) {
+    if (p.group_cnt) {
         slot = p.group_slot[g];
-        r0 = p.group_off[g];
-        r1 = p.group_off[g + 1];
+        r0 = g * p.seg;
+        r1 = r0 + p.group_cnt[g];
     } else {
         slot = p.single_slot;
         r0 = 0;
@@ -314,9 +314,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ---------------- scheduler + TMA producer
             int it = 0;
             bool kernel_dep = false;  // griddepcontrol.wait done: the previous kernel's outputs are visible
+            if (p.group_cnt) {
+                // grouped launches: the unit geometry (rows per expert) is written by the gate kernel
+                // that immediately precedes this one, so it may only be read after the dependency wait
+                pdl_wait();
+                kernel_dep = true;
+            }
             for (int pub = 0;; ++pub) {
-                // dynamic work distribution: claim the next non-empty unit (unit geometry comes from the
-                // routing kernels, which completed before the kernel preceding this one could trigger)
+                // dynamic work distribution: claim the next non-empty unit (single-group geometry is
+                // host-known; grouped geometry was waited for above)
                 int u;
                 Unit w;
                 do {
@@ -536,9 +542,10 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.ph[0] = make_phase(a);
     p.nphase = b ? 2 : 1;
     if (b) p.ph[1] = make_phase(*b);
-    p.group_off = a.group_off;
+    p.group_cnt = a.group_cnt;
     p.group_slot = a.group_slot;
-    p.G = a.group_off ? a.G : 1;
+    p.G = a.group_cnt ? a.G : 1;
+    p.seg = a.seg;
     p.single_rows = a.single_rows;
     p.single_slot = a.single_slot;
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
@@ -577,9 +584,10 @@ void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s) {
 
 void launch_moe_tc(const TcGemmArgs& up, const TcGemmArgs& down, cudaStream_t s) {
     if (up.Nout <= 0 || up.rows_bound <= 0) return;
-    if (!up.group_off || !up.done || up.G > kMaxGroups)
+    if (!up.group_cnt || !up.done || up.G > kMaxGroups)
         throw Error(kInvariant, "fused expert GEMM: needs <= 64 groups and completion counters");
-    if (down.epi != kEpiStoreF32 || down.group_off != up.group_off || down.rows_bound != up.rows_bound)
+    if (down.epi != kEpiStoreF32 || down.group_cnt != up.group_cnt || down.seg != up.seg ||
+        down.rows_bound != up.rows_bound)
         throw Error(kInvariant, "fused expert GEMM: down projection must share the up projection's groups");
     if (up.epi == kEpiSwiglu) launch_phases<kEpiSwiglu, kEpiStoreF32>(up, &down, s);
     else if (up.epi == kEpiTanh) launch_phases<kEpiTanh, kEpiStoreF32>(up, &down, s);

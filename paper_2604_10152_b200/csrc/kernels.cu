@@ -162,11 +162,7 @@ __global__ void k_gate(GateArgs a) {
     }
     ss = block_sum(ss, red + 8 * 32);
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        const float v = xf[i] * inv;
-        xf[i] = v;
-        store_op<OT>(a.xa, base + i, v);
-    }
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xf[i] *= inv;
     __syncthreads();
     // gate GEMV (model.cpp:229-230): 8 experts at a time, fixed-order block reduction
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -198,124 +194,82 @@ __global__ void k_gate(GateArgs a) {
         }
         __syncthreads();
     }
-    if (threadIdx.x != 0) return;
-    // softmax (model.cpp:145-157), max-subtracted
-    float mx = gl[0];
-    bool finite = true;
-    for (int e = 0; e < E; ++e) {
-        finite &= isfinite(gl[e]);
-        if (gl[e] > mx) mx = gl[e];
-    }
-    if (!finite) atomicOr(a.flags, kFlagNonFiniteGate);
-    float* p = gl + E;
-    float sum = 0.f;
-    for (int e = 0; e < E; ++e) {
-        p[e] = expf(gl[e] - mx);
-        sum += p[e];
-    }
-    // top-K: repeated first-max selection == stable sort descending (model.cpp:159-170)
-    unsigned long long taken = 0ull;  // E <= 64
-    int chosen[16];
-    for (int k = 0; k < K; ++k) {
-        int best = -1;
-        for (int e = 0; e < E; ++e)
-            if (!((taken >> e) & 1ull) && (best < 0 || gl[e] > gl[best])) best = e;
-        taken |= 1ull << best;
-        const int pick = best;
-        int ex = pick;
-        if (a.in_draft) {
-            bool dup = false;
-            for (int j = 0; j < k; ++j) dup |= chosen[j] == pick;
-            if (!(a.in_draft[pick] && !dup)) {
-                ex = -1;
-                if (a.use_affinity) {  // nearest by (distance, index): first non-excluded rank
-                    for (int j = 0; j < a.N && ex < 0; ++j) {
-                        int c = a.rank[pick * a.N + j];
-                        if (c < 0) break;  // padded row (smaller set on this layer)
-                        bool ex_c = false;
-                        for (int q = 0; q < k; ++q) ex_c |= chosen[q] == c;
-                        if (!ex_c) ex = c;
-                    }
-                } else {  // hash surrogate (drafting.cpp:140-151)
-                    int cnt = 0;
-                    for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
-                        bool ex_c = false;
-                        for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
-                        cnt += !ex_c;
-                    }
-                    if (cnt > 0) {
-                        uint64_t h = substream(0x5eed5eedull,
-                                               ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
-                                               (uint64_t)a.row_plen[r]);
-                        int want = (int)(h % (uint64_t)cnt);
+    __shared__ int dst[16];
+    if (threadIdx.x == 0) {
+        // softmax (model.cpp:145-157), max-subtracted
+        float mx = gl[0];
+        bool finite = true;
+        for (int e = 0; e < E; ++e) {
+            finite &= isfinite(gl[e]);
+            if (gl[e] > mx) mx = gl[e];
+        }
+        if (!finite) atomicOr(a.flags, kFlagNonFiniteGate);
+        float* p = gl + E;
+        float sum = 0.f;
+        for (int e = 0; e < E; ++e) {
+            p[e] = expf(gl[e] - mx);
+            sum += p[e];
+        }
+        // top-K: repeated first-max selection == stable sort descending (model.cpp:159-170)
+        unsigned long long taken = 0ull;  // E <= 64
+        int chosen[16];
+        for (int k = 0; k < K; ++k) {
+            int best = -1;
+            for (int e = 0; e < E; ++e)
+                if (!((taken >> e) & 1ull) && (best < 0 || gl[e] > gl[best])) best = e;
+            taken |= 1ull << best;
+            const int pick = best;
+            int ex = pick;
+            if (a.in_draft) {
+                bool dup = false;
+                for (int j = 0; j < k; ++j) dup |= chosen[j] == pick;
+                if (!(a.in_draft[pick] && !dup)) {
+                    ex = -1;
+                    if (a.use_affinity) {  // nearest by (distance, index): first non-excluded rank
+                        for (int j = 0; j < a.N && ex < 0; ++j) {
+                            int c = a.rank[pick * a.N + j];
+                            if (c < 0) break;  // padded row (smaller set on this layer)
+                            bool ex_c = false;
+                            for (int q = 0; q < k; ++q) ex_c |= chosen[q] == c;
+                            if (!ex_c) ex = c;
+                        }
+                    } else {  // hash surrogate (drafting.cpp:140-151)
+                        int cnt = 0;
                         for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
                             bool ex_c = false;
                             for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
-                            if (!ex_c && want-- == 0) { ex = a.draft_sorted[j]; break; }
+                            cnt += !ex_c;
+                        }
+                        if (cnt > 0) {
+                            uint64_t h = substream(0x5eed5eedull,
+                                                   ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
+                                                   (uint64_t)a.row_plen[r]);
+                            int want = (int)(h % (uint64_t)cnt);
+                            for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
+                                bool ex_c = false;
+                                for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
+                                if (!ex_c && want-- == 0) { ex = a.draft_sorted[j]; break; }
+                            }
                         }
                     }
-                }
-                if (ex < 0) {
-                    atomicOr(a.flags, kFlagEmptyRemap);
-                    ex = pick;
+                    if (ex < 0) {
+                        atomicOr(a.flags, kFlagEmptyRemap);
+                        ex = pick;
+                    }
                 }
             }
+            chosen[k] = ex;
+            a.raw[r * K + k] = pick;
+            a.fin[r * K + k] = ex;
+            a.wgt[r * K + k] = p[pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
+            // dispatch: a row of expert ex's segment
+            const int row = ex * a.T + atomicAdd(&a.cnt[ex], 1);
+            a.pos[r * K + k] = row;
+            dst[k] = row;
         }
-        chosen[k] = ex;
-        a.raw[r * K + k] = pick;
-        a.fin[r * K + k] = ex;
-        a.wgt[r * K + k] = p[pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
-    }
-}
-
-// ------------------------------------------------------------------ K6 permutation
-__global__ void k_route(const int* __restrict__ fin, int n, int E, const int* __restrict__ slot_of,
-                        int* __restrict__ off, int* __restrict__ gslot, int* __restrict__ pos) {
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ int s[];  // fin[n], cnt[E+1]
-    int* f = s;
-    int* cnt = s + n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) f[i] = fin[i];
-    for (int i = threadIdx.x; i <= E; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[f[i]], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int e = 0; e < E; ++e) {
-            int c = cnt[e];
-            cnt[e] = run;
-            off[e] = run;
-            gslot[e] = slot_of[e];
-            run += c;
-        }
-        off[E] = run;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int e = f[i];
-        int rank = 0;
-        for (int q = 0; q < i; ++q) rank += f[q] == e;
-        pos[i] = cnt[e] + rank;
-    }
-}
-
-__global__ void k_single_group(int T, int slot, int* off, int* gslot) {
-    off[0] = 0;
-    off[1] = T;
-    gslot[0] = slot;
-}
-
-__global__ void k_gather(const uint4* __restrict__ xa, const int* __restrict__ pos, int K, int vecs,
-                         uint4* __restrict__ xp) {
-    pdl_wait();
-    pdl_trigger();
-    const int p = blockIdx.x;
-    const int t = p / K;
-    const uint4* src = xa + (long long)t * vecs;
-    uint4* dst = xp + (long long)pos[p] * vecs;
-    for (int i = threadIdx.x; i < vecs; i += blockDim.x) dst[i] = src[i];
+    for (int k = 0; k < K; ++k) store_row_op<OT>(a.xperm, (long long)dst[k] * d, xf, d, 1.0f);
 }
 
 // ------------------------------------------------------------------ K9 combine (+ next rms)
@@ -333,7 +287,7 @@ __global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P
     for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int k = 0; k < (dense ? 1 : K); ++k) {
-            const long long src = (dense ? (long long)t : (long long)pos[t * K + k]) * d + i4;
+            const long long src = (dense ? (long long)t : pos ? (long long)pos[t * K + k] : (long long)t * K + k) * d + i4;
             float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int s = 0; s < S; ++s) {
                 const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src);
@@ -542,23 +496,6 @@ void launch_gate(const GateArgs& a, cudaStream_t s) {
     const int threads = row_threads(a.d);  // one row per block: enough loads in flight for the partials
     if (a.op == kF32) launch_k(k_gate<float>, a.T, threads, smem, s, a);
     else launch_k(k_gate<__nv_bfloat16>, a.T, threads, smem, s, a);
-}
-
-void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot, int* pos,
-                  cudaStream_t s) {
-    const int n = T * K;
-    launch_k(k_route, 1, 1024, sizeof(int) * (n + E + 1), s, fin, n, E, slot_of, group_off, group_slot, pos);
-}
-
-void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaStream_t s) {
-    k_single_group<<<1, 1, 0, s>>>(T, slot, group_off, group_slot);
-}
-
-void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s) {
-    if (T <= 0) return;
-    const int vecs = d * (op == kF32 ? 4 : 2) / 16;
-    launch_k(k_gather, T * K, 128, 0, s, reinterpret_cast<const uint4*>(xa), pos, K, vecs,
-             reinterpret_cast<uint4*>(xperm));
 }
 
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,

@@ -28,9 +28,12 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T, int d, void* xa, WType op,
                       cudaStream_t s);
 
-// K4+K5 (model.cpp:229-246, drafting.cpp:123-151): fused rms + gate GEMV + bias + softmax +
-// top-K + (restricted) remap.  Writes the normalised row (operand type) for the experts, raw/final
-// picks [T][K] and the combine weight p[raw] [T][K].
+// K4+K5+K6 (model.cpp:229-246, drafting.cpp:123-151): fused rms + gate GEMV + bias + softmax +
+// top-K + (restricted) remap + dispatch.  Writes raw/final picks [T][K], the combine weight p[raw]
+// [T][K], and dispatches the normalised row (operand type) straight into its experts' segments of
+// xperm: pick (t,k) of expert e lands in row e*T + slot, slot = atomicAdd(&cnt[e], 1), and
+// pos[t*K+k] records it.  Row order inside a segment is arbitrary: every GEMM column depends only on
+// its own row, so results do not depend on it.
 struct GateArgs {
     float* x;                 // residual stream; the mix partials are added first (x += sum_s pmix[s])
     const float* pmix;
@@ -39,7 +42,9 @@ struct GateArgs {
     int T, d, E, K;
     const float* gate_w;  // [E][d]
     const float* gate_b;  // [E]
-    void* xa;             // out [T][d] operand type
+    void* xperm;          // out [E*T][d] operand type (expert segments of T rows)
+    int* cnt;             // in/out [E] rows dispatched per expert (zero on entry)
+    int* pos;             // out [T][K] xperm row of pick (t,k)
     WType op;
     int* raw;             // out [T][K]
     int* fin;             // out [T][K]
@@ -56,16 +61,9 @@ struct GateArgs {
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 
-// K6: stable (expert, token, k) permutation.  group_off [E+1], group_slot [E] (slot of each expert
-// in the weight pool via slot_of[E]), pos [T*K] = destination row of pick (t,k).
-void launch_route(const int* fin, int T, int K, int E, const int* slot_of, int* group_off, int* group_slot,
-                  int* pos, cudaStream_t s);
-// Single group {0, T} -> slot (dense layers / head / mix).
-void launch_single_group(int T, int slot, int* group_off, int* group_slot, cudaStream_t s);
-// xperm[pos[t*K+k]] = xa[t]
-void launch_gather(const void* xa, const int* pos, int T, int K, int d, void* xperm, WType op, cudaStream_t s);
 
-// K9 (model.cpp:248-257) + the next rms: y_k = sum_s P[s][pos[t,k]] (split-K partials, s in order),
+// K9 (model.cpp:248-257) + the next rms: y_k = sum_s P[s][pos[t,k]] (split-K partials, s in order;
+// pos == nullptr: row t*K+k),
 // x[t] += sum_k wgt[t,k] * y_k (k in order; dense: x[t] += y), then xa[t] = rms(x[t]).
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
                         int K, int d, int dense, void* xa, WType op, cudaStream_t s);
@@ -86,16 +84,16 @@ void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int
                    int tok_stride, const int* take, int na, int d, cudaStream_t s);
 
 // Grouped skinny GEMM on CUDA cores (f32 or bf16 weights, f32 accumulation):
-//   for group g with slot s = group_slot[g] >= 0 and rows [group_off[g], group_off[g+1]):
+//   for group g with slot s = group_slot[g] >= 0 and rows [g*seg, g*seg + group_cnt[g]):
 //     acc[r][n] = sum_k W[s][n][k] * X[r][k]       (n < Nout)
 //   epilogue per Epi.  For kEpiSwiglu, W[s] has 2*Nout rows, interleaved: 2n = w1, 2n+1 = w3.
 struct GemmArgs {
     const void* W;
     long long slot_stride;  // elements between slots
     int Nout, K;
-    const int* group_off;  // nullptr -> single group {0, single_rows} with slot single_slot
+    const int* group_cnt;  // nullptr -> single group {0, single_rows} with slot single_slot
     const int* group_slot;
-    int G;
+    int G, seg;            // G groups; group g's rows start at g*seg
     int single_rows, single_slot;
     int rows_bound;  // upper bound on rows in any group (host-known)
     const void* X;   // [rows][K] operand type

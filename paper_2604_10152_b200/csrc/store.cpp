@@ -108,11 +108,11 @@ void Engine::store_pin_sets(const std::vector<std::vector<int>>& sets) {
 }
 
 // Inside an unrestricted pass, after route(mo): fetch this layer's missing experts.
-void Engine::store_fetch_layer(int mo, int T, const int* raw_dev) {
-    int* goff = h_store + (size_t)M * E;
-    int* gslot = goff + E + 1;
+void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt_dev) {
+    int* cnt = h_store + (size_t)M * E;
+    int* gslot = cnt + E + 1;
     int* raw = gslot + E;
-    SMOE_CUDA(cudaMemcpyAsync(goff, group_off, sizeof(int) * (E + 1), cudaMemcpyDeviceToHost, stream));
+    SMOE_CUDA(cudaMemcpyAsync(cnt, cnt_dev, sizeof(int) * E, cudaMemcpyDeviceToHost, stream));
     SMOE_CUDA(cudaMemcpyAsync(raw, raw_dev, sizeof(int) * T * K, cudaMemcpyDeviceToHost, stream));
     sync();
     cudaEvent_t a, b;
@@ -121,8 +121,8 @@ void Engine::store_fetch_layer(int mo, int T, const int* raw_dev) {
     SMOE_CUDA(cudaEventRecord(a, copy_stream));
     for (int e = 0; e < E; ++e) {
         const int key = mo * E + e;
-        if (goff[e + 1] > goff[e] && h_slot_of[key] < 0) store_copy_in(key, store_take_slot(key));
-        gslot[e] = goff[e + 1] > goff[e] ? h_slot_of[key] : -1;
+        if (cnt[e] > 0 && h_slot_of[key] < 0) store_copy_in(key, store_take_slot(key));
+        gslot[e] = cnt[e] > 0 ? h_slot_of[key] : -1;
     }
     SMOE_CUDA(cudaEventRecord(b, copy_stream));
     SMOE_CUDA(cudaStreamWaitEvent(stream, b, 0));
