@@ -45,7 +45,7 @@ def args_parse():
     p.add_argument("--expert", default="swiglu3", choices=["swiglu3", "tanh2"])
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--gamma", type=int, default=4)
-    p.add_argument("--n-draft", type=int, default=4)
+    p.add_argument("--n-draft", type=int, default=0, help="0: the shape's default (4; 8 for C4, SURVEY 8)")
     p.add_argument("--e2e-tokens", type=int, default=12)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
@@ -54,7 +54,10 @@ def args_parse():
     p.add_argument("--offload-batch", type=int, default=64)
     p.add_argument("--offload-steps", type=int, default=2)
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallelism")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.n_draft == 0:
+        a.n_draft = 8 if a.shape == "c4" else 4
+    return a
 
 
 def dist_env():

@@ -164,108 +164,122 @@ __global__ void k_gate(GateArgs a) {
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
     for (int i = threadIdx.x; i < d; i += blockDim.x) xf[i] *= inv;
     __syncthreads();
-    // gate GEMV (model.cpp:229-230): 8 experts at a time, fixed-order block reduction
+    // gate GEMV (model.cpp:229-230): warp w owns experts w, w+nw, ...; each lane strides d in float4s
+    // (fixed order, then a butterfly), so every row's logits are computed identically in any pass
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int e0 = 0; e0 < E; e0 += 8) {
-        const int ne = min(8, E - e0);
-        float acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-        for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
-            const float4 xv = *reinterpret_cast<const float4*>(xf + i4);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < ne) {
-                    const float4 g = *reinterpret_cast<const float4*>(a.gate_w + (long long)(e0 + j) * d + i4);
-                    acc[j] += g.x * xv.x + g.y * xv.y + g.z * xv.z + g.w * xv.w;
-                }
+    {
+        const float4* xv = reinterpret_cast<const float4*>(xf);
+        const int d4 = d >> 2;
+        for (int e = w; e < E; e += nw) {
+            const float4* g = reinterpret_cast<const float4*>(a.gate_w + (long long)e * d);
+            float acc = 0.f;
+#pragma unroll 8
+            for (int i = lane; i < d4; i += 32) {
+                const float4 gv = g[i], x4 = xv[i];
+                acc += gv.x * x4.x + gv.y * x4.y + gv.z * x4.z + gv.w * x4.w;
             }
+            acc = warp_sum(acc);
+            if (lane == 0) gl[e] = acc + a.gate_b[e];
         }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float v = warp_sum(acc[j]);
-            if (lane == 0) red[w * 8 + j] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x < ne) {
-            float t = 0.f;
-            for (int q = 0; q < nw; ++q) t += red[q * 8 + threadIdx.x];
-            gl[e0 + threadIdx.x] = t + a.gate_b[e0 + threadIdx.x];
-        }
-        __syncthreads();
     }
+    __syncthreads();
+    // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
-    if (threadIdx.x == 0) {
-        // softmax (model.cpp:145-157), max-subtracted
-        float mx = gl[0];
-        bool finite = true;
-        for (int e = 0; e < E; ++e) {
-            finite &= isfinite(gl[e]);
-            if (gl[e] > mx) mx = gl[e];
-        }
-        if (!finite) atomicOr(a.flags, kFlagNonFiniteGate);
+    if (threadIdx.x < 32) {
+        const unsigned FULL = 0xffffffffu;
+        const int l0 = lane, l1 = lane + 32;
+        const float g0 = l0 < E ? gl[l0] : 0.f, g1 = l1 < E ? gl[l1] : 0.f;
+        const bool fin_ok = (l0 >= E || isfinite(g0)) && (l1 >= E || isfinite(g1));
+        if (!__all_sync(FULL, fin_ok) && lane == 0) atomicOr(a.flags, kFlagNonFiniteGate);
+        // softmax (model.cpp:145-157), max-subtracted; the max is exact in any order, the sum runs in
+        // expert order on lane 0
+        float mx = fmaxf(l0 < E ? g0 : -INFINITY, l1 < E ? g1 : -INFINITY);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
         float* p = gl + E;
+        if (l0 < E) p[l0] = expf(g0 - mx);
+        if (l1 < E) p[l1] = expf(g1 - mx);
+        __syncwarp();
         float sum = 0.f;
-        for (int e = 0; e < E; ++e) {
-            p[e] = expf(gl[e] - mx);
-            sum += p[e];
-        }
-        // top-K: repeated first-max selection == stable sort descending (model.cpp:159-170)
-        unsigned long long taken = 0ull;  // E <= 64
-        int chosen[16];
+        if (lane == 0)
+            for (int e = 0; e < E; ++e) sum += p[e];
+        sum = __shfl_sync(FULL, sum, 0);
+        // top-K: K rounds of a warp argmax, ties -> lower index == repeated first-max (model.cpp:159-170)
+        unsigned long long taken = 0ull, chosen = 0ull;
+        int my_pick = 0, my_ex = 0;  // lane k keeps pick k
         for (int k = 0; k < K; ++k) {
-            int best = -1;
-            for (int e = 0; e < E; ++e)
-                if (!((taken >> e) & 1ull) && (best < 0 || gl[e] > gl[best])) best = e;
-            taken |= 1ull << best;
-            const int pick = best;
+            float v = 0.f;
+            int idx = -1;
+            if (l0 < E && !((taken >> l0) & 1ull)) { v = g0; idx = l0; }
+            if (l1 < E && !((taken >> l1) & 1ull) && (idx < 0 || g1 > v)) { v = g1; idx = l1; }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ov = __shfl_xor_sync(FULL, v, o);
+                const int oi = __shfl_xor_sync(FULL, idx, o);
+                if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+            }
+            const int pick = idx;
+            taken |= 1ull << pick;
             int ex = pick;
-            if (a.in_draft) {
-                bool dup = false;
-                for (int j = 0; j < k; ++j) dup |= chosen[j] == pick;
-                if (!(a.in_draft[pick] && !dup)) {
-                    ex = -1;
-                    if (a.use_affinity) {  // nearest by (distance, index): first non-excluded rank
-                        for (int j = 0; j < a.N && ex < 0; ++j) {
-                            int c = a.rank[pick * a.N + j];
-                            if (c < 0) break;  // padded row (smaller set on this layer)
-                            bool ex_c = false;
-                            for (int q = 0; q < k; ++q) ex_c |= chosen[q] == c;
-                            if (!ex_c) ex = c;
-                        }
-                    } else {  // hash surrogate (drafting.cpp:140-151)
-                        int cnt = 0;
-                        for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
-                            bool ex_c = false;
-                            for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
-                            cnt += !ex_c;
-                        }
-                        if (cnt > 0) {
-                            uint64_t h = substream(0x5eed5eedull,
-                                                   ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
-                                                   (uint64_t)a.row_plen[r]);
-                            int want = (int)(h % (uint64_t)cnt);
-                            for (int j = 0; j < a.N && a.draft_sorted[j] >= 0; ++j) {
-                                bool ex_c = false;
-                                for (int q = 0; q < k; ++q) ex_c |= chosen[q] == a.draft_sorted[j];
-                                if (!ex_c && want-- == 0) { ex = a.draft_sorted[j]; break; }
+            if (a.in_draft && !(a.in_draft[pick] && !((chosen >> pick) & 1ull))) {
+                // restricted (draft) semantics: remap into draft \ chosen (drafting.cpp:123-151)
+                ex = -1;
+                if (a.use_affinity) {
+                    // nearest by (distance, index) = first rank entry not yet chosen; -1 pads short sets
+                    for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
+                        const int j = j0 + lane;
+                        const int c = j < a.N ? a.rank[pick * a.N + j] : -1;
+                        const unsigned pad = __ballot_sync(FULL, j < a.N && c < 0);
+                        const unsigned ok = __ballot_sync(FULL, j < a.N && c >= 0 && !((chosen >> c) & 1ull));
+                        const unsigned before_pad = pad ? (1u << (__ffs(pad) - 1)) - 1u : FULL;
+                        const unsigned m = ok & before_pad;
+                        if (m) ex = __shfl_sync(FULL, c, __ffs(m) - 1);
+                        if (pad) break;
+                    }
+                } else {  // hash surrogate (drafting.cpp:140-151): want-th non-chosen draft member
+                    int total = 0;
+                    for (int j0 = 0; j0 < a.N; j0 += 32) {
+                        const int j = j0 + lane;
+                        const int c = j < a.N ? a.draft_sorted[j] : -1;
+                        total += __popc(__ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull)));
+                    }
+                    if (total > 0) {
+                        const uint64_t h = substream(0x5eed5eedull, ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
+                                                     (uint64_t)a.row_plen[r]);
+                        int want = (int)(h % (uint64_t)total);
+                        for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
+                            const int j = j0 + lane;
+                            const int c = j < a.N ? a.draft_sorted[j] : -1;
+                            unsigned m = __ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull));
+                            const int n = __popc(m);
+                            if (want < n) {
+                                for (int q = 0; q < want; ++q) m &= m - 1;  // drop the lowest `want` members
+                                ex = __shfl_sync(FULL, c, __ffs(m) - 1);
+                            } else {
+                                want -= n;
                             }
                         }
                     }
-                    if (ex < 0) {
-                        atomicOr(a.flags, kFlagEmptyRemap);
-                        ex = pick;
-                    }
+                }
+                if (ex < 0) {
+                    if (lane == 0) atomicOr(a.flags, kFlagEmptyRemap);
+                    ex = pick;
                 }
             }
-            chosen[k] = ex;
-            a.raw[r * K + k] = pick;
-            a.fin[r * K + k] = ex;
-            a.wgt[r * K + k] = p[pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
-            // dispatch: a row of expert ex's segment
-            const int row = ex * a.T + atomicAdd(&a.cnt[ex], 1);
-            a.pos[r * K + k] = row;
-            dst[k] = row;
+            chosen |= 1ull << ex;
+            if (lane == k) {
+                my_pick = pick;
+                my_ex = ex;
+            }
+        }
+        if (lane < K) {
+            a.raw[r * K + lane] = my_pick;
+            a.fin[r * K + lane] = my_ex;
+            a.wgt[r * K + lane] = p[my_pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
+            // dispatch: lanes 0..K-1 claim their rows of the experts' segments concurrently
+            const int row = my_ex * a.T + atomicAdd(&a.cnt[my_ex], 1);
+            a.pos[r * K + lane] = row;
+            dst[lane] = row;
         }
     }
     __syncthreads();

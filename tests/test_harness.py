@@ -220,3 +220,55 @@ def test_trace_round_trip_matches_oracle_hotness(tmp_path, ref):
     assert np.array_equal(counts, o.hotness)
     from oracle.oracle import skewness
     assert float(r.stdout.split()[1]) == pytest.approx(skewness(ref, o.hotness, len(o.trace) // 4), abs=0)
+
+
+# ------------------------------------------------------------------ SPEC acceptance criteria
+def _rows(tmp_path, name, **kw):
+    out = str(tmp_path / f"{name}.csv")
+    cli("run", "--config", toy(tmp_path, f"{name}.cfg", **kw), "--out", out, check=True)
+    return list(csv.DictReader(open(out)))
+
+
+@pytest.mark.gpu
+def test_acceptance_4_coalescing_zero_speculation_bytes(tmp_path):
+    rows = _rows(tmp_path, "a4", skew=1.5, batch="1, 8, 32", seeds="0..3")
+    for r in rows:
+        assert int(r["bytes_spec"]) == 0 and int(r["bytes_total"]) == int(r["bytes_verify"])
+
+
+@pytest.mark.gpu
+def test_acceptance_5_transfer_reduction_trend(tmp_path):
+    """Skewed toy (gate_skew 1.5), B=32, 20 seeds: specmoe < caching < ondemand == overlap (mean bytes)."""
+    mean = {}
+    for engine in ("specmoe", "caching", "ondemand", "overlap"):
+        rows = _rows(tmp_path, f"a5_{engine}", skew=1.5, batch="32", seeds="0..19", engine=engine)
+        mean[engine] = np.mean([int(r["bytes_total"]) for r in rows])
+        if engine == "overlap":
+            per_seed_overlap = [int(r["bytes_total"]) for r in rows]
+        if engine == "ondemand":
+            per_seed_ondemand = [int(r["bytes_total"]) for r in rows]
+    assert mean["specmoe"] < mean["caching"] < mean["ondemand"]
+    assert per_seed_overlap == per_seed_ondemand
+
+
+@pytest.mark.gpu
+def test_acceptance_7_tau_nondecreasing_in_n(tmp_path):
+    """N sweep {2,4,8,16}: mean tau over 20 seeds is non-decreasing in N (slack 0.1)."""
+    rows = _rows(tmp_path, "a7", skew=1.5, n="2, 4, 8, 16", batch="4", seeds="0..19", gamma="5")
+    taus = [np.mean([float(r["tau"]) for r in rows if int(r["n_draft"]) == n]) for n in (2, 4, 8, 16)]
+    for a, b in zip(taus, taus[1:]):
+        assert b >= a - 0.1, taus
+    assert taus[-1] == 6.0  # identity limit (acceptance 2): N = E accepts every draft
+
+
+@pytest.mark.gpu
+def test_acceptance_6_policy_order_and_affinity(tmp_path):
+    """20 seeds on a skewed toy: random <= hot_global <= hot_temporal (slack 0.05); affinity remap >= hash."""
+    tau = {}
+    for policy in ("random", "hot_global", "hot_temporal"):
+        rows = _rows(tmp_path, f"a6_{policy}", skew=1.5, batch="8", seeds="0..19", policy=policy)
+        tau[policy] = np.mean([float(r["tau"]) for r in rows])
+    rows = _rows(tmp_path, "a6_hash", skew=1.5, batch="8", seeds="0..19", extra="use_affinity = false\n")
+    tau_hash = np.mean([float(r["tau"]) for r in rows])
+    assert tau["random"] <= tau["hot_global"] + 0.05 and tau["hot_global"] <= tau["hot_temporal"] + 0.05, tau
+    assert tau["hot_temporal"] >= tau_hash - 0.05, (tau, tau_hash)

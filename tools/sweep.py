@@ -10,13 +10,20 @@ from paper_2604_10152_b200.prompts import make_prompts  # noqa: E402
 
 batches = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,8,16,32,64").split(",")]
 gamma = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-spec = ModelSpec(num_layers=32, experts=8, top_k=2, hidden=4096, ffn=14336, vocab=32000, expert_kind=SWIGLU3)
+import os  # noqa: E402
+SHAPE = os.environ.get("SHAPE", "c2")
+if SHAPE == "c4":  # fine-grained E64 K6, layer 0 dense (C4)
+    spec = ModelSpec(num_layers=28, experts=64, top_k=6, hidden=2048, ffn=1408, vocab=102400, expert_kind=SWIGLU3,
+                     moe_mask=[0] + [1] * 27)
+else:
+    spec = ModelSpec(num_layers=32, experts=8, top_k=2, hidden=4096, ffn=14336, vocab=32000, expert_kind=SWIGLU3)
+N_DRAFT = 8 if SHAPE == "c4" else 4
 e = Engine(spec, weight_type=BF16, max_batch=max(batches), max_gamma=gamma).init_device(0)
 e.build_affinity_device()
 st = torch.cuda.ExternalStream(e.stream)
 rows = []
 for B in batches:
-    e.spec_begin(RunCfg(gamma=gamma, n_draft=4, max_new_tokens=1 << 30), make_prompts(1000, B, 8, spec.vocab))
+    e.spec_begin(RunCfg(gamma=gamma, n_draft=N_DRAFT, max_new_tokens=1 << 30), make_prompts(1000, B, 8, spec.vocab))
     for _ in range(2):
         e.spec_step()
     e.counters(reset=True)
