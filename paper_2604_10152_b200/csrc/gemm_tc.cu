@@ -71,6 +71,7 @@ struct TcParams {
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
 #ifdef SMOE_TC_BULK_A
     const uint8_t* a_ptr[2];
+    long long a_tiles[2];
 #endif
 };
 
@@ -352,7 +353,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_expect_tx(&full[s], bytes);
 #ifdef SMOE_TC_BULK_A
                     {
+#ifdef SMOE_TC_WAVE_A
+                        const long long tile = arow / BM, wave = tile / 148, lane148 = tile % 148;
+                        const long long width = min(148ll, p.a_tiles[w.phase] - wave * 148);
+                        const uint8_t* src = p.a_ptr[w.phase] +
+                                             (wave * 148 * p.ph[w.phase].num_kb + (long long)kb * width + lane148) * kABytes;
+#else
                         const uint8_t* src = p.a_ptr[w.phase] + ((long long)arow / BM * p.ph[w.phase].num_kb + kb) * kABytes;
+#endif
                         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(st)), "l"(src), "r"(kABytes), "r"(smem_u32(&full[s])) : "memory");
                     }
 #else
@@ -532,7 +540,10 @@ Phase make_phase(const TcGemmArgs& a) {
 
 template <int EPI0, int EPI1>
 void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
-    constexpr int kSmemBudget = 220 * 1024;
+#ifndef SMOE_TC_SMEM_KB
+#define SMOE_TC_SMEM_KB 220
+#endif
+    constexpr int kSmemBudget = SMOE_TC_SMEM_KB * 1024;  // stages + 1.5 KB control <= 227 KB
     static bool configured = false;
     if (!configured) {
         SMOE_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI0, EPI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -558,6 +569,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
 #ifdef SMOE_TC_BULK_A
     p.a_ptr[0] = (const uint8_t*)a.A.base;
     p.a_ptr[1] = b ? (const uint8_t*)b->A.base : nullptr;
+    p.a_tiles[0] = a.A.rows / BM;
+    p.a_tiles[1] = b ? b->A.rows / BM : 0;
 #endif
     const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
     const CUtensorMap& ma0 = tensor_map(a.A, BM);
