@@ -139,14 +139,16 @@ def forward_macs(s: dict, n_layers: int, mats: int) -> float:
     return n_layers * (d * d + d * E + K * mats * d * f) + d * V
 
 
-def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: int) -> dict:
+def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: int, steps: int = 1,
+                  warmup: int = 0) -> dict:
     """Time the reference's own CPU path on a bounded sample of the workload.
 
     Sample: a one-MoE-layer slice of the shape (full d, f, E, K, V), built by the reference's
     build_model; `threads` host threads run forward() concurrently on the shared weights; tau comes
     from one reference run_specmoe phase on the slice.  forward() is a per-layer loop, so its time is
     extrapolated to the full depth (and from the reference's 2-matrix expert to SwiGLU's 3) by its
-    multiply-add count.  tokens/s = forwards/s * tau / (2*gamma + 1)."""
+    multiply-add count.  tokens/s = forwards/s * tau / (2*gamma + 1).  With steps > 1 the slice is built
+    once and the concurrent forward is timed `warmup` + `steps` times (median of the timed ones)."""
     from oracle.oracle import LIBS, ModelSpec as OSpec, Oracle, RunCfg as ORun
     from paper_2604_10152_b200.prompts import make_prompts
     kind = "ref" if os.path.exists(LIBS["ref"]) else "port"
@@ -159,7 +161,10 @@ def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: in
     build_s = time.time() - t0
     prompt = make_prompts(0, 1, 8, full["vocab"])
     t1 = m.time_forward(prompt[0], threads=1, iters=1)
-    tp = m.time_forward(prompt[0], threads=threads, iters=1)
+    for _ in range(max(0, warmup)):
+        m.time_forward(prompt[0], threads=threads, iters=1)
+    samples = [m.time_forward(prompt[0], threads=threads, iters=1) for _ in range(max(1, steps))]
+    tp = statistics.median(samples)
     sp = m.run_specmoe(ORun(gamma=gamma, n_draft=min(n_draft, full["experts"]), max_new_tokens=gamma + 1,
                             run_seed=0), prompt)
     tau = sp.metrics["tau_mean"]
@@ -173,7 +178,8 @@ def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: in
                        f"{threads} threads x 1 forward() = {tp:.3f}s (1 thread {t1:.3f}s); tau {tau:.3f} from one "
                        f"reference run_specmoe phase (gamma {gamma}); extrapolated x{scale:.1f} by forward MACs "
                        f"to L={n_moe} {expert}; slice build {build_s:.0f}s untimed"),
-            "tau": tau, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale}
+            "tau": tau, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale,
+            "step_values": [threads * tau / ((2 * gamma + 1) * t * scale) for t in samples]}
 
 
 # ---------------------------------------------------------------- the B200 arm
@@ -184,11 +190,16 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-def ncu_traffic():
-    """dram bytes per expert-GEMM launch from the committed ncu --set full summary, if present."""
-    p = os.path.join(ROOT, "profiles", "ncu_expert_gemm.json")
+def ncu_traffic(draft_passes: int = 4):
+    """DRAM bytes per fused-MoE launch from the committed ncu --set full captures (profiles/
+    r01_ncu_fused_moe.json: one draft-pass and one verify-pass launch), weighted like the step
+    (gamma draft passes : 1 verify pass), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_fused_moe.json")
     try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
+        la = json.load(open(p))["launches"]
+        d, v = la[0], la[1]
+        mb = (draft_passes * (d["dram_read_MB"] + d["dram_write_MB"]) + v["dram_read_MB"] + v["dram_write_MB"])
+        return mb / (draft_passes + 1) * 1e6
     except Exception:
         return None
 
@@ -389,7 +400,10 @@ def run_b200(a) -> None:
         "gpu_launches": int(launches_timed),
         "roofline": {"bound": "hbm", "kernel": "k_gemm_tc (tcgen05 grouped expert GEMM)", "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                     "traffic": ncu_traffic(), "launches": prof["launches"],
+                     "traffic": ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 else None,
+                     "traffic_source": "ncu --set full, profiles/r01_ncu_fused_moe.json: dram read+write of one draft-pass "
+                                       "and one verify-pass launch, weighted gamma:1 like the step",
+                     "launches": prof["launches"],
                      "avg_launch_ms": prof["ms"] / max(1, prof["launches"]),
                      "share_of_step": prof["ms"] / ms_prof if ms_prof else None,
                      "measured_over": "profiled copy of the timed steps (events around each GEMM launch)",
@@ -422,15 +436,11 @@ def run_reference(a) -> None:
     if rank != 0:
         return
     thr = a.cpu_threads or os.cpu_count()
-    steps = []
-    cb = None
-    for _ in range(max(1, a.steps if a.steps <= 2 else 2)):
-        cb = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr)
-        steps.append(cb["value"])
-    value = statistics.median(steps)
+    cb = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr, steps=a.steps, warmup=a.warmup)
+    value = statistics.median(cb["step_values"])
     cb = dict(cb, value=value)
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": world,
-            "steps": len(steps), "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference build_model seeded weights, synthetic prompts)",
             "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert}, gamma={a.gamma}, N={a.n_draft}, "
                                    f"reference CPU path (oracle/_ref) on {thr} host threads",
