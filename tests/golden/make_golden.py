@@ -81,6 +81,11 @@ def main():
                     os.path.join(ROOT, "tests", "cpp", "caller.cpp")] +
                    sorted(__import__("glob").glob("/root/reference/proj/core/src/*.cpp")) + ["-o", exe], check=True)
     gold["cpp_caller"] = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+    exe = os.path.join(ROOT, "oracle", "_ref", "caller_sampling_ref")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I/root/reference/proj/core/include",
+                    os.path.join(ROOT, "tests", "cpp", "caller_sampling.cpp")] +
+                   sorted(__import__("glob").glob("/root/reference/proj/core/src/*.cpp")) + ["-o", exe], check=True)
+    gold["cpp_caller_sampling"] = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
 
     for k, v in gold.items():
         with open(os.path.join(OUT, f"{k}.json"), "w") as f:
