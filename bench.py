@@ -190,11 +190,11 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-def ncu_traffic(draft_passes: int = 4):
-    """DRAM bytes per fused-MoE launch from the committed ncu --set full captures (profiles/
-    r01_ncu_fused_moe.json: one draft-pass and one verify-pass launch), weighted like the step
-    (gamma draft passes : 1 verify pass), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_fused_moe.json")
+def ncu_traffic(draft_passes: int = 4, name: str = "r01_ncu_fused_moe.json"):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu --set full capture (profiles/
+    <name>: one draft-pass and one verify-pass launch), weighted like the step (gamma draft passes : 1
+    verify pass), or None."""
+    p = os.path.join(ROOT, "profiles", name)
     try:
         la = json.load(open(p))["launches"]
         d, v = la[0], la[1]
@@ -350,6 +350,7 @@ def run_b200(a) -> None:
     prof = eng.profile_read("expert_gemm")
     dense = eng.profile_read("dense_gemm")
     head = eng.profile_read("head_gemm")
+    pas = eng.profile_read("pass")
     res = eng.spec_end()
     ms, tokens = reduce_over_ranks(ms, tokens, sum_tokens=not ep)
 
@@ -373,7 +374,25 @@ def run_b200(a) -> None:
             dist.destroy_process_group()
         return
     pk = peaks()
-    achieved = cnt["alg_expert_bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] > 0 else 0.0
+    if pas["launches"] > 0:
+        # persistent pass kernel (every layer of a pass in one launch): its algorithmic bytes are the
+        # touched expert weights plus the Mix (and dense-FFN) weights of every pass; the head GEMM is a
+        # separate launch
+        head_bytes = float(head["launches"]) * spec.vocab * spec.hidden * 2
+        alg_bytes = cnt["alg_expert_bytes"] + cnt["alg_dense_bytes"] - head_bytes
+        dom = pas
+        roof_kernel = "k_pass_tc (persistent pass kernel: Mix GEMM, gate/top-K/remap/dispatch, fused SwiGLU expert GEMMs, combine+rms for all 32 layers; tcgen05/TMEM/TMA)"
+        roof_alg = "per pass: distinct (layer, expert) touched x 3*d*f*2 B + L*d*d*2 B Mix weights (bf16)"
+        traffic = ncu_traffic(a.gamma, "r02_ncu_pass.json") if a.shape == "c2" and a.batch == 64 else None
+        traffic_src = "ncu --set full, profiles/r02_ncu_pass.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
+    else:
+        alg_bytes = cnt["alg_expert_bytes"]
+        dom = prof
+        roof_kernel = "k_gemm_tc (tcgen05 grouped expert GEMM)"
+        roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
+        traffic = ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 else None
+        traffic_src = "ncu --set full, profiles/r01_ncu_fused_moe.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
+    achieved = alg_bytes / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
     line = {
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
@@ -398,18 +417,17 @@ def run_b200(a) -> None:
                 "note": f"run_specmoe via the C ABI, {a.e2e_tokens} new tokens per sequence, host prompts in / host "
                         f"tokens out, per-phase control copies inside"},
         "gpu_launches": int(launches_timed),
-        "roofline": {"bound": "hbm", "kernel": "k_gemm_tc (tcgen05 grouped expert GEMM)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                     "traffic": ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 else None,
-                     "traffic_source": "ncu --set full, profiles/r01_ncu_fused_moe.json: dram read+write of one draft-pass "
-                                       "and one verify-pass launch, weighted gamma:1 like the step",
-                     "launches": prof["launches"],
-                     "avg_launch_ms": prof["ms"] / max(1, prof["launches"]),
-                     "share_of_step": prof["ms"] / ms_prof if ms_prof else None,
-                     "measured_over": "profiled copy of the timed steps (events around each GEMM launch)",
-                     "algorithmic_bytes": "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "launches": dom["launches"],
+                     "avg_launch_ms": dom["ms"] / max(1, dom["launches"]),
+                     "algorithmic_bytes_per_launch": alg_bytes / max(1, dom["launches"]),
+                     "share_of_step": dom["ms"] / ms_prof if ms_prof else None,
+                     "measured_over": "profiled copy of the timed steps (CUDA events around each launch on the engine stream)",
+                     "algorithmic_bytes": roof_alg,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
-        "breakdown_ms": {"expert_gemm": prof["ms"], "dense_gemm": dense["ms"], "head_gemm": head["ms"],
+        "breakdown_ms": {"pass_kernel": pas["ms"], "expert_gemm": prof["ms"], "dense_gemm": dense["ms"], "head_gemm": head["ms"],
                          "profiled_steps_total": ms_prof, "timed_steps_total": ms},
         "clocks": clocks,
     }

@@ -68,6 +68,26 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+// Pinned float arithmetic for the row reductions shared by the per-layer kernels (kernels.cu) and the
+// pass kernel (pass_tc.cu): both evaluate exactly these operations in exactly the same reduction tree,
+// so a row's results are bit-identical whichever launch strategy computed it.
+#ifdef __CUDACC__
+__device__ __forceinline__ float sumsq4(const float4 v) {
+    return __fmaf_rn(v.w, v.w, __fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x))));
+}
+__device__ __forceinline__ float dot4f(const float4 a, const float4 b) {
+    return __fmaf_rn(a.w, b.w, __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, __fmul_rn(a.x, b.x))));
+}
+__device__ __forceinline__ void axpy4(float4& acc, float w, const float4 y) {
+    acc.x = __fmaf_rn(w, y.x, acc.x);
+    acc.y = __fmaf_rn(w, y.y, acc.y);
+    acc.z = __fmaf_rn(w, y.z, acc.z);
+    acc.w = __fmaf_rn(w, y.w, acc.w);
+}
+#endif
+// threads per row of the per-layer row kernels (and the virtual block the pass kernel emulates)
+__host__ __device__ inline int row_threads(int d) { return d >= 4096 ? 1024 : d >= 1024 ? 512 : 256; }
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // Programmatic dependent launch (PDL).  Every hot-path kernel starts with pdl_wait() (no-op when not

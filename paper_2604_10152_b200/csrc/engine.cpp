@@ -187,6 +187,9 @@ Engine::Engine(const smoe_engine_config& c) {
     moe_done = dalloc<int>(128);
     SMOE_CUDA(cudaMemset(moe_done, 0, 128 * sizeof(int)));
     if (const char* v = getenv("SMOE_FUSED_MOE")) fuse_moe = atoi(v) != 0;
+    if (const char* v = getenv("SMOE_PASS_KERNEL")) pass_kernel = atoi(v) != 0;
+    if (const char* v = getenv("SMOE_PASS_MAX_ROWS")) pass_kernel_max_rows = atoi(v);
+    if (const char* v = getenv("SMOE_PASS_MIN_ROWS")) pass_kernel_min_rows = atoi(v);
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
@@ -207,7 +210,7 @@ Engine::~Engine() {
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
     fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
-    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
+    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
     fr(stage_up); fr(stage_down);
@@ -663,6 +666,20 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     // K1+K2: x0 and the first rms
     launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
                   stream);
+    if (pass_kernel && fuse_moe && T >= pass_kernel_min_rows && T <= pass_kernel_max_rows && pass_kernel_supported(*this)) {
+        // every layer in one persistent launch (pass_tc.cu), then the head and the argmax
+        {
+            ProfScope ps(*this, "pass");
+            launch_pass_tc(*this, T, restricted, use_aff, log_slot);
+        }
+        gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, 0, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32,
+             "head_gemm", (double)V * d * ws);
+        launch_argmax(logits, T, V, amax, flags, stream);
+        SMOE_CUDA(cudaGetLastError());
+        launches += 5;
+        alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
+        return;
+    }
     const double wbytes_dd = (double)d * d * ws;
     const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;

@@ -182,6 +182,11 @@ public:
     int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][2]
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
+    int pass_kernel = 1;         // one persistent launch per pass (pass_tc.cu; env SMOE_PASS_KERNEL=0: per-layer)
+    // row range of the passes that use it (measured on the C2 shape, profiles/r02_pass_kernel.md): at
+    // T < 16 the expert phase is short and the per-layer launches win; above, the pass kernel wins
+    int pass_kernel_min_rows = 16, pass_kernel_max_rows = 1 << 30;
+    int* pass_ctr = nullptr;     // pass kernel dependency counters (self-resetting)
     unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
     size_t scratch64_n = 0;
@@ -248,6 +253,10 @@ public:
     // stepped loop
     std::unique_ptr<SpecState, SpecStateDeleter> st;
 };
+
+// pass_tc.cu: the whole pass (all layers) as one persistent tcgen05 kernel (bf16, HBM-resident, 1 GPU)
+bool pass_kernel_supported(const Engine& e);
+void launch_pass_tc(Engine& e, int T, bool restricted, int use_aff, int log_slot);
 
 // loop.cpp
 RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);

@@ -1,0 +1,112 @@
+// gate_dev.cuh -- K5/K6 selection shared by k_gate (kernels.cu) and the pass kernel (pass_tc.cu):
+// softmax (model.cpp:145-157), top-K with ties -> lower index (model.cpp:159-170), restricted-mode
+// remap (drafting.cpp:123-151) and the dispatch of each pick into its expert's segment.
+#pragma once
+#include "kernels.h"
+
+namespace smoe {
+
+// Called by ONE full warp for row r.  gl[0..E) = gate logits incl. bias; gl[E..2E) is scratch for
+// the softmax numerators.  Writes raw/fin/wgt/pos of row r and dst[k] = the xperm row of pick k.
+__device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float* gl, int* dst) {
+    const int lane = threadIdx.x & 31, E = a.E, K = a.K;
+    {
+        const unsigned FULL = 0xffffffffu;
+        const int l0 = lane, l1 = lane + 32;
+        const float g0 = l0 < E ? gl[l0] : 0.f, g1 = l1 < E ? gl[l1] : 0.f;
+        const bool fin_ok = (l0 >= E || isfinite(g0)) && (l1 >= E || isfinite(g1));
+        if (!__all_sync(FULL, fin_ok) && lane == 0) atomicOr(a.flags, kFlagNonFiniteGate);
+        // softmax (model.cpp:145-157), max-subtracted; the max is exact in any order, the sum runs in
+        // expert order on lane 0
+        float mx = fmaxf(l0 < E ? g0 : -INFINITY, l1 < E ? g1 : -INFINITY);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        float* p = gl + E;
+        if (l0 < E) p[l0] = expf(g0 - mx);
+        if (l1 < E) p[l1] = expf(g1 - mx);
+        __syncwarp();
+        float sum = 0.f;
+        if (lane == 0)
+            for (int e = 0; e < E; ++e) sum += p[e];
+        sum = __shfl_sync(FULL, sum, 0);
+        // top-K: K rounds of a warp argmax, ties -> lower index == repeated first-max (model.cpp:159-170)
+        unsigned long long taken = 0ull, chosen = 0ull;
+        int my_pick = 0, my_ex = 0;  // lane k keeps pick k
+        for (int k = 0; k < K; ++k) {
+            float v = 0.f;
+            int idx = -1;
+            if (l0 < E && !((taken >> l0) & 1ull)) { v = g0; idx = l0; }
+            if (l1 < E && !((taken >> l1) & 1ull) && (idx < 0 || g1 > v)) { v = g1; idx = l1; }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ov = __shfl_xor_sync(FULL, v, o);
+                const int oi = __shfl_xor_sync(FULL, idx, o);
+                if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
+            }
+            const int pick = idx;
+            taken |= 1ull << pick;
+            int ex = pick;
+            if (a.in_draft && !(a.in_draft[pick] && !((chosen >> pick) & 1ull))) {
+                // restricted (draft) semantics: remap into draft \ chosen (drafting.cpp:123-151)
+                ex = -1;
+                if (a.use_affinity) {
+                    // nearest by (distance, index) = first rank entry not yet chosen; -1 pads short sets
+                    for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
+                        const int j = j0 + lane;
+                        const int c = j < a.N ? a.rank[pick * a.N + j] : -1;
+                        const unsigned pad = __ballot_sync(FULL, j < a.N && c < 0);
+                        const unsigned ok = __ballot_sync(FULL, j < a.N && c >= 0 && !((chosen >> c) & 1ull));
+                        const unsigned before_pad = pad ? (1u << (__ffs(pad) - 1)) - 1u : FULL;
+                        const unsigned m = ok & before_pad;
+                        if (m) ex = __shfl_sync(FULL, c, __ffs(m) - 1);
+                        if (pad) break;
+                    }
+                } else {  // hash surrogate (drafting.cpp:140-151): want-th non-chosen draft member
+                    int total = 0;
+                    for (int j0 = 0; j0 < a.N; j0 += 32) {
+                        const int j = j0 + lane;
+                        const int c = j < a.N ? a.draft_sorted[j] : -1;
+                        total += __popc(__ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull)));
+                    }
+                    if (total > 0) {
+                        const uint64_t h = substream(0x5eed5eedull, ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
+                                                     (uint64_t)a.row_plen[r]);
+                        int want = (int)(h % (uint64_t)total);
+                        for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
+                            const int j = j0 + lane;
+                            const int c = j < a.N ? a.draft_sorted[j] : -1;
+                            unsigned m = __ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull));
+                            const int n = __popc(m);
+                            if (want < n) {
+                                for (int q = 0; q < want; ++q) m &= m - 1;  // drop the lowest `want` members
+                                ex = __shfl_sync(FULL, c, __ffs(m) - 1);
+                            } else {
+                                want -= n;
+                            }
+                        }
+                    }
+                }
+                if (ex < 0) {
+                    if (lane == 0) atomicOr(a.flags, kFlagEmptyRemap);
+                    ex = pick;
+                }
+            }
+            chosen |= 1ull << ex;
+            if (lane == k) {
+                my_pick = pick;
+                my_ex = ex;
+            }
+        }
+        if (lane < K) {
+            a.raw[r * K + lane] = my_pick;
+            a.fin[r * K + lane] = my_ex;
+            a.wgt[r * K + lane] = p[my_pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
+            // dispatch: lanes 0..K-1 claim their rows of the experts' segments concurrently
+            const int row = my_ex * a.T + atomicAdd(&a.cnt[my_ex], 1);
+            a.pos[r * K + lane] = row;
+            dst[lane] = row;
+        }
+        }
+}
+
+}  // namespace smoe

@@ -31,33 +31,14 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
+#include <cstdio>
 
-#include "engine.h"
+#include "tc_common.cuh"
 
 namespace smoe {
 namespace {
-
-constexpr int BM = 128;
-constexpr int BK = 64;        // 64 bf16 = 128 B = one swizzle-atom row
-constexpr int BN_MAX = 256;   // max tokens per unit (MMA N)
-constexpr int BOX_N = 32;     // token rows per TMA box
-constexpr int kThreads = 192;
-constexpr int kMaxStages = 12;
-constexpr int kABytes = BM * BK * 2;
-constexpr int kBoxBytes = BOX_N * BK * 2;
-constexpr int kTmemCols = 512;  // 2 accumulators x BN_MAX
-
-constexpr int kRing = 8;        // unit ids published by the producer to the MMA / epilogue roles
-constexpr int kMaxGroups = 64;  // completion counters per two-phase launch
-
-struct Phase {
-    int Nrows;  // valid weight rows per slot to compute (Nout, or 2*Nout for SwiGLU)
-    long long a_rows_per_slot;
-    int m_tiles, splits, kb_per_split, num_kb;
-    void* Y;
-    int ldy;
-    long long split_stride;  // elements between split-K partial outputs
-};
+using namespace tc;
 
 struct TcParams {
     Phase ph[2];
@@ -69,88 +50,30 @@ struct TcParams {
     int stages, b_region;  // b_region = bytes of token boxes per stage
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
+    int tr;                // trace slot (SMOE_TC_TRACE builds)
 #ifdef SMOE_TC_BULK_A
     const uint8_t* a_ptr[2];
     long long a_tiles[2];
 #endif
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+#ifdef SMOE_TC_TRACE
+// Timeline instrumentation (tools/tc_trace.py; variant builds only): per launch, per unit
+// {cta, t_claim, t_tma_done, t_mma_first, t_mma_done, t_epi_done} and per CTA {t_start, t_end}, globaltimer ns.
+constexpr int kTrLaunches = 192, kTrUnits = 8192, kTrCtas = 160;
+struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done; };
+__device__ TrUnit g_tr_unit[kTrLaunches][kTrUnits];
+__device__ long long g_tr_cta[kTrLaunches][kTrCtas][2];
+__device__ int g_tr_meta[kTrLaunches][4];  // total units, nphase, T rows bound, grid
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Bounded wait: a pipeline bug traps (context error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    const long long t0 = clock64();
-    while (true) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(parity)
-            : "memory");
-        if (done) return;
-        if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s
-    }
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void proxy_fence_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// K-major operand tile, 128-byte swizzle: 128-B rows, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// kind::f16 instruction descriptor: D f32, A/B bf16, K-major, N>>3 at [17,23), M>>4 at [24,29).
-__device__ __forceinline__ uint32_t idesc_bf16(int m, int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
-}
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accum)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-struct Unit {
-    int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks;
-};
+#define TR(x) x
+#else
+#define TR(x)
+#endif
 
 __device__ __forceinline__ int units_of_phase(const TcParams& p, int ph) {
     return p.G * p.n_tiles * p.ph[ph].m_tiles * p.ph[ph].splits;
@@ -223,39 +146,8 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
     }
     if (u < 0) return false;
     decode_unit(p, u, w);
+    w.id = u;
     return true;
-}
-
-// One 16-column TMEM chunk of a finished accumulator -> the phase's output.
-template <int EPI>
-__device__ __forceinline__ void epilogue_store(const Phase& P, const Unit& w, int row, int lane, int c,
-                                               const uint32_t* v) {
-    if (EPI == kEpiSwiglu) {
-        // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const float mine = __uint_as_float(v[j]);
-            const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-            if (!(lane & 1) && row < P.Nrows && c + j < w.n_valid) {
-                const float h = mine / (1.0f + expf(-mine)) * other;
-                reinterpret_cast<__nv_bfloat16*>(P.Y)[(long long)(w.n0 + c + j) * P.ldy + (row >> 1)] =
-                    __float2bfloat16_rn(h);
-            }
-        }
-    } else if (row < P.Nrows) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (c + j >= w.n_valid) break;
-            const long long o = (long long)(w.n0 + c + j) * P.ldy + row;
-            const float a = __uint_as_float(v[j]);
-            if (EPI == kEpiStoreF32)
-                reinterpret_cast<float*>(P.Y)[o + (long long)w.ks * P.split_stride] = a;
-            else if (EPI == kEpiResidAdd)
-                reinterpret_cast<float*>(P.Y)[o] += a;
-            else
-                reinterpret_cast<__nv_bfloat16*>(P.Y)[o] = __float2bfloat16_rn(tanhf(a));
-        }
-    }
 }
 
 template <int EPI0, int EPI1>
@@ -266,6 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int stages = p.stages;
     const int stage_bytes = kABytes + p.b_region;
     const int total_units = units_of_phase(p, 0) + (p.nphase > 1 ? units_of_phase(p, 1) : 0);
+    TR(const int trs = p.tr % kTrLaunches; if (threadIdx.x == 0) {
+        g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
+        if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, 0); g_tr_meta[trs][3] = gridDim.x; }
+    })
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -329,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 do {
                     u = atomicAdd(&p.sched[0], 1);
                 } while (u < total_units && !decode_unit(p, u, w));
+                TR(if (u < total_units && u < kTrUnits) { g_tr_unit[trs][u].cta = blockIdx.x | ((long long)p.tr << 32); g_tr_unit[trs][u].claim = gtimer(); })
                 const int r = pub % kRing;
                 mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
                 ring[r] = u < total_units ? u : -1;
@@ -343,8 +240,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
                 // boxes are issued; at most `stages` of them are held back.
                 const int need = w.phase ? phase0_units_of_group(p, w.g) : 0;
-                bool ready = kernel_dep && (w.phase == 0 || ld_acquire(&p.done[w.g]) >= need);
-                if (ready && w.phase) proxy_fence_async();
+                bool ready = kernel_dep && (w.phase == 0 || ld_relaxed(&p.done[w.g]) >= need);
+                if (ready && w.phase) {
+                    fence_acquire();
+                    proxy_fence_async();
+                }
                 const int pend_it = it;
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
                     const int s = it % stages;
@@ -377,11 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         kernel_dep = true;
                     }
                     if (w.phase) {
-                        const long long t0 = clock64();
-                        while (ld_acquire(&p.done[w.g]) < need) {
-                            __nanosleep(100);
-                            if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s: a lost publication
-                        }
+                        spin_until(&p.done[w.g], need);
                         proxy_fence_async();  // generic-proxy stores of H before async-proxy (TMA) reads
                     }
                     ready = true;
@@ -392,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_2d(mB, &full[j2 % stages], sp + j * kBoxBytes, k2 * BK, w.n0 + j * BOX_N);
                     }
                 }
+                TR(if (u < kTrUnits) g_tr_unit[trs][u].tma_done = gtimer();)
             }
             if (!kernel_dep) pdl_wait();
         }
@@ -411,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = it % stages;
                     mbar_wait(&full[s], (uint32_t)((it / stages) & 1));
                     tc_fence_after();
+                    TR(if (kb == w.kb0) g_tr_unit[trs][w.id % kTrUnits].mma_first = gtimer();)
                     const uint32_t a_base = smem_u32(smem + s * stage_bytes);
                     const uint32_t b_base = a_base + kABytes;
 #pragma unroll
@@ -420,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&acc_full[acc]);
+                TR(g_tr_unit[trs][w.id % kTrUnits].mma_done = gtimer();)
                 ++cnt;
             }
         }
@@ -453,11 +352,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_done = gtimer();)
             ++cnt;
         }
     }
     tc_fence_before();
     __syncthreads();
+    TR(if (threadIdx.x == 0) g_tr_cta[trs][blockIdx.x % kTrCtas][1] = gtimer();)
     if (threadIdx.x == 0) {  // last CTA out resets the scheduler (and counters) for the next launch
         __threadfence();
         if (atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1) {
@@ -474,7 +375,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+}  // namespace
+
 // ------------------------------------------------------------------ host side
+namespace tc {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -537,6 +441,11 @@ Phase make_phase(const TcGemmArgs& a) {
     P.split_stride = a.split_stride;
     return P;
 }
+}  // namespace tc
+
+namespace {
+using namespace tc;
+int g_launch_no = 0;  // trace slot of the next launch (SMOE_TC_TRACE builds)
 
 template <int EPI0, int EPI1>
 void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
@@ -566,6 +475,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.stages = std::max(2, std::min(kMaxStages, (kSmemBudget - 1024 - 512) / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
+    p.tr = g_launch_no++;
 #ifdef SMOE_TC_BULK_A
     p.a_ptr[0] = (const uint8_t*)a.A.base;
     p.a_ptr[1] = b ? (const uint8_t*)b->A.base : nullptr;
@@ -608,3 +518,29 @@ void launch_moe_tc(const TcGemmArgs& up, const TcGemmArgs& down, cudaStream_t s)
 }
 
 }  // namespace smoe
+
+// Trace dump for tools/tc_trace.py (SMOE_TC_TRACE variant builds; returns -1 otherwise).
+extern "C" int smoe_tc_trace_dump(const char* path) {
+#ifdef SMOE_TC_TRACE
+    using namespace smoe;
+    std::vector<TrUnit> u((size_t)kTrLaunches * kTrUnits);
+    std::vector<long long> c((size_t)kTrLaunches * kTrCtas * 2);
+    std::vector<int> m((size_t)kTrLaunches * 4);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    cudaMemcpyFromSymbol(u.data(), g_tr_unit, u.size() * sizeof(TrUnit));
+    cudaMemcpyFromSymbol(c.data(), g_tr_cta, c.size() * sizeof(long long));
+    cudaMemcpyFromSymbol(m.data(), g_tr_meta, m.size() * sizeof(int));
+    FILE* fp = fopen(path, "wb");
+    if (!fp) return -3;
+    int hdr[3] = {kTrLaunches, kTrUnits, kTrCtas};
+    fwrite(hdr, sizeof(hdr), 1, fp);
+    fwrite(m.data(), sizeof(int), m.size(), fp);
+    fwrite(c.data(), sizeof(long long), c.size(), fp);
+    fwrite(u.data(), sizeof(TrUnit), u.size(), fp);
+    fclose(fp);
+    return 0;
+#else
+    (void)path;
+    return -1;
+#endif
+}

@@ -6,6 +6,7 @@
 #include <cstdlib>
 
 #include "kernels.h"
+#include "gate_dev.cuh"
 
 namespace smoe {
 
@@ -129,7 +130,7 @@ __global__ void k_resid_rms(float* __restrict__ x, const float* __restrict__ P, 
         v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
         *reinterpret_cast<float4*>(x + base + i4) = v;
         *reinterpret_cast<float4*>(row + i4) = v;
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        ss = __fadd_rn(ss, sumsq4(v));
     }
     ss = block_sum(ss, red);
     store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
@@ -158,7 +159,7 @@ __global__ void k_gate(GateArgs a) {
         v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
         *reinterpret_cast<float4*>(a.x + base + i4) = v;
         *reinterpret_cast<float4*>(xf + i4) = v;
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        ss = __fadd_rn(ss, sumsq4(v));
     }
     ss = block_sum(ss, red + 8 * 32);
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
@@ -175,8 +176,7 @@ __global__ void k_gate(GateArgs a) {
             float acc = 0.f;
 #pragma unroll 8
             for (int i = lane; i < d4; i += 32) {
-                const float4 gv = g[i], x4 = xv[i];
-                acc += gv.x * x4.x + gv.y * x4.y + gv.z * x4.z + gv.w * x4.w;
+                acc = __fadd_rn(acc, dot4f(g[i], xv[i]));
             }
             acc = warp_sum(acc);
             if (lane == 0) gl[e] = acc + a.gate_b[e];
@@ -185,103 +185,7 @@ __global__ void k_gate(GateArgs a) {
     __syncthreads();
     // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
-    if (threadIdx.x < 32) {
-        const unsigned FULL = 0xffffffffu;
-        const int l0 = lane, l1 = lane + 32;
-        const float g0 = l0 < E ? gl[l0] : 0.f, g1 = l1 < E ? gl[l1] : 0.f;
-        const bool fin_ok = (l0 >= E || isfinite(g0)) && (l1 >= E || isfinite(g1));
-        if (!__all_sync(FULL, fin_ok) && lane == 0) atomicOr(a.flags, kFlagNonFiniteGate);
-        // softmax (model.cpp:145-157), max-subtracted; the max is exact in any order, the sum runs in
-        // expert order on lane 0
-        float mx = fmaxf(l0 < E ? g0 : -INFINITY, l1 < E ? g1 : -INFINITY);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-        float* p = gl + E;
-        if (l0 < E) p[l0] = expf(g0 - mx);
-        if (l1 < E) p[l1] = expf(g1 - mx);
-        __syncwarp();
-        float sum = 0.f;
-        if (lane == 0)
-            for (int e = 0; e < E; ++e) sum += p[e];
-        sum = __shfl_sync(FULL, sum, 0);
-        // top-K: K rounds of a warp argmax, ties -> lower index == repeated first-max (model.cpp:159-170)
-        unsigned long long taken = 0ull, chosen = 0ull;
-        int my_pick = 0, my_ex = 0;  // lane k keeps pick k
-        for (int k = 0; k < K; ++k) {
-            float v = 0.f;
-            int idx = -1;
-            if (l0 < E && !((taken >> l0) & 1ull)) { v = g0; idx = l0; }
-            if (l1 < E && !((taken >> l1) & 1ull) && (idx < 0 || g1 > v)) { v = g1; idx = l1; }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const float ov = __shfl_xor_sync(FULL, v, o);
-                const int oi = __shfl_xor_sync(FULL, idx, o);
-                if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
-            }
-            const int pick = idx;
-            taken |= 1ull << pick;
-            int ex = pick;
-            if (a.in_draft && !(a.in_draft[pick] && !((chosen >> pick) & 1ull))) {
-                // restricted (draft) semantics: remap into draft \ chosen (drafting.cpp:123-151)
-                ex = -1;
-                if (a.use_affinity) {
-                    // nearest by (distance, index) = first rank entry not yet chosen; -1 pads short sets
-                    for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
-                        const int j = j0 + lane;
-                        const int c = j < a.N ? a.rank[pick * a.N + j] : -1;
-                        const unsigned pad = __ballot_sync(FULL, j < a.N && c < 0);
-                        const unsigned ok = __ballot_sync(FULL, j < a.N && c >= 0 && !((chosen >> c) & 1ull));
-                        const unsigned before_pad = pad ? (1u << (__ffs(pad) - 1)) - 1u : FULL;
-                        const unsigned m = ok & before_pad;
-                        if (m) ex = __shfl_sync(FULL, c, __ffs(m) - 1);
-                        if (pad) break;
-                    }
-                } else {  // hash surrogate (drafting.cpp:140-151): want-th non-chosen draft member
-                    int total = 0;
-                    for (int j0 = 0; j0 < a.N; j0 += 32) {
-                        const int j = j0 + lane;
-                        const int c = j < a.N ? a.draft_sorted[j] : -1;
-                        total += __popc(__ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull)));
-                    }
-                    if (total > 0) {
-                        const uint64_t h = substream(0x5eed5eedull, ((uint64_t)a.moe_ordinal << 32) | (uint32_t)pick,
-                                                     (uint64_t)a.row_plen[r]);
-                        int want = (int)(h % (uint64_t)total);
-                        for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
-                            const int j = j0 + lane;
-                            const int c = j < a.N ? a.draft_sorted[j] : -1;
-                            unsigned m = __ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull));
-                            const int n = __popc(m);
-                            if (want < n) {
-                                for (int q = 0; q < want; ++q) m &= m - 1;  // drop the lowest `want` members
-                                ex = __shfl_sync(FULL, c, __ffs(m) - 1);
-                            } else {
-                                want -= n;
-                            }
-                        }
-                    }
-                }
-                if (ex < 0) {
-                    if (lane == 0) atomicOr(a.flags, kFlagEmptyRemap);
-                    ex = pick;
-                }
-            }
-            chosen |= 1ull << ex;
-            if (lane == k) {
-                my_pick = pick;
-                my_ex = ex;
-            }
-        }
-        if (lane < K) {
-            a.raw[r * K + lane] = my_pick;
-            a.fin[r * K + lane] = my_ex;
-            a.wgt[r * K + lane] = p[my_pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
-            // dispatch: lanes 0..K-1 claim their rows of the experts' segments concurrently
-            const int row = my_ex * a.T + atomicAdd(&a.cnt[my_ex], 1);
-            a.pos[r * K + lane] = row;
-            dst[lane] = row;
-        }
-    }
+    if (threadIdx.x < 32) gate_select_warp(a, r, gl, dst);
     __syncthreads();
     for (int k = 0; k < K; ++k) store_row_op<OT>(a.xperm, (long long)dst[k] * d, xf, d, 1.0f);
 }
@@ -307,18 +211,14 @@ __global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P
                 const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src);
                 y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
             }
-            if (dense) {
-                acc = y;
-            } else {
-                const float wk = wgt[t * K + k];
-                acc.x += wk * y.x; acc.y += wk * y.y; acc.z += wk * y.z; acc.w += wk * y.w;
-            }
+            if (dense) acc = y;
+            else axpy4(acc, wgt[t * K + k], y);
         }
         float4 v = *reinterpret_cast<const float4*>(x + base + i4);
         v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
         *reinterpret_cast<float4*>(x + base + i4) = v;
         *reinterpret_cast<float4*>(row + i4) = v;
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        ss = __fadd_rn(ss, sumsq4(v));
     }
     ss = block_sum(ss, red);
     store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
@@ -475,7 +375,6 @@ void launch_x0(const double* emb64, const double* seq_sum, const int* seq_len, c
                            row_plen);
 }
 
-static int row_threads(int d) { return d >= 4096 ? 1024 : d >= 1024 ? 512 : 256; }
 
 void launch_x0_rms(const double* emb64, const double* seq_sum, const int* seq_len, const int* pend, int pend_stride,
                    const int* row_seq, const int* row_extra, int extra_uniform, int T, int d, float* x, int* row_plen,

@@ -1,0 +1,181 @@
+// tc_common.cuh -- tcgen05 / TMEM / TMA / mbarrier building blocks shared by the grouped GEMM
+// (gemm_tc.cu) and the persistent pass kernel (pass_tc.cu).  sm_100a only.
+#pragma once
+#include <cuda.h>
+
+#include "engine.h"
+
+namespace smoe {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;        // 64 bf16 = 128 B = one swizzle-atom row
+constexpr int BN_MAX = 256;   // max tokens per unit (MMA N)
+constexpr int BOX_N = 32;     // token rows per TMA box
+constexpr int kThreads = 192;
+constexpr int kMaxStages = 12;
+constexpr int kABytes = BM * BK * 2;
+constexpr int kBoxBytes = BOX_N * BK * 2;
+constexpr int kTmemCols = 512;  // 2 accumulators x BN_MAX
+
+constexpr int kRing = 8;        // unit ids published by the producer to the MMA / epilogue roles
+constexpr int kMaxGroups = 64;  // completion counters per two-phase launch
+
+struct Phase {
+    int Nrows;  // valid weight rows per slot to compute (Nout, or 2*Nout for SwiGLU)
+    long long a_rows_per_slot;
+    int m_tiles, splits, kb_per_split, num_kb;
+    void* Y;
+    int ldy;
+    long long split_stride;  // elements between split-K partial outputs
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// add tx bytes to the current phase without arriving (several fills, one arrive.expect_tx commits)
+__device__ __forceinline__ void mbar_add_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: a pipeline bug traps (context error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s
+    }
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+                 : "memory");
+}
+// 1D bulk copy global -> shared (async proxy), completion on an mbarrier; bytes % 16 == 0
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void proxy_fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Wait until *c >= target.  Polls with relaxed loads (an acquire load costs an L1 invalidate per poll,
+// which stalls the whole SM's memory pipe) and acquires once; traps after ~2 s (a lost publication).
+__device__ __forceinline__ void spin_until(const int* c, int target) {
+    const long long t0 = clock64();
+    while (ld_relaxed(c) < target) {
+        __nanosleep(32);
+        if (clock64() - t0 > 4000000000ll) __trap();
+    }
+    fence_acquire();
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// K-major operand tile, 128-byte swizzle: 128-B rows, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, K-major, N>>3 at [17,23), M>>4 at [24,29).
+__device__ __forceinline__ uint32_t idesc_bf16(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+struct Unit {
+    int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks, id;
+};
+
+// One 16-column TMEM chunk of a finished accumulator -> the phase's output.
+template <int EPI>
+__device__ __forceinline__ void epilogue_store(const Phase& P, const Unit& w, int row, int lane, int c,
+                                               const uint32_t* v) {
+    if (EPI == kEpiSwiglu) {
+        // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float mine = __uint_as_float(v[j]);
+            const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+            if (!(lane & 1) && row < P.Nrows && c + j < w.n_valid) {
+                const float h = mine / (1.0f + expf(-mine)) * other;
+                reinterpret_cast<__nv_bfloat16*>(P.Y)[(long long)(w.n0 + c + j) * P.ldy + (row >> 1)] =
+                    __float2bfloat16_rn(h);
+            }
+        }
+    } else if (row < P.Nrows) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (c + j >= w.n_valid) break;
+            const long long o = (long long)(w.n0 + c + j) * P.ldy + row;
+            const float a = __uint_as_float(v[j]);
+            if (EPI == kEpiStoreF32)
+                reinterpret_cast<float*>(P.Y)[o + (long long)w.ks * P.split_stride] = a;
+            else if (EPI == kEpiResidAdd)
+                reinterpret_cast<float*>(P.Y)[o] += a;
+            else
+                reinterpret_cast<__nv_bfloat16*>(P.Y)[o] = __float2bfloat16_rn(tanhf(a));
+        }
+    }
+}
+
+
+// host: cached 2D tensor map (K-major bf16, 128B swizzle, box BK x box_rows); SM count
+const CUtensorMap& tensor_map(const TcOperand& op, int box_rows);
+int sm_count();
+Phase make_phase(const TcGemmArgs& a);
+
+}  // namespace tc
+}  // namespace smoe
