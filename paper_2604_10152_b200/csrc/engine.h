@@ -182,10 +182,11 @@ public:
     int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][2]
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
-    int pass_kernel = 1;         // one persistent launch per pass (pass_tc.cu; env SMOE_PASS_KERNEL=0: per-layer)
-    // row range of the passes that use it (measured on the C2 shape, profiles/r02_pass_kernel.md): at
-    // T < 16 the expert phase is short and the per-layer launches win; above, the pass kernel wins
-    int pass_kernel_min_rows = 16, pass_kernel_max_rows = 1 << 30;
+    // one persistent launch per pass (pass_tc.cu), opt-in with env SMOE_PASS_KERNEL=1: bit-identical to
+    // the per-layer launches but 2-4% slower end to end at B = 1..64 (profiles/r02_pass_kernel.md)
+    int pass_kernel = 0;
+    // row range of the passes that use it when enabled (env SMOE_PASS_MIN_ROWS / SMOE_PASS_MAX_ROWS)
+    int pass_kernel_min_rows = 1, pass_kernel_max_rows = 1 << 30;
     int* pass_ctr = nullptr;     // pass kernel dependency counters (self-resetting)
     unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials

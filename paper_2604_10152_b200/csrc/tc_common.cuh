@@ -11,7 +11,10 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;        // 64 bf16 = 128 B = one swizzle-atom row
 constexpr int BN_MAX = 256;   // max tokens per unit (MMA N)
-constexpr int BOX_N = 32;     // token rows per TMA box
+#ifndef SMOE_BOX_N
+#define SMOE_BOX_N 32  // 16 measured: no gain in the bench, slower at T=320 (profiles/r02_pass_kernel.md)
+#endif
+constexpr int BOX_N = SMOE_BOX_N;  // token rows per TMA box
 constexpr int kThreads = 192;
 constexpr int kMaxStages = 12;
 constexpr int kABytes = BM * BK * 2;
