@@ -301,7 +301,7 @@ def run_b200(a) -> None:
         return
     shp = dict(SHAPES[a.shape])
     spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
-    ep = world > 1 and not a.replicas  # N > 1: experts sharded over the GPUs (NCCL), tokens replicated
+    ep = world > 1 and not a.replicas  # N > 1: experts sharded, rows split, NCCL all-to-all dispatch/combine
     eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local,
                  ep_rank=rank if ep else 0, ep_world=world if ep else 1)
     if ep:
@@ -399,7 +399,7 @@ def run_b200(a) -> None:
         "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init N(0,1/sqrt(d)) weights, synthetic prompts)",
         "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert} experts HBM-resident, "
-                               f"B={a.batch}{'' if ep else '/GPU'}{f', experts sharded over {world} GPUs (NCCL)' if ep else ''}, "
+                               f"B={a.batch}{'' if ep else '/GPU'}{f', experts sharded over {world} GPUs, rows split, NCCL all-to-all dispatch/combine' if ep else ''}, "
                                f"gamma={a.gamma}, N={a.n_draft}, hot_temporal+affinity, greedy",
                    "model": f"{a.shape} L{spec.num_layers} E{spec.experts} K{spec.top_k} d{spec.hidden} f{spec.ffn} "
                             f"V{spec.vocab}",

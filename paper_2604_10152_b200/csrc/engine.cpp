@@ -168,10 +168,26 @@ Engine::Engine(const smoe_engine_config& c) {
         if (const char* v = getenv("SMOE_S_DOWN")) s_down = pick(nkb_f, atoi(v));
     }
     ybuf = dalloc<float>((size_t)s_down * seg_rows * d);
-    if (ep_world > 1) yred = dalloc<float>((size_t)Tmax * K * d);
+    if (ep_world > 1) {
+        xrecv = dalloc_bytes(seg_rows * d * ws);
+        ysend = dalloc<float>(seg_rows * d);
+        yret = dalloc<float>(seg_rows * d);
+        rcnt = dalloc<int>(E);
+        ep_gslot = dalloc<int>((size_t)std::max(1, M) * E);
+        ep_logs = dalloc<int>((size_t)(1 + ep_world) * 2 * std::max(1, M) * Tmax * K);
+        amax_loc = dalloc<int>(Tmax);
+        logits_loc = dalloc<float>((size_t)Tmax * V);
+        // group g = (source rank g / (E/G), local expert g % (E/G)) -> this rank's weight slot
+        std::vector<int> gs((size_t)std::max(1, M) * E);
+        const int eo = E / ep_world;
+        for (int m = 0; m < M; ++m)
+            for (int g = 0; g < E; ++g) gs[(size_t)m * E + g] = h_slot_of[(size_t)m * E + e_lo + g % eo];
+        h2d(ep_gslot, gs.data(), sizeof(int) * gs.size());
+    }
     pmix = dalloc<float>((size_t)s_mix * Tmax * d);
-    logits = dalloc<float>((size_t)Tmax * V);
-    amax = dalloc<int>(Tmax);
+    // + ep_world rows: an EP all-gather writes G * ceil(T/G) >= T rows
+    logits = dalloc<float>((size_t)(Tmax + ep_world) * V);
+    amax = dalloc<int>(Tmax + ep_world);
     in_draft = dalloc<uint8_t>((size_t)M * E);
     draft_sorted = dalloc<int>((size_t)M * E);
     rank = dalloc<int>((size_t)M * E * E);
@@ -199,6 +215,7 @@ Engine::Engine(const smoe_engine_config& c) {
     op_head = {head, (long long)V, d};
     op_xa = {xa, (long long)Tmax, d};
     op_xperm = {xperm, (long long)seg_rows, d};
+    if (xrecv) op_xrecv = {xrecv, (long long)seg_rows, d};
     op_h = {hbuf, (long long)seg_rows, f};
     SMOE_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets above vs. the non-blocking engine stream
 }
@@ -208,7 +225,8 @@ Engine::~Engine() {
     if (stream) cudaStreamSynchronize(stream);
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
-    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix); fr(yred);
+    fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);
+    fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
@@ -623,12 +641,16 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
 
 // Grouped expert FFN of the current MoE layer: xperm segments -> hbuf (up) -> ybuf split partials
 // (down).  Group e = rows [e*T, e*T + cnt[e]) in weight slot slots[e].
-void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls) {
+void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls, const void* X, const TcOperand* xop) {
     const size_t ws = wt == kF32 ? 4 : 2;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     const long long yd_stride = (long long)E * Tmax * d;
+    if (!X) {
+        X = xperm;
+        xop = &op_xperm;
+    }
     if (!(use_tc && fuse_moe && E <= 64)) {
-        gemm(up_pool, (long long)U * d, op_up, U, f, d, cnt, slots, E, T, 0, 0, T, xperm, op_xperm, hbuf, f, up_epi,
+        gemm(up_pool, (long long)U * d, op_up, U, f, d, cnt, slots, E, T, 0, 0, T, X, *xop, hbuf, f, up_epi,
              cls, (double)U * d * ws);
         gemm(down_pool, (long long)d * f, op_down, d, d, f, cnt, slots, E, T, 0, 0, T, hbuf, op_h, ybuf, d,
              kEpiStoreF32, cls, (double)d * f * ws, s_down, yd_stride);
@@ -637,7 +659,7 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
     cudaEvent_t ev;
     prof_begin(cls, &ev);
     const unsigned slot = gemm_launches++ & 1;
-    TcGemmArgs up{op_up, U, op_xperm, f, d, cnt, slots, E, T, 0, 0, T, hbuf, f, up_epi, 1, 0, sched + 2 * slot,
+    TcGemmArgs up{op_up, U, *xop, f, d, cnt, slots, E, T, 0, 0, T, hbuf, f, up_epi, 1, 0, sched + 2 * slot,
                   moe_done + 64 * slot};
     TcGemmArgs dn{op_down, d, op_h, d, f, cnt, slots, E, T, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
                   sched + 2 * slot, moe_done + 64 * slot};
@@ -660,6 +682,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                   int log_slot) {
     if (T <= 0) return;
     if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
+    if (ep_world > 1) return pass_ep(T, rseq, rextra, extra_uniform, restricted, use_aff, log_slot);
     const size_t ws = wt == kF32 ? 4 : 2;
     const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)E * Tmax * d;
     if (M > 0) SMOE_CUDA(cudaMemsetAsync(grp_cnt, 0, sizeof(int) * (size_t)M * E, stream));  // dispatch counters
@@ -695,7 +718,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             GateArgs g{x, pmix, s_mix, pm_stride, T, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E,
                        xperm, cnt, pos, wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr,
                        draft_sorted + (size_t)mo * E, rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft,
-                       use_aff, mo, row_plen, flags};
+                       use_aff, mo, 0, row_plen, flags};
             {
                 ProfScope ps(*this, "gate");
                 launch_gate(g, stream);  // x += a; rms; gate, top-K, remap; dispatch rows into xperm
@@ -706,12 +729,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             // passes touch only pinned draft experts)
             expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
             if (fetch) store_finish_layer(mo);
-            if (ep_world > 1) {  // EP: this rank's picks (zeros elsewhere), summed across ranks -- exact
-                if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
-                launch_ep_pack(ybuf, s_down, yd_stride, pos, fl, e_lo, e_hi, T * K, d, yred, stream);
-                comm->allreduce_sum(yred, (size_t)T * K * d, stream);
-                launch_combine_rms(x, yred, 1, 0, nullptr, wgt, T, K, d, 0, xa, wt, stream);
-            } else {
+            {
                 // K9 combine + residual + the next layer's (or the head's) rms
                 ProfScope ps(*this, "combine");
                 launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
@@ -729,8 +747,86 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
          "head_gemm", (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
-    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 4 : 5) + (uint64_t)n_dense * 5 +
-                (ep_world > 1 ? (uint64_t)M : 0);
+    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 4 : 5) + (uint64_t)n_dense * 5;
+    alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
+}
+
+// Expert-parallel pass (ep.h): this rank runs rows [r0, r0 + Tl) of the pass (contiguous blocks of
+// seg = ceil(T/G)) through the dense path, gate, head and argmax; per MoE layer its routed rows go to
+// the expert owners and come back finished through two all-to-alls; the pass's argmax tokens and
+// routing logs are all-gathered, so every rank ends the pass with the same host-visible state as G = 1.
+// Every rank issues the same collectives in the same order (a rank with no rows sends empty segments).
+void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
+                     int log_slot) {
+    if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
+    const int G = ep_world, eo = E / G;
+    const int seg = (T + G - 1) / G, r0 = ep_rank * seg, Tl = std::max(0, std::min(seg, T - r0));
+    const size_t ws = wt == kF32 ? 4 : 2;
+    const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)E * Tmax * d;
+    if (M > 0) SMOE_CUDA(cudaMemsetAsync(grp_cnt, 0, sizeof(int) * (size_t)M * E, stream));
+    if (Tl > 0)
+        launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq + r0, rextra ? rextra + r0 : nullptr, extra_uniform,
+                      Tl, d, x, row_plen, xa, wt, stream);
+    const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
+    for (int l = 0; l < L; ++l) {
+        if (Tl > 0)
+            gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, 0, Tl, l, Tl, xa, op_xa, pmix, d,
+                 kEpiStoreF32, "dense_gemm", (double)d * d * ws, s_mix, pm_stride);
+        const int mo = moe_ord[l];
+        if (mo < 0) {  // dense layer: local rows only
+            if (Tl > 0) {
+                launch_resid_rms(x, pmix, s_mix, pm_stride, Tl, d, xa, wt, stream);
+                gemm(up_pool, (long long)U * d, op_up, U, f, d, nullptr, nullptr, 1, 0, Tl, dense_slot[l], Tl, xa,
+                     op_xa, hbuf, f, up_epi, "dense_gemm", (double)U * d * ws);
+                gemm(down_pool, (long long)d * f, op_down, d, d, f, nullptr, nullptr, 1, 0, Tl, dense_slot[l], Tl, hbuf,
+                     op_h, ybuf, d, kEpiStoreF32, "dense_gemm", (double)d * f * ws, s_down, yd_stride);
+                launch_combine_rms(x, ybuf, s_down, yd_stride, nullptr, nullptr, Tl, 1, d, 1, xa, wt, stream);
+            }
+            continue;
+        }
+        int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
+        int* fl = fin_log + ((size_t)log_slot * M + mo) * Tmax * K;
+        int* cnt = grp_cnt + (size_t)mo * E;
+        if (Tl > 0) {
+            GateArgs g{x, pmix, s_mix, pm_stride, Tl, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E,
+                       xperm, cnt, pos, wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr,
+                       draft_sorted + (size_t)mo * E, rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft,
+                       use_aff, mo, seg, row_plen, flags};
+            ProfScope ps(*this, "gate");
+            launch_gate(g, stream);  // rows of expert e land in xperm rows [e*seg, e*seg + cnt[e])
+        }
+        // dispatch: chunk r of the expert-major segments = rank r's experts
+        comm->alltoall(xperm, xrecv, (size_t)eo * seg * d * ws, stream);
+        comm->alltoall(cnt, rcnt, sizeof(int) * eo, stream);
+        // owner: one grouped FFN over the (source rank, local expert) groups, finished rows summed over the
+        // split-K partials exactly as the combine would, then returned into the senders' [E][seg] layout
+        expert_ffn(seg, rcnt, ep_gslot + (size_t)mo * E, "expert_gemm", xrecv, &op_xrecv);
+        launch_ep_sum_partials(ybuf, s_down, yd_stride, rcnt, E, seg, d, ysend, stream);
+        comm->alltoall(ysend, yret, (size_t)eo * seg * d * sizeof(float), stream);
+        if (Tl > 0) {
+            ProfScope ps(*this, "combine");
+            launch_combine_rms(x, yret, 1, 0, pos, wgt, Tl, K, d, 0, xa, wt, stream);
+        }
+    }
+    if (Tl > 0) {
+        gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, 0, Tl, 0, Tl, xa, op_xa, ep_gather_logits ? logits_loc : logits,
+             V, kEpiStoreF32, "head_gemm", (double)V * d * ws);
+        launch_argmax(ep_gather_logits ? logits_loc : logits, Tl, V, amax_loc, flags, stream);
+    }
+    // replicate the pass outputs: argmax tokens, routing logs of this log slot, optionally the logits
+    comm->allgather(amax_loc, amax, sizeof(int) * seg, stream);
+    if (M > 0) {
+        int* pk = ep_logs;
+        int* gathered = ep_logs + (size_t)2 * M * Tmax * K;
+        launch_ep_pack_logs(raw_log + (size_t)log_slot * M * Tmax * K, fin_log + (size_t)log_slot * M * Tmax * K, M,
+                            Tmax, K, Tl, seg, pk, stream);
+        comm->allgather(pk, gathered, sizeof(int) * 2 * M * seg * K, stream);
+        launch_ep_unpack_logs(gathered, G, M, Tmax, K, T, seg, raw_log + (size_t)log_slot * M * Tmax * K,
+                              fin_log + (size_t)log_slot * M * Tmax * K, stream);
+    }
+    if (ep_gather_logits) comm->allgather(logits_loc, logits, sizeof(float) * seg * V, stream);
+    SMOE_CUDA(cudaGetLastError());
+    launches += 2 + (uint64_t)M * 5 + (uint64_t)n_dense * 5 + 2;
     alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
 }
 
@@ -810,7 +906,9 @@ void Engine::forward_one(const std::vector<int>& prefix, const int* restricted, 
     reset_sequences({prefix});
     int zero = 0;
     upload_ints(row_seq, &zero, 1);
+    ep_gather_logits = true;  // under expert parallelism row 0 lives on rank 0 only
     pass(1, row_seq, nullptr, 0, restricted != nullptr, use_aff, 0);
+    ep_gather_logits = false;
     sync();
     check_flags();
     if (logits_out) SMOE_CUDA(cudaMemcpy(logits_out, logits, sizeof(float) * V, cudaMemcpyDeviceToHost));

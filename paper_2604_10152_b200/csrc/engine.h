@@ -105,7 +105,18 @@ public:
     // expert parallelism: this rank owns experts [e_lo, e_hi) of every MoE layer
     int ep_rank = 0, ep_world = 1, e_lo = 0, e_hi = 0;
     std::unique_ptr<Comm> comm;
-    float* yred = nullptr;        // [Tmax*K][d] this rank's expert outputs, summed across ranks
+    // EP buffers (pass_ep): received routed rows, finished rows to return / returned, received counts,
+    // per-layer group slots of the (source rank, local expert) groups, gathered logs / argmax / logits
+    void* xrecv = nullptr;        // [E*Tmax][d] operand type
+    float* ysend = nullptr;       // [E*Tmax][d]
+    float* yret = nullptr;        // [E*Tmax][d]
+    int* rcnt = nullptr;          // [E]
+    int* ep_gslot = nullptr;      // [M][E]
+    int* ep_logs = nullptr;       // [2][M][Tmax][K] packed + [G][2][M][Tmax][K] gathered
+    int* amax_loc = nullptr;      // [Tmax]
+    float* logits_loc = nullptr;  // [Tmax][V]
+    bool ep_gather_logits = false;  // forward(): every rank needs row 0's logits
+    TcOperand op_xrecv{};
     bool dev_rng = false;         // weights came from init_device (regenerable anywhere)
     uint64_t dev_seed = 0;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -225,8 +236,13 @@ public:
               const int* gcnt, const int* gslot, int G, int seg, int single_rows, int single_slot, int rows_bound,
               const void* X, const TcOperand& bop, void* Y, int ldy, Epi epi, const char* cls, double bytes,
               int splits = 1, long long split_stride = 0);
-    // a MoE layer's expert FFN (grouped up + down projection), fused into one launch on tcgen05
-    void expert_ffn(int T, const int* cnt, const int* slots, const char* cls);
+    // a MoE layer's expert FFN (grouped up + down projection), fused into one launch on tcgen05; rows of
+    // group g are [g*seg, g*seg + cnt[g]) of X (xperm, or the received rows under EP)
+    void expert_ffn(int seg, const int* cnt, const int* slots, const char* cls, const void* X = nullptr,
+                    const TcOperand* xop = nullptr);
+    // expert-parallel pass: rows split across ranks, all-to-all dispatch / combine per MoE layer (ep.h)
+    void pass_ep(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
+                 int log_slot);
 
     // ---- host<->device helpers
     void upload_ints(int* dst, const int* src, size_t n);  // via pinned staging, async on stream

@@ -16,35 +16,43 @@ namespace smoe {
 
 namespace {
 
-// y[j] = sum_s P[s][pos[j]] for picks j of this rank's experts (fin[j] in [e0, e1)), else 0: the
-// rank's contribution in pick order, so the sum over ranks is exact and feeds the combine directly.
-__global__ void k_ep_pack(const float* __restrict__ P, int S, long long pstride, const int* __restrict__ pos,
-                          const int* __restrict__ fin, int e0, int e1, int d, float* __restrict__ y) {
+__global__ void k_ep_sum_partials(const float* __restrict__ P, int S, long long pstride, const int* __restrict__ cnt,
+                                  int seg, int d, float* __restrict__ y) {
     pdl_wait();
     pdl_trigger();
-    const int j = blockIdx.x;
-    const int e = fin[j];
-    const bool mine = e >= e0 && e < e1;
-    const long long src = (long long)pos[j] * d, dst = (long long)j * d;
+    const int g = blockIdx.y, t = blockIdx.x;
+    if (t >= cnt[g]) return;
+    const long long row = ((long long)g * seg + t) * d;
     for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (mine)
-            for (int s = 0; s < S; ++s) {
-                const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src + i);
-                a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
-            }
-        *reinterpret_cast<float4*>(y + dst + i) = a;
+        for (int s = 0; s < S; ++s) {
+            const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + row + i);
+            a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+        }
+        *reinterpret_cast<float4*>(y + row + i) = a;
     }
 }
 
-struct Ptrs {
-    const float* p[16];
-};
-__global__ void k_sum_ranks(Ptrs in, int world, size_t n, float* __restrict__ out) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        float a = 0.f;
-        for (int r = 0; r < world; ++r) a += in.p[r][i];  // rank order (exact: disjoint supports)
-        out[i] = a;
+__global__ void k_ep_pack_logs(const int* __restrict__ raw, const int* __restrict__ fin, int M, int Tmax, int K,
+                               int Tl, int seg, int* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int n = M * seg * K;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
+        const int w = i / n, j = i % n, m = j / (seg * K), t = (j / K) % seg, k = j % K;
+        out[i] = t < Tl ? (w ? fin : raw)[((long long)m * Tmax + t) * K + k] : -1;
+    }
+}
+
+__global__ void k_ep_unpack_logs(const int* __restrict__ in, int G, int M, int Tmax, int K, int T, int seg,
+                                 int* __restrict__ raw, int* __restrict__ fin) {
+    pdl_wait();
+    pdl_trigger();
+    const int n = M * seg * K;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G * 2 * n; i += gridDim.x * blockDim.x) {
+        const int r = i / (2 * n), w = (i / n) % 2, j = i % n, m = j / (seg * K), t = (j / K) % seg, k = j % K;
+        const int row = r * seg + t;
+        if (row < T) (w ? fin : raw)[((long long)m * Tmax + row) * K + k] = in[i];
     }
 }
 
@@ -53,7 +61,11 @@ struct NcclApi {
     void* h = nullptr;
     ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
     ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
@@ -68,12 +80,17 @@ NcclApi& nccl() {
         if (!a.h) return a;
         a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.h, "ncclGetUniqueId"));
         a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.h, "ncclCommInitRank"));
-        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.h, "ncclAllReduce"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(a.h, "ncclAllGather"));
+        a.send = reinterpret_cast<decltype(a.send)>(dlsym(a.h, "ncclSend"));
+        a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(a.h, "ncclRecv"));
+        a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(a.h, "ncclGroupStart"));
+        a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(a.h, "ncclGroupEnd"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(a.h, "ncclCommDestroy"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.h, "ncclGetErrorString"));
         return a;
     }();
-    if (!api.h || !api.get_unique_id || !api.comm_init_rank || !api.all_reduce)
+    if (!api.h || !api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.send || !api.recv ||
+        !api.group_start || !api.group_end)
         throw Error(kCuda, "NCCL (libnccl.so.2) not loadable");
     return api;
 }
@@ -94,8 +111,18 @@ public:
     }
     int rank() const override { return rank_; }
     int world() const override { return world_; }
-    void allreduce_sum(float* buf, size_t n, cudaStream_t s) override {
-        nccl_check(nccl().all_reduce(buf, buf, n, ncclFloat32, ncclSum, comm_, s), "ncclAllReduce");
+    void alltoall(const void* send, void* recv, size_t chunk, cudaStream_t s) override {
+        // grouped point-to-point: one send and one receive per peer (self included), fixed-size chunks,
+        // so no counts ever travel to the host
+        nccl_check(nccl().group_start(), "ncclGroupStart");
+        for (int r = 0; r < world_; ++r) {
+            nccl_check(nccl().send(static_cast<const char*>(send) + r * chunk, chunk, ncclInt8, r, comm_, s), "ncclSend");
+            nccl_check(nccl().recv(static_cast<char*>(recv) + r * chunk, chunk, ncclInt8, r, comm_, s), "ncclRecv");
+        }
+        nccl_check(nccl().group_end(), "ncclGroupEnd");
+    }
+    void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        nccl_check(nccl().all_gather(send, recv, bytes, ncclInt8, comm_, s), "ncclAllGather");
     }
 
 private:
@@ -127,7 +154,7 @@ struct LoopbackGroup {
     std::condition_variable cv;
     int arrived = 0;
     unsigned long long gen = 0;
-    std::vector<float*> bufs;
+    std::vector<const void*> bufs;
     explicit LoopbackGroup(int w) : world(w), bufs(w, nullptr) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
@@ -152,34 +179,34 @@ namespace {
 class LoopbackComm : public Comm {
 public:
     LoopbackComm(LoopbackGroup* g, int rank) : g_(g), rank_(rank) {}
-    ~LoopbackComm() override {
-        if (scratch_) cudaFree(scratch_);
-    }
     int rank() const override { return rank_; }
     int world() const override { return g_->world; }
-    void allreduce_sum(float* buf, size_t n, cudaStream_t s) override {
-        if (n > cap_) {
-            if (scratch_) SMOE_CUDA(cudaFree(scratch_));
-            SMOE_CUDA(cudaMalloc(&scratch_, n * sizeof(float)));
-            cap_ = n;
-        }
-        SMOE_CUDA(cudaStreamSynchronize(s));
-        g_->bufs[rank_] = buf;
-        g_->barrier();  // every rank's contribution is ready
-        Ptrs p{};
-        for (int r = 0; r < g_->world; ++r) p.p[r] = g_->bufs[r];
-        k_sum_ranks<<<148 * 4, 256, 0, s>>>(p, g_->world, n, scratch_);
-        SMOE_CUDA(cudaGetLastError());
-        SMOE_CUDA(cudaStreamSynchronize(s));
-        g_->barrier();  // every rank has read every buffer
-        SMOE_CUDA(cudaMemcpyAsync(buf, scratch_, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    // Every virtual rank publishes its send buffer; after a barrier each copies its chunks out of the
+    // others' buffers on its own stream; a second barrier keeps senders from reusing their buffers early.
+    void alltoall(const void* send, void* recv, size_t chunk, cudaStream_t s) override {
+        exchange(send, [&](int r, const char* peer) {
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + r * chunk, peer + rank_ * chunk, chunk,
+                                      cudaMemcpyDeviceToDevice, s));
+        }, s);
+    }
+    void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        exchange(send, [&](int r, const char* peer) {
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + r * bytes, peer, bytes, cudaMemcpyDeviceToDevice, s));
+        }, s);
     }
 
 private:
+    template <typename F>
+    void exchange(const void* send, F copy_from, cudaStream_t s) {
+        SMOE_CUDA(cudaStreamSynchronize(s));
+        g_->bufs[rank_] = send;
+        g_->barrier();  // every rank's send buffer is ready
+        for (int r = 0; r < g_->world; ++r) copy_from(r, static_cast<const char*>(g_->bufs[r]));
+        SMOE_CUDA(cudaStreamSynchronize(s));
+        g_->barrier();  // every rank has read every buffer
+    }
     LoopbackGroup* g_;
     int rank_;
-    float* scratch_ = nullptr;
-    size_t cap_ = 0;
 };
 }  // namespace
 
@@ -188,10 +215,20 @@ std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank) {
     return std::make_unique<LoopbackComm>(g, rank);
 }
 
-void launch_ep_pack(const float* P, int S, long long pstride, const int* pos, const int* fin, int e0, int e1, int picks,
-                    int d, float* y_red, cudaStream_t s) {
-    if (picks <= 0) return;
-    launch_k(k_ep_pack, picks, 256, 0, s, P, S, pstride, pos, fin, e0, e1, d, y_red);
+void launch_ep_sum_partials(const float* P, int S, long long pstride, const int* cnt, int groups, int seg, int d,
+                            float* y, cudaStream_t s) {
+    if (groups <= 0 || seg <= 0) return;
+    launch_k(k_ep_sum_partials, dim3(seg, groups), 256, 0, s, P, S, pstride, cnt, seg, d, y);
+}
+void launch_ep_pack_logs(const int* raw, const int* fin, int M, int Tmax, int K, int Tl, int seg, int* out,
+                         cudaStream_t s) {
+    if (M <= 0 || seg <= 0) return;
+    launch_k(k_ep_pack_logs, 64, 256, 0, s, raw, fin, M, Tmax, K, Tl, seg, out);
+}
+void launch_ep_unpack_logs(const int* in, int G, int M, int Tmax, int K, int T, int seg, int* raw, int* fin,
+                           cudaStream_t s) {
+    if (M <= 0 || seg <= 0) return;
+    launch_k(k_ep_unpack_logs, 128, 256, 0, s, in, G, M, Tmax, K, T, seg, raw, fin);
 }
 
 }  // namespace smoe

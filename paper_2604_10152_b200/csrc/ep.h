@@ -1,9 +1,14 @@
 // ep.h -- expert-parallel communication.
 //
-// Experts are sharded across G ranks in contiguous blocks (owner(e) = e / (E/G)); every rank runs the
-// dense path and the routing for all rows, computes only its own experts' rows, and the per-layer
-// expert outputs -- one row per pick, zeros for other ranks' picks -- are summed across ranks.  A sum in
-// which every element has one non-zero term is exact in any order, so the token stream, routing and
+// Experts are sharded across G ranks in contiguous blocks (owner(e) = e / (E/G)); the rows of every
+// pass are split across the ranks in contiguous blocks of seg = ceil(T/G) (the dense path, gate, head
+// and argmax of a row run on its rank).  Per MoE layer the gate writes a rank's routed rows into
+// expert-major segments [E][seg][d], which IS the all-to-all send buffer (chunk r = rank r's experts):
+// dispatch = all-to-all of those rows and of the per-expert counts, the owners run one grouped GEMM over
+// (source rank, local expert) groups, and combine = all-to-all of the finished rows back into the same
+// [E][seg][d] layout, which the combine kernel reads through the unchanged pick positions.  Every row is
+// computed by the same kernels in the same order as at G = 1, and routing logs and argmax tokens are
+// all-gathered once per pass so the host bookkeeping is replicated, hence token streams, routing and
 // ledger are bit-identical at G = 1, 2, 4, 8 (tested with the loopback transport on one GPU).
 #pragma once
 #include <cuda_runtime.h>
@@ -18,8 +23,10 @@ public:
     virtual ~Comm() = default;
     virtual int rank() const = 0;
     virtual int world() const = 0;
-    // in-place sum over ranks of a device f32 buffer, ordered on `s`
-    virtual void allreduce_sum(float* buf, size_t n, cudaStream_t s) = 0;
+    // send[r * chunk .. (r+1) * chunk) -> rank r's recv[me * chunk ..), all ranks at once, ordered on `s`
+    virtual void alltoall(const void* send, void* recv, size_t chunk_bytes, cudaStream_t s) = 0;
+    // recv[r * bytes ..) = rank r's send[0 .. bytes)
+    virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
 };
 
 // NCCL (dlopen'ed libnccl.so.2, so the engine shares whichever NCCL the process already loaded)
@@ -32,8 +39,15 @@ LoopbackGroup* loopback_create(int world);
 void loopback_destroy(LoopbackGroup* g);
 std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank);
 
-// y_red[j] = (e0 <= fin[j] < e1) ? sum_s P[s][pos[j]] : 0 for the T*K picks j (pick order)
-void launch_ep_pack(const float* P, int S, long long pstride, const int* pos, const int* fin, int e0, int e1, int picks,
-                    int d, float* y_red, cudaStream_t s);
+// y[r] = sum_s P[s][r] (s in order from 0, as the combine sums split partials) for the rows r of the
+// groups g with rows [g*seg, g*seg + cnt[g]): the owner's finished expert rows, ready to be returned
+void launch_ep_sum_partials(const float* P, int S, long long pstride, const int* cnt, int groups, int seg, int d,
+                            float* y, cudaStream_t s);
+// routing logs of a pass: pack this rank's rows [0, Tl) of raw/fin [M][Tmax][K] into [2][M][seg][K]
+// and, after the all-gather, unpack rank r's block into rows [r*seg, min(T, (r+1)*seg)) of the logs
+void launch_ep_pack_logs(const int* raw, const int* fin, int M, int Tmax, int K, int Tl, int seg, int* out,
+                         cudaStream_t s);
+void launch_ep_unpack_logs(const int* in, int G, int M, int Tmax, int K, int T, int seg, int* raw, int* fin,
+                           cudaStream_t s);
 
 }  // namespace smoe

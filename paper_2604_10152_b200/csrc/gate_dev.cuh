@@ -102,7 +102,7 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
             a.fin[r * K + lane] = my_ex;
             a.wgt[r * K + lane] = p[my_pick] / sum;  // the raw pick's weight, no renormalisation (model.cpp:249)
             // dispatch: lanes 0..K-1 claim their rows of the experts' segments concurrently
-            const int row = my_ex * a.T + atomicAdd(&a.cnt[my_ex], 1);
+            const int row = my_ex * (a.seg > 0 ? a.seg : a.T) + atomicAdd(&a.cnt[my_ex], 1);
             a.pos[r * K + lane] = row;
             dst[lane] = row;
         }

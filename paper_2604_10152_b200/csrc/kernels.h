@@ -56,6 +56,7 @@ struct GateArgs {
     int N;
     int use_affinity;
     int moe_ordinal;
+    int seg;                  // rows per expert segment of xperm (0: T)
     const int* row_plen;      // prefix length per row (surrogate hash)
     int* flags;
 };

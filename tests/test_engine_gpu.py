@@ -285,7 +285,7 @@ def test_bf16_fine_grained_lossless():
 
 
 # ---------------------------------------------------------------- expert parallelism (virtual ranks)
-def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False):
+def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False, work_fn=None):
     import threading
     from paper_2604_10152_b200.engine import LoopbackGroup
     grp = LoopbackGroup(G)
@@ -300,7 +300,10 @@ def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False):
     def work(r):
         try:
             eng = engines[r]
-            out[r] = eng.run_ondemand(cfg, prompts) if ondemand else eng.run_specmoe(cfg, prompts)
+            if work_fn is not None:
+                out[r] = work_fn(eng)
+            else:
+                out[r] = eng.run_ondemand(cfg, prompts) if ondemand else eng.run_specmoe(cfg, prompts)
         except Exception as ex:  # pragma: no cover - surfaced below
             errs.append(ex)
 
@@ -329,6 +332,32 @@ def test_expert_parallel_bitexact_bf16(G):
     for r in _run_ep(G, s, init, cfg, prompts):
         assert r.tokens == want.tokens and r.trace == want.trace and r.ledger == want.ledger
         assert r.outcomes == want.outcomes
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_expert_parallel_fine_grained_bitexact(G):
+    """C4-like shape (64 experts top-6, dense layer 0) with rows split over G ranks and the experts'
+    rows exchanged by all-to-all: token stream, routing trace, ledger and forward() logits equal G = 1."""
+    s = ModelSpec(num_layers=3, experts=64, top_k=6, hidden=256, ffn=256, vocab=512, expert_kind=SWIGLU3,
+                  moe_mask=[0, 1, 1], gate_skew=0.5, seed=4)
+    prompts = make_prompts(8, 5, 8, s.vocab)  # B=5: ragged row blocks at every G
+    cfg = RunCfg(gamma=4, n_draft=8, max_new_tokens=12, collect_trace=True)
+
+    def init(e):
+        e.init_device(13)
+        e.build_affinity_device()
+
+    one = Engine(s, weight_type=BF16, max_batch=5, max_gamma=4)
+    init(one)
+    want = one.run_specmoe(cfg, prompts)
+    want_lg = one.forward(prompts[2] + [7, 9])
+
+    def work(e):
+        r = e.run_specmoe(cfg, prompts)
+        return r, e.forward(prompts[2] + [7, 9])
+    for r, lg in _run_ep(G, s, init, cfg, prompts, work_fn=work):
+        assert r.tokens == want.tokens and r.trace == want.trace and r.ledger == want.ledger
+        assert np.array_equal(lg[0], want_lg[0]) and np.array_equal(lg[1], want_lg[1])
 
 
 def test_expert_parallel_f32_equals_reference():
