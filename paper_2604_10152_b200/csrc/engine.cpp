@@ -171,7 +171,12 @@ Engine::Engine(const smoe_engine_config& c) {
     if (ep_world > 1) {
         xrecv = dalloc_bytes(seg_rows * d * ws);
         ysend = dalloc<float>(seg_rows * d);
-        yret = dalloc<float>(seg_rows * d);
+        yret = dalloc<float>((size_t)s_down * seg_rows * d);
+        ep_flags = dalloc<int>(2 * (size_t)ep_world);
+        SMOE_CUDA(cudaMemset(ep_flags, 0, sizeof(int) * 2 * ep_world));
+        ep_peer = dalloc<void*>(4 * (size_t)ep_world);
+        const char* mode = getenv("SMOE_EP_MODE");
+        ep_p2p = use_tc && fuse_moe && E <= 64 && !(mode && std::string(mode) == "a2a");
         rcnt = dalloc<int>(E);
         ep_gslot = dalloc<int>((size_t)std::max(1, M) * E);
         ep_logs = dalloc<int>((size_t)(1 + ep_world) * 2 * std::max(1, M) * Tmax * K);
@@ -226,7 +231,9 @@ Engine::~Engine() {
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
     fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);
+    for (void* q : ep_ipc_opened) cudaIpcCloseMemHandle(q);
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
+    fr(ep_flags); fr(ep_peer);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
@@ -641,7 +648,8 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
 
 // Grouped expert FFN of the current MoE layer: xperm segments -> hbuf (up) -> ybuf split partials
 // (down).  Group e = rows [e*T, e*T + cnt[e]) in weight slot slots[e].
-void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls, const void* X, const TcOperand* xop) {
+void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls, const void* X, const TcOperand* xop,
+                        void* const* peer_y) {
     const size_t ws = wt == kF32 ? 4 : 2;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     const long long yd_stride = (long long)E * Tmax * d;
@@ -663,6 +671,11 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
                   moe_done + 64 * slot};
     TcGemmArgs dn{op_down, d, op_h, d, f, cnt, slots, E, T, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
                   sched + 2 * slot, moe_done + 64 * slot};
+    if (peer_y) {
+        dn.peer_y = peer_y;
+        dn.peer_eo = E / ep_world;
+        dn.peer_me = ep_rank;
+    }
     launch_moe_tc(up, dn, stream);
     prof_end(cls, ev, (double)(U + d) * f * ws);
 }
@@ -751,6 +764,21 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
 }
 
+// Peer tables for the fused exchange: every rank's xrecv, rcnt, yret and flag array, addressable from
+// this rank (CUDA IPC under NCCL, shared pointers under the loopback group).
+void Engine::ep_setup_peers() {
+    if (ep_world < 2 || !comm || ep_peers_ready) return;
+    ep_peers_ready = true;
+    void* mine[4] = {xrecv, rcnt, yret, ep_flags};
+    std::vector<void*> all;
+    comm->share_buffers(mine, 4, all, ep_ipc_opened);
+    std::vector<void*> tab(4 * (size_t)ep_world);
+    for (int r = 0; r < ep_world; ++r)
+        for (int i = 0; i < 4; ++i) tab[(size_t)i * ep_world + r] = all[(size_t)r * 4 + i];
+    h2d(ep_peer, tab.data(), sizeof(void*) * tab.size());
+    sync();
+}
+
 // Expert-parallel pass (ep.h): this rank runs rows [r0, r0 + Tl) of the pass (contiguous blocks of
 // seg = ceil(T/G)) through the dense path, gate, head and argmax; per MoE layer its routed rows go to
 // the expert owners and come back finished through two all-to-alls; the pass's argmax tokens and
@@ -759,6 +787,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
 void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
                      int log_slot) {
     if (!comm) throw Error(kInvariant, "expert parallelism: no transport attached");
+    if (ep_p2p) ep_setup_peers();  // collective: the first pass of every rank exchanges the peer tables
     const int G = ep_world, eo = E / G;
     const int seg = (T + G - 1) / G, r0 = ep_rank * seg, Tl = std::max(0, std::min(seg, T - r0));
     const size_t ws = wt == kF32 ? 4 : 2;
@@ -792,8 +821,32 @@ void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_unifor
                        xperm, cnt, pos, wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr,
                        draft_sorted + (size_t)mo * E, rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft,
                        use_aff, mo, seg, row_plen, flags};
+            if (ep_p2p) {
+                g.peer_x = const_cast<void* const*>(ep_peer);
+                g.ep_eo = eo;
+                g.ep_me = ep_rank;
+            }
             ProfScope ps(*this, "gate");
             launch_gate(g, stream);  // rows of expert e land in xperm rows [e*seg, e*seg + cnt[e])
+        }
+        if (ep_p2p) {
+            // fused exchange over peer memory: the gate has stored this rank's routed rows into the owners'
+            // xrecv; counts + flag -> owners; the owners' down-projection epilogues store the finished
+            // split partials into the senders' yret; done flags -> senders; the combine reads yret
+            const int seq = ++ep_seq;
+            void* const* peer = const_cast<void* const*>(ep_peer);
+            launch_ep_signal(cnt, E, eo, ep_rank, G, peer + G, peer + 3 * G, 0, seq, stream);
+            comm->fence(stream);
+            launch_ep_wait(ep_flags, G, 0, seq, stream);
+            expert_ffn(seg, rcnt, ep_gslot + (size_t)mo * E, "expert_gemm", xrecv, &op_xrecv, peer + 2 * G);
+            launch_ep_signal(nullptr, E, eo, ep_rank, G, peer + G, peer + 3 * G, 1, seq, stream);
+            comm->fence(stream);
+            launch_ep_wait(ep_flags, G, 1, seq, stream);
+            if (Tl > 0) {
+                ProfScope ps(*this, "combine");
+                launch_combine_rms(x, yret, s_down, yd_stride, pos, wgt, Tl, K, d, 0, xa, wt, stream);
+            }
+            continue;
         }
         // dispatch: chunk r of the expert-major segments = rank r's experts
         comm->alltoall(xperm, xrecv, (size_t)eo * seg * d * ws, stream);

@@ -40,6 +40,8 @@ struct TcGemmArgs {
     long long split_stride;
     int* sched;               // device [2] zero-initialised work counter (self-resetting)
     int* done = nullptr;      // device [64] zeroed per-group completion counters (fused launches)
+    void* const* peer_y = nullptr;  // EP fused return (see tc::Phase): device table of the ranks' return buffers
+    int peer_eo = 0, peer_me = 0;
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
 // One launch for a MoE layer's grouped up- (tanh / SwiGLU) and down-projection (f32 split partials):
@@ -109,7 +111,7 @@ public:
     // per-layer group slots of the (source rank, local expert) groups, gathered logs / argmax / logits
     void* xrecv = nullptr;        // [E*Tmax][d] operand type
     float* ysend = nullptr;       // [E*Tmax][d]
-    float* yret = nullptr;        // [E*Tmax][d]
+    float* yret = nullptr;        // [s_down][E*Tmax][d]
     int* rcnt = nullptr;          // [E]
     int* ep_gslot = nullptr;      // [M][E]
     int* ep_logs = nullptr;       // [2][M][Tmax][K] packed + [G][2][M][Tmax][K] gathered
@@ -117,6 +119,16 @@ public:
     float* logits_loc = nullptr;  // [Tmax][V]
     bool ep_gather_logits = false;  // forward(): every rank needs row 0's logits
     TcOperand op_xrecv{};
+    // fused peer-memory exchange (default; env SMOE_EP_MODE=a2a selects the NCCL all-to-all path): the gate
+    // stores routed rows into the owners' xrecv, the down-projection epilogue stores partials into the
+    // senders' yret ([s_down][E][Tmax][d]); per-layer sequence flags replace the collectives
+    bool ep_p2p = false;
+    int* ep_flags = nullptr;      // [2][G]: dispatch flags from the senders, done flags from the owners
+    void** ep_peer = nullptr;     // device [4][G]: every rank's xrecv, rcnt, yret, ep_flags
+    std::vector<void*> ep_ipc_opened;  // peer allocations opened through CUDA IPC (closed at teardown)
+    int ep_seq = 0;               // MoE layer-passes exchanged so far (identical on every rank)
+    bool ep_peers_ready = false;
+    void ep_setup_peers();
     bool dev_rng = false;         // weights came from init_device (regenerable anywhere)
     uint64_t dev_seed = 0;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -239,7 +251,7 @@ public:
     // a MoE layer's expert FFN (grouped up + down projection), fused into one launch on tcgen05; rows of
     // group g are [g*seg, g*seg + cnt[g]) of X (xperm, or the received rows under EP)
     void expert_ffn(int seg, const int* cnt, const int* slots, const char* cls, const void* X = nullptr,
-                    const TcOperand* xop = nullptr);
+                    const TcOperand* xop = nullptr, void* const* peer_y = nullptr);
     // expert-parallel pass: rows split across ranks, all-to-all dispatch / combine per MoE layer (ep.h)
     void pass_ep(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
                  int log_slot);

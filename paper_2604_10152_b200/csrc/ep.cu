@@ -1,6 +1,7 @@
 // ep.cu -- expert-parallel transports (NCCL over NVLink/NVSwitch; loopback for virtual ranks) and the
 // pack kernel that prepares a rank's disjoint expert-output contribution.
 #include <dlfcn.h>
+#include <cstdio>
 #include <cstring>
 #include <nccl.h>
 
@@ -31,6 +32,43 @@ __global__ void k_ep_sum_partials(const float* __restrict__ P, int S, long long 
         }
         *reinterpret_cast<float4*>(y + row + i) = a;
     }
+}
+
+__global__ void k_ep_signal(const int* __restrict__ cnt, int E, int eo, int me, int G, void* const* peer_cnt,
+                            void* const* peer_flags, int slot, int seq) {
+    pdl_wait();
+    pdl_trigger();
+    if (cnt)
+        for (int e = threadIdx.x; e < E; e += blockDim.x)
+            reinterpret_cast<int*>(peer_cnt[e / eo])[me * eo + e % eo] = cnt[e];
+    __threadfence_system();
+    __syncthreads();
+    for (int r = threadIdx.x; r < G; r += blockDim.x) {
+        int* f = reinterpret_cast<int*>(peer_flags[r]) + slot * G + me;
+        asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(seq) : "memory");
+    }
+}
+
+__global__ void k_ep_wait(const int* flags, int G, int slot, int seq) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        for (int r = 0; r < G; ++r) {
+            while (true) {
+                int v;
+                asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + slot * G + r) : "memory");
+                if (v - seq >= 0) break;
+                __nanosleep(64);
+                if (clock64() - t0 > 8000000000ll) {  // ~4 s: a peer stopped exchanging
+                    printf("smoe ep wait timeout: slot %d seq %d, flag of rank %d = %d (G %d)\n", slot, seq, r, v, G);
+                    __trap();
+                }
+            }
+        }
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_trigger();
 }
 
 __global__ void k_ep_pack_logs(const int* __restrict__ raw, const int* __restrict__ fin, int M, int Tmax, int K,
@@ -124,6 +162,31 @@ public:
     void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
         nccl_check(nccl().all_gather(send, recv, bytes, ncclInt8, comm_, s), "ncclAllGather");
     }
+    void share_buffers(void* const* mine, int n, std::vector<void*>& all, std::vector<void*>& opened) override {
+        std::vector<cudaIpcMemHandle_t> h(n);
+        for (int i = 0; i < n; ++i) SMOE_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
+        const size_t bytes = sizeof(cudaIpcMemHandle_t) * n;
+        char* dev = nullptr;
+        SMOE_CUDA(cudaMalloc(&dev, bytes * (world_ + 1)));
+        SMOE_CUDA(cudaMemcpy(dev, h.data(), bytes, cudaMemcpyHostToDevice));
+        allgather(dev, dev + bytes, bytes, nullptr);
+        std::vector<cudaIpcMemHandle_t> every((size_t)n * world_);
+        SMOE_CUDA(cudaStreamSynchronize(nullptr));
+        SMOE_CUDA(cudaMemcpy(every.data(), dev + bytes, bytes * world_, cudaMemcpyDeviceToHost));
+        SMOE_CUDA(cudaFree(dev));
+        all.assign((size_t)n * world_, nullptr);
+        for (int r = 0; r < world_; ++r)
+            for (int i = 0; i < n; ++i) {
+                if (r == rank_) {
+                    all[(size_t)r * n + i] = mine[i];
+                    continue;
+                }
+                void* p = nullptr;
+                SMOE_CUDA(cudaIpcOpenMemHandle(&p, every[(size_t)r * n + i], cudaIpcMemLazyEnablePeerAccess));
+                all[(size_t)r * n + i] = p;
+                opened.push_back(p);
+            }
+    }
 
 private:
     int rank_, world_;
@@ -155,6 +218,7 @@ struct LoopbackGroup {
     int arrived = 0;
     unsigned long long gen = 0;
     std::vector<const void*> bufs;
+    std::vector<void*> shared;  // share_buffers table
     explicit LoopbackGroup(int w) : world(w), bufs(w, nullptr) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
@@ -195,6 +259,25 @@ public:
         }, s);
     }
 
+    void fence(cudaStream_t s) override {
+        SMOE_CUDA(cudaStreamSynchronize(s));
+        g_->barrier();
+    }
+    void share_buffers(void* const* mine, int n, std::vector<void*>& all, std::vector<void*>& opened) override {
+        (void)opened;
+        {
+            std::lock_guard<std::mutex> lk(g_->mu);
+            g_->shared.resize((size_t)g_->world * n);
+            for (int i = 0; i < n; ++i) g_->shared[(size_t)rank_ * n + i] = mine[i];
+        }
+        g_->barrier();
+        {
+            std::lock_guard<std::mutex> lk(g_->mu);
+            all.assign(g_->shared.begin(), g_->shared.begin() + (size_t)g_->world * n);
+        }
+        g_->barrier();
+    }
+
 private:
     template <typename F>
     void exchange(const void* send, F copy_from, cudaStream_t s) {
@@ -219,6 +302,13 @@ void launch_ep_sum_partials(const float* P, int S, long long pstride, const int*
                             float* y, cudaStream_t s) {
     if (groups <= 0 || seg <= 0) return;
     launch_k(k_ep_sum_partials, dim3(seg, groups), 256, 0, s, P, S, pstride, cnt, seg, d, y);
+}
+void launch_ep_signal(const int* cnt, int E, int eo, int me, int G, void* const* peer_cnt, void* const* peer_flags,
+                      int slot, int seq, cudaStream_t s) {
+    launch_k(k_ep_signal, 1, 64, 0, s, cnt, E, eo, me, G, peer_cnt, peer_flags, slot, seq);
+}
+void launch_ep_wait(const int* flags, int G, int slot, int seq, cudaStream_t s) {
+    launch_k(k_ep_wait, 1, 32, 0, s, flags, G, slot, seq);
 }
 void launch_ep_pack_logs(const int* raw, const int* fin, int M, int Tmax, int K, int Tl, int seg, int* out,
                          cudaStream_t s) {

@@ -15,6 +15,7 @@
 #include <stddef.h>
 
 #include <memory>
+#include <vector>
 
 namespace smoe {
 
@@ -27,6 +28,15 @@ public:
     virtual void alltoall(const void* send, void* recv, size_t chunk_bytes, cudaStream_t s) = 0;
     // recv[r * bytes ..) = rank r's send[0 .. bytes)
     virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+    // every rank's n device buffers, addressable from this rank: all[r * n + i] (own: mine[i]).  NCCL:
+    // CUDA IPC handles exchanged by an all-gather and opened with peer access; opened pointers are
+    // appended to `opened` for the caller to close.  Loopback: the buffers of the other virtual ranks.
+    virtual void share_buffers(void* const* mine, int n, std::vector<void*>& all, std::vector<void*>& opened) = 0;
+    // After a fused-exchange signal: no-op with one process per GPU.  Virtual ranks sharing one device
+    // must not let a device-side wait spin for a peer whose host thread is blocked in a device-wide
+    // synchronisation (cudaFree, cudaMalloc, ...) queued behind that very wait; the loopback transport
+    // therefore drains its stream and meets the other ranks here, so every wait finds its flags set.
+    virtual void fence(cudaStream_t s) { (void)s; }
 };
 
 // NCCL (dlopen'ed libnccl.so.2, so the engine shares whichever NCCL the process already loaded)
@@ -47,6 +57,12 @@ void launch_ep_sum_partials(const float* P, int S, long long pstride, const int*
 // and, after the all-gather, unpack rank r's block into rows [r*seg, min(T, (r+1)*seg)) of the logs
 void launch_ep_pack_logs(const int* raw, const int* fin, int M, int Tmax, int K, int Tl, int seg, int* out,
                          cudaStream_t s);
+// Fused exchange signalling (peer memory).  signal: rank `me` publishes its per-expert counts into the
+// owners' receive-count arrays (cnt != nullptr), makes every prior store system-visible and sets its
+// flag flags[r][slot * G + me] = seq on every rank r.  wait: until flags[slot * G + r] == seq for all r.
+void launch_ep_signal(const int* cnt, int E, int eo, int me, int G, void* const* peer_cnt, void* const* peer_flags,
+                      int slot, int seq, cudaStream_t s);
+void launch_ep_wait(const int* flags, int G, int slot, int seq, cudaStream_t s);
 void launch_ep_unpack_logs(const int* in, int G, int M, int Tmax, int K, int T, int seg, int* raw, int* fin,
                            cudaStream_t s);
 

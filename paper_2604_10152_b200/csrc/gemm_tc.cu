@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++cnt;
         }
     }
+    if (p.nphase > 1 && p.ph[1].peer_y) __threadfence_system();  // peer stores performed before the grid ends
     tc_fence_before();
     __syncthreads();
     TR(if (threadIdx.x == 0) g_tr_cta[trs][blockIdx.x % kTrCtas][1] = gtimer();)
@@ -439,6 +440,10 @@ Phase make_phase(const TcGemmArgs& a) {
     P.Y = a.Y;
     P.ldy = a.ldy;
     P.split_stride = a.split_stride;
+    P.peer_y = a.peer_y;
+    P.peer_eo = a.peer_eo;
+    P.peer_me = a.peer_me;
+    P.peer_seg = a.seg;
     return P;
 }
 }  // namespace tc

@@ -187,7 +187,18 @@ __global__ void k_gate(GateArgs a) {
     __shared__ int dst[16];
     if (threadIdx.x < 32) gate_select_warp(a, r, gl, dst);
     __syncthreads();
-    for (int k = 0; k < K; ++k) store_row_op<OT>(a.xperm, (long long)dst[k] * d, xf, d, 1.0f);
+    const int sg = a.seg > 0 ? a.seg : a.T;
+    for (int k = 0; k < K; ++k) {
+        void* base = a.xperm;
+        long long row = dst[k];
+        if (a.peer_x) {  // fused EP dispatch over peer memory
+            const int e = (int)(row / sg);
+            base = a.peer_x[e / a.ep_eo];
+            row = (long long)(a.ep_me * a.ep_eo + e % a.ep_eo) * sg + (row - (long long)e * sg);
+        }
+        store_row_op<OT>(base, row * d, xf, d, 1.0f);
+    }
+    if (a.peer_x) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ K9 combine (+ next rms)

@@ -59,6 +59,10 @@ struct GateArgs {
     int seg;                  // rows per expert segment of xperm (0: T)
     const int* row_plen;      // prefix length per row (surrogate hash)
     int* flags;
+    // expert parallelism, fused dispatch: expert e's rows go straight into rank e / ep_eo's receive buffer
+    // (device table peer_x) at rows (ep_me * ep_eo + e % ep_eo) * seg + slot; nullptr = local xperm
+    void* const* peer_x;
+    int ep_eo, ep_me;
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 

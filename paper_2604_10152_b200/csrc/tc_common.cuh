@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdio>
+
 #include "engine.h"
 
 namespace smoe {
@@ -31,6 +33,10 @@ struct Phase {
     void* Y;
     int ldy;
     long long split_stride;  // elements between split-K partial outputs
+    // expert parallelism, fused return (kEpiStoreF32): group g's rows go straight into the return buffer
+    // of rank g / peer_eo over peer memory, at the rows [(me*eo + g % eo) * seg, ...) it dispatched them from
+    void* const* peer_y;
+    int peer_eo, peer_me, peer_seg;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -61,7 +67,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity)
             : "memory");
         if (done) return;
-        if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s
+        if (clock64() - t0 > 4000000000ll) {  // ~2 s
+            printf("smoe mbar_wait timeout: block %d thread %d parity %u\n", (int)blockIdx.x, (int)threadIdx.x, parity);
+            __trap();
+        }
     }
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
@@ -98,7 +107,10 @@ __device__ __forceinline__ void spin_until(const int* c, int target) {
     const long long t0 = clock64();
     while (ld_relaxed(c) < target) {
         __nanosleep(32);
-        if (clock64() - t0 > 4000000000ll) __trap();
+        if (clock64() - t0 > 4000000000ll) {
+            printf("smoe spin_until timeout: block %d counter %d < %d\n", (int)blockIdx.x, ld_relaxed(c), target);
+            __trap();
+        }
     }
     fence_acquire();
 }
@@ -159,13 +171,19 @@ __device__ __forceinline__ void epilogue_store(const Phase& P, const Unit& w, in
             }
         }
     } else if (row < P.Nrows) {
+        float* yf = reinterpret_cast<float*>(P.Y);
+        long long n0 = w.n0;
+        if (EPI == kEpiStoreF32 && P.peer_y) {
+            yf = reinterpret_cast<float*>(P.peer_y[w.g / P.peer_eo]);
+            n0 = (long long)(P.peer_me * P.peer_eo + w.g % P.peer_eo) * P.peer_seg + (w.n0 - (long long)w.g * P.peer_seg);
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             if (c + j >= w.n_valid) break;
             const long long o = (long long)(w.n0 + c + j) * P.ldy + row;
             const float a = __uint_as_float(v[j]);
             if (EPI == kEpiStoreF32)
-                reinterpret_cast<float*>(P.Y)[o + (long long)w.ks * P.split_stride] = a;
+                yf[(n0 + c + j) * P.ldy + row + (long long)w.ks * P.split_stride] = a;
             else if (EPI == kEpiResidAdd)
                 reinterpret_cast<float*>(P.Y)[o] += a;
             else

@@ -314,8 +314,15 @@ def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False, work_
     return out
 
 
+@pytest.fixture(params=["p2p", "a2a"])
+def ep_mode(request):
+    """Both exchange paths: fused peer-memory stores (default) and the all-to-all collectives."""
+    with _env(SMOE_EP_MODE=request.param):
+        yield request.param
+
+
 @pytest.mark.parametrize("G", [2, 4])
-def test_expert_parallel_bitexact_bf16(G):
+def test_expert_parallel_bitexact_bf16(G, ep_mode):
     """Experts sharded over G virtual ranks (loopback transport, one GPU): every rank produces the
     single-GPU token stream, routing trace and ledger bit for bit."""
     s = _c1_like(SWIGLU3, skew=1.0)
@@ -335,7 +342,7 @@ def test_expert_parallel_bitexact_bf16(G):
 
 
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_expert_parallel_fine_grained_bitexact(G):
+def test_expert_parallel_fine_grained_bitexact(G, ep_mode):
     """C4-like shape (64 experts top-6, dense layer 0) with rows split over G ranks and the experts'
     rows exchanged by all-to-all: token stream, routing trace, ledger and forward() logits equal G = 1."""
     s = ModelSpec(num_layers=3, experts=64, top_k=6, hidden=256, ffn=256, vocab=512, expert_kind=SWIGLU3,
