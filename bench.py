@@ -190,7 +190,7 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
 
 
-def ncu_traffic(draft_passes: int = 4, name: str = "r01_ncu_fused_moe.json"):
+def ncu_traffic(draft_passes: int = 4, name: str = "r02_ncu_fused_moe.json"):
     """DRAM bytes per launch of the dominant kernel from a committed ncu --set full capture (profiles/
     <name>: one draft-pass and one verify-pass launch), weighted like the step (gamma draft passes : 1
     verify pass), or None."""
@@ -391,7 +391,7 @@ def run_b200(a) -> None:
         roof_kernel = "k_gemm_tc (tcgen05 grouped expert GEMM)"
         roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
         traffic = ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 else None
-        traffic_src = "ncu --set full, profiles/r01_ncu_fused_moe.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
+        traffic_src = "ncu --set full, profiles/r02_ncu_fused_moe.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
     achieved = alg_bytes / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
     line = {
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
