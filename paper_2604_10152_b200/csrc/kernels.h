@@ -61,8 +61,8 @@ struct GateArgs {
     int* flags;
     // expert parallelism, fused dispatch: expert e's rows go straight into rank e / ep_eo's receive buffer
     // (device table peer_x) at rows (ep_me * ep_eo + e % ep_eo) * seg + slot; nullptr = local xperm
-    void* const* peer_x;
-    int ep_eo, ep_me;
+    void* const* peer_x = nullptr;
+    int ep_eo = 0, ep_me = 0;
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 

@@ -71,7 +71,8 @@ def analyze(path):
                  tail_us=float(np.mean((t1 - last_done) / 1e3)),
                  up_unit_us=float(np.median(unit_us[up])) if up.any() else 0.0,
                  down_unit_us=float(np.median(unit_us[~up])) if (~up).any() else 0.0,
-                 n_up=int(up.sum()), n_down=int((~up).sum()))
+                 n_up=int(up.sum()), n_down=int((~up).sum()),
+                 cta_start_spread=float((cta[s, :grid, 0].max() - t0) / 1e3))
         rows.append(r)
     rows.sort(key=lambda r: r["launch"])
     # aggregate per class (moe launches split by their unit count: draft passes touch fewer experts)
@@ -83,7 +84,7 @@ def analyze(path):
         f = lambda k: round(float(np.mean([x[k] for x in rs])), 1)  # noqa: E731
         print(json.dumps(dict(kind=key[0], n_up=key[1], n_down=key[2], launches=len(rs), dur_us=f("dur_us"),
                               ramp_us=f("ramp_us"), tail_us=f("tail_us"), up_unit_us=f("up_unit_us"),
-                              down_unit_us=f("down_unit_us"))))
+                              down_unit_us=f("down_unit_us"), cta_start_spread=f("cta_start_spread"))))
     return rows
 
 
