@@ -7,7 +7,7 @@ HBM-resident, batch 64, gamma 4, N 4 draft experts, hot_temporal + affinity, gre
 A "step" = one speculative phase over the batch: gamma restricted draft passes, one batched verify
 pass over B*(gamma+1) positions, accept/rollback, hotness + re-pin + ledger.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--shape c1|c2|c4] [--batch B]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--shape c1|c2|c4|c5] [--batch B]
 
 N > 1 (torchrun): one replica per GPU with independent sequences (weak scaling); time = max over
 ranks, value = tokens of all ranks / that time.  --impl reference times the reference's own CPU
@@ -31,8 +31,11 @@ SHAPES = {
     "c1": dict(num_layers=4, experts=8, top_k=2, hidden=512, ffn=1024, vocab=1024),
     "c2": dict(num_layers=32, experts=8, top_k=2, hidden=4096, ffn=14336, vocab=32000),
     "c4": dict(num_layers=28, experts=64, top_k=6, hidden=2048, ffn=1408, vocab=102400, moe_mask=[0] + [1] * 27),
+    # Mixtral-8x22B shape: 270.6 GB of SwiGLU experts -> expert parallel over >= 2 GPUs only
+    "c5": dict(num_layers=56, experts=8, top_k=2, hidden=6144, ffn=16384, vocab=32768),
 }
-SHAPE_NAMES = {"c1": "tiny synthetic MoE (C1)", "c2": "Mixtral-8x7B shape (C2)", "c4": "fine-grained E64 K6 (C4)"}
+SHAPE_NAMES = {"c1": "tiny synthetic MoE (C1)", "c2": "Mixtral-8x7B shape (C2)", "c4": "fine-grained E64 K6 (C4)",
+               "c5": "Mixtral-8x22B shape (C5)"}
 
 
 def args_parse():
@@ -43,10 +46,10 @@ def args_parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--shape", default="c2", choices=sorted(SHAPES))
     p.add_argument("--expert", default="swiglu3", choices=["swiglu3", "tanh2"])
-    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--batch", type=int, default=0, help="0: the shape's default (64; 128 for C5)")
     p.add_argument("--gamma", type=int, default=4)
     p.add_argument("--n-draft", type=int, default=0, help="0: the shape's default (4; 8 for C4, SURVEY 8)")
-    p.add_argument("--e2e-tokens", type=int, default=12)
+    p.add_argument("--e2e-tokens", type=int, default=128, help="new tokens per sequence of the e2e run (SURVEY 8d: 128)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--offload", action="store_true", help="headline = C3 (experts in pinned host DRAM)")
@@ -57,6 +60,8 @@ def args_parse():
     a = p.parse_args()
     if a.n_draft == 0:
         a.n_draft = 8 if a.shape == "c4" else 4
+    if a.batch == 0:
+        a.batch = 128 if a.shape == "c5" else 64
     return a
 
 
@@ -287,6 +292,12 @@ def run_b200(a) -> None:
     from paper_2604_10152_b200.engine import BF16, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
 
+    if a.shape == "c5" and (world < 2 or a.replicas):
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unavailable": "C5 (Mixtral-8x22B shape, 270.6 GB of "
+                              "experts) needs expert parallelism over >= 2 GPUs: torchrun --nproc-per-node N bench.py "
+                              "--gpus N --shape c5"}), flush=True)
+        return
     if a.offload:
         if rank == 0:
             sec = offload_section(a, local, a.batch, a.steps, a.warmup, gammas=(a.gamma,))

@@ -367,6 +367,27 @@ def test_expert_parallel_fine_grained_bitexact(G, ep_mode):
         assert np.array_equal(lg[0], want_lg[0]) and np.array_equal(lg[1], want_lg[1])
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("G", [2, 8])
+def test_expert_parallel_c5_slice_bitexact(G, ep_mode):
+    """Two-layer slice of the Mixtral-8x22B shape (C5: d=6144, f=16384, V=32768, SwiGLU bf16), B=16:
+    expert-parallel runs over G virtual ranks equal the single-engine run token for token."""
+    s = ModelSpec(num_layers=2, experts=8, top_k=2, hidden=6144, ffn=16384, vocab=32768, expert_kind=SWIGLU3, seed=5)
+    prompts = make_prompts(21, 16, 8, s.vocab)
+    cfg = RunCfg(gamma=4, n_draft=4, max_new_tokens=6, collect_trace=True)
+
+    def init(e):
+        e.init_device(17)
+        e.build_affinity_device()
+
+    one = Engine(s, weight_type=BF16, max_batch=16, max_gamma=4)
+    init(one)
+    want = one.run_specmoe(cfg, prompts)
+    one.close()
+    for r in _run_ep(G, s, init, cfg, prompts):
+        assert r.tokens == want.tokens and r.trace == want.trace and r.ledger == want.ledger
+
+
 def test_expert_parallel_f32_equals_reference():
     """fp32 exact weights sharded over 2 ranks: still equal to the reference golden run."""
     g = gold("toy")[1]
