@@ -117,9 +117,12 @@ int smoe_spec_step(smoe_engine* e, int* tokens_accepted_out, int* active_out);
 int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
 
 /* Expert parallelism.  Experts sharded in contiguous blocks, the rows of every pass split in
- * contiguous blocks of ceil(T/G); per MoE layer an all-to-all dispatches routed rows to the expert owners
- * and a second one returns the finished rows; argmax tokens and routing logs are all-gathered once per
- * pass, so every rank holds the same host state and the results are bit-identical at any G.
+ * contiguous blocks of ceil(T/G); per MoE layer the gate kernel stores routed rows into the expert
+ * owners' memory and the owners' down-projection epilogue stores the finished rows back (NVLink peer
+ * memory, CUDA IPC handles exchanged on the first pass, per-layer flags); env SMOE_EP_MODE=a2a uses two
+ * NCCL all-to-alls instead.  Argmax tokens and routing logs are all-gathered once per pass, so every
+ * rank holds the same host state and the results are bit-identical at any G.  Every engine call is
+ * collective across the ranks.
  * NCCL: rank 0 calls smoe_ep_nccl_unique_id, the id is broadcast out of band, every rank attaches.
  * Loopback: G engines on one device driven by G host threads (validation without a multi-GPU box). */
 typedef struct smoe_ep_loopback smoe_ep_loopback;
