@@ -59,7 +59,7 @@ __global__ void k_ep_wait(const int* flags, int G, int slot, int seq) {
                 asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + slot * G + r) : "memory");
                 if (v - seq >= 0) break;
                 __nanosleep(64);
-                if (clock64() - t0 > 8000000000ll) {  // ~4 s: a peer stopped exchanging
+                if (clock64() - t0 > 40000000000ll) {  // ~20 s: a peer stopped exchanging
                     printf("smoe ep wait timeout: slot %d seq %d, flag of rank %d = %d (G %d)\n", slot, seq, r, v, G);
                     __trap();
                 }
