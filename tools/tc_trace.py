@@ -53,7 +53,7 @@ def analyze(path):
         valid = un[s, :, 1] > 0
         if not valid.any() or grid <= 0:
             continue
-        t = np.bincount(tag[valid]).argmax()
+        t = tag[valid].max()  # the slot's latest launch (older launches leave stale unit records)
         m = valid & (tag == t)
         ids = np.nonzero(m)[0]
         U = un[s, m]
