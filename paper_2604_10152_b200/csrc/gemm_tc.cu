@@ -40,17 +40,21 @@ namespace smoe {
 namespace {
 using namespace tc;
 
-// Token (activation) operand maps with box heights 32, 64, 128 and 256 rows: a unit loads its tokens
-// with the smallest box that covers them, one TMA issue per stage.  Measured (tools/gemm_bench.py,
-// T=320, 80 rows per expert): up projection 0.707 -> 0.751 of the HBM peak, down 0.731 -> 0.766 vs
-// three 32-row boxes per stage; unchanged at <= 32 rows.
-constexpr int kTokBoxes = 4, kTokBox0 = 32;
+// Token (activation) operand maps with box heights 32, 64, ..., 256 rows: a unit loads its tokens with
+// the smallest box that covers them, one TMA issue per stage (measured, tools/gemm_bench.py, T=320 with
+// 80 rows per expert: up projection 0.707 -> 0.751 of the HBM peak, down 0.731 -> 0.766 vs three 32-row
+// boxes per stage).  The stage ring of a grouped launch is laid out at run time from the routing
+// counts: token space for the largest group's box only, every other byte of shared memory for more
+// weight stages (a verify pass at B=64 gets 7 stages instead of 4 sized for 256 rows).
+constexpr int kTokBoxes = 8, kTokBox0 = 32;
 struct TokenMaps {
     CUtensorMap m[kTokBoxes];
 };
 __host__ __device__ __forceinline__ int tok_box_index(int rows) {
-    return rows <= 32 ? 0 : rows <= 64 ? 1 : rows <= 128 ? 2 : 3;
+    rows = rows < 1 ? 1 : (rows > BN_MAX ? BN_MAX : rows);
+    return (rows + kTokBox0 - 1) / kTokBox0 - 1;
 }
+__host__ __device__ __forceinline__ int tok_box_bytes(int bi) { return (bi + 1) * kTokBox0 * BK * 2; }
 
 struct TcParams {
     Phase ph[2];
@@ -59,7 +63,8 @@ struct TcParams {
     const int* group_slot;
     int G, seg, single_rows, single_slot;  // group g: rows [g*seg, g*seg + group_cnt[g])
     int n_tiles;
-    int stages, b_region;  // b_region = bytes of token boxes per stage
+    int stages, b_region;  // host layout (single-group launches): stage count, token bytes per stage
+    int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
@@ -86,6 +91,16 @@ __device__ __forceinline__ long long gtimer() {
 #else
 #define TR(x)
 #endif
+
+// Stage ring of a grouped launch from the routing counts (call after the dependency wait; every role
+// computes the same layout): token space for the largest group's box, the rest for weight stages.
+__device__ __forceinline__ void grouped_layout(const TcParams& p, int& stages, int& stage_bytes) {
+    int mx = 1;
+    for (int g = 0; g < p.G; ++g)
+        if (p.group_slot[g] >= 0) mx = max(mx, min(BN_MAX, p.group_cnt[g]));
+    stage_bytes = kABytes + tok_box_bytes(tok_box_index(mx));
+    stages = max(2, min(kMaxStages, p.stage_space / stage_bytes));
+}
 
 __device__ __forceinline__ int units_of_phase(const TcParams& p, int ph) {
     return p.G * p.n_tiles * p.ph[ph].m_tiles * p.ph[ph].splits;
@@ -167,17 +182,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ TokenMaps mapB0,
               const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ TokenMaps mapB1, TcParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int stages = p.stages;
-    const int stage_bytes = kABytes + p.b_region;
+    // single-group launches: host layout (their weights stream before the dependency wait); grouped
+    // launches: re-laid out from the counts by the producer and the MMA lane after the wait
+    int stages = p.stages;
+    int stage_bytes = kABytes + p.b_region;
     const int total_units = units_of_phase(p, 0) + (p.nphase > 1 ? units_of_phase(p, 1) : 0);
     TR(const int trs = p.tr % kTrLaunches; if (threadIdx.x == 0) {
         g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
         if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, 0); g_tr_meta[trs][3] = gridDim.x; }
     })
 
+    // control block first (fixed size), then the 1024-aligned stage ring
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~uintptr_t(15));
     uint64_t* empty = full + kMaxStages;
     uint64_t* acc_full = empty + kMaxStages;  // [2]
     uint64_t* acc_empty = acc_full + 2;       // [2]
@@ -185,9 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* ring_empty = ring_full + kRing; // [kRing]
     int* ring = reinterpret_cast<int*>(ring_empty + kRing);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 1023) & ~uintptr_t(1023));
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) {
+        for (int s = 0; s < kMaxStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -228,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // that immediately precedes this one, so it may only be read after the dependency wait
                 pdl_wait();
                 kernel_dep = true;
+                grouped_layout(p, stages, stage_bytes);
             }
             for (int pub = 0;; ++pub) {
                 // dynamic work distribution: claim the next non-empty unit (single-group geometry is
@@ -249,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int bi = tok_box_index(w.n_valid);
                 const CUtensorMap* mB = w.phase ? &mapB1.m[bi] : &mapB0.m[bi];
                 const int arow = (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0);
-                const uint32_t bytes = kABytes + (uint32_t)(kTokBox0 << bi) * BK * 2;
+                const uint32_t bytes = kABytes + (uint32_t)tok_box_bytes(bi);
                 // Activations may be read once (a) the previous kernel is complete (PDL) and (b) for a
                 // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
                 // boxes are issued; at most `stages` of them are held back.
@@ -305,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         pdl_wait();
+        if (p.group_cnt) grouped_layout(p, stages, stage_bytes);
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
             Unit w;
@@ -465,7 +485,7 @@ int g_launch_no = 0;  // trace slot of the next launch (SMOE_TC_TRACE builds)
 
 TokenMaps token_maps(const TcOperand& op) {
     TokenMaps t;
-    for (int i = 0; i < kTokBoxes; ++i) t.m[i] = tensor_map(op, kTokBox0 << i);
+    for (int i = 0; i < kTokBoxes; ++i) t.m[i] = tensor_map(op, kTokBox0 * (i + 1));
     return t;
 }
 
@@ -491,9 +511,11 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.single_rows = a.single_rows;
     p.single_slot = a.single_slot;
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
-    p.b_region = (kTokBox0 << tok_box_index(std::min(a.rows_bound, BN_MAX))) * BK * 2;
+    constexpr int kCtrl = 1024;  // control block (barriers, unit ring, TMEM slot) + alignment slack below
+    p.b_region = tok_box_bytes(tok_box_index(std::min(a.rows_bound, BN_MAX)));
     const int stage_bytes = kABytes + p.b_region;
-    p.stages = std::max(2, std::min(kMaxStages, (kSmemBudget - 1024 - 512) / stage_bytes));
+    p.stage_space = kSmemBudget - kCtrl - 1024;
+    p.stages = std::max(2, std::min(kMaxStages, p.stage_space / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
     p.tr = g_launch_no++;
@@ -503,7 +525,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.a_tiles[0] = a.A.rows / BM;
     p.a_tiles[1] = b ? b->A.rows / BM : 0;
 #endif
-    const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 512;
+    const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;
     const CUtensorMap& ma0 = tensor_map(a.A, BM);
     const TokenMaps mb0 = token_maps(a.B);
     const CUtensorMap& ma1 = b ? tensor_map(b->A, BM) : ma0;
