@@ -46,7 +46,10 @@ using namespace tc;
 // boxes per stage).  The stage ring of a grouped launch is laid out at run time from the routing
 // counts: token space for the largest group's box only, every other byte of shared memory for more
 // weight stages (a verify pass at B=64 gets 7 stages instead of 4 sized for 256 rows).
-constexpr int kTokBoxes = 8, kTokBox0 = 32;
+#ifndef SMOE_TOK_BOX0
+#define SMOE_TOK_BOX0 32
+#endif
+constexpr int kTokBox0 = SMOE_TOK_BOX0, kTokBoxes = 256 / kTokBox0;
 struct TokenMaps {
     CUtensorMap m[kTokBoxes];
 };
