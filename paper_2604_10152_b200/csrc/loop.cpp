@@ -308,10 +308,22 @@ void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>&
     e.st = std::move(S);
 }
 
+// env SMOE_HOST_PROF=1: per phase, host time before the first launch / launching / waiting for the
+// device / bookkeeping after the readback (stderr)
+static const bool g_host_prof = [] {
+    const char* v = std::getenv("SMOE_HOST_PROF");
+    return v && v[0] == '1';
+}();
+static double host_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int spec_step(Engine& e, int* accepted_tokens) {
     SpecState& S = *e.st;
     const int B = S.B, M = S.M, E = S.E, K = S.K, g = S.g;
     if (accepted_tokens) *accepted_tokens = 0;
+    const double hp0 = g_host_prof ? host_now() : 0.0;
+    double hp1 = 0.0, hp2 = 0.0, hp3 = 0.0;
     std::vector<int> act;
     for (int b = 0; b < B; ++b)
         if (S.gen[b] < S.c.max_new_tokens) act.push_back(b);
@@ -341,6 +353,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
     e.upload_ints(e.seqs, act.data(), na);
 
     // (a) speculation: gamma restricted passes, drafts stay on device
+    if (g_host_prof) hp1 = host_now();
     for (int t = 0; t < g; ++t) {
         e.pass(na, drows, nullptr, t, true, S.c.use_affinity, t);
         launch_scatter_tokens(e.amax, drows, nullptr, t, na, e.drafts, e.stride, e.stream);
@@ -374,7 +387,9 @@ int spec_step(Engine& e, int* accepted_tokens) {
     read_log(e, e.raw_log, g, TV, S.vraw);
     std::vector<std::vector<int>> dfin(g);
     for (int t = 0; t < g; ++t) read_log(e, e.fin_log, t, na, dfin[t]);
+    if (g_host_prof) hp2 = host_now();
     e.sync();
+    if (g_host_prof) hp3 = host_now();
     e.check_flags();
     e.launches += (uint64_t)g + 2;  // scatters + accept (commit counted below)
     e.ctl_d2h += sizeof(int) * ((size_t)2 * na + (size_t)e.Bmax * e.stride + (size_t)M * K * (TV + (size_t)g * na));
@@ -483,6 +498,9 @@ int spec_step(Engine& e, int* accepted_tokens) {
     S.res->flush();
     ++S.phase;
     if (accepted_tokens) *accepted_tokens = total_take;
+    if (g_host_prof)
+        std::fprintf(stderr, "smoe host phase %d: prep %.3f ms, launch %.3f ms, device wait %.3f ms, bookkeeping %.3f ms\n",
+                     S.phase, (hp1 - hp0) * 1e3, (hp2 - hp1) * 1e3, (hp3 - hp2) * 1e3, (host_now() - hp3) * 1e3);
     return na;
 }
 
