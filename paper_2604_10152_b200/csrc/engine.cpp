@@ -17,7 +17,12 @@
 #include <numeric>
 #include <random>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace smoe {
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 namespace {
 
@@ -694,6 +699,7 @@ struct ProfScope {
 void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, bool restricted, int use_aff,
                   int log_slot) {
     if (T <= 0) return;
+    NvtxRange nv(restricted ? "smoe draft pass" : "smoe pass");
     if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
     if (ep_world > 1) return pass_ep(T, rseq, rextra, extra_uniform, restricted, use_aff, log_slot);
     const size_t ws = wt == kF32 ? 4 : 2;

@@ -17,6 +17,14 @@
 
 namespace smoe {
 
+// NVTX range for profilers (nsys / ncu --nvtx): a no-op unless a tool is attached (header-only nvtx3).
+struct NvtxRange {
+    explicit NvtxRange(const char* name);
+    ~NvtxRange();
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // tcgen05 grouped GEMM (gemm_tc.cu).  A = weights (TMA, K-major, 128-row tiles), B = activations.
 struct TcOperand {
     const void* base;  // bf16, row-major [rows][K]

@@ -324,6 +324,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
     if (accepted_tokens) *accepted_tokens = 0;
     const double hp0 = g_host_prof ? host_now() : 0.0;
     double hp1 = 0.0, hp2 = 0.0, hp3 = 0.0;
+    NvtxRange nv_phase("smoe speculative phase");
     std::vector<int> act;
     for (int b = 0; b < B; ++b)
         if (S.gen[b] < S.c.max_new_tokens) act.push_back(b);
@@ -388,8 +389,12 @@ int spec_step(Engine& e, int* accepted_tokens) {
     std::vector<std::vector<int>> dfin(g);
     for (int t = 0; t < g; ++t) read_log(e, e.fin_log, t, na, dfin[t]);
     if (g_host_prof) hp2 = host_now();
-    e.sync();
+    {
+        NvtxRange nv("smoe device wait");
+        e.sync();
+    }
     if (g_host_prof) hp3 = host_now();
+    NvtxRange nv_book("smoe bookkeeping (reference order)");
     e.check_flags();
     e.launches += (uint64_t)g + 2;  // scatters + accept (commit counted below)
     e.ctl_d2h += sizeof(int) * ((size_t)2 * na + (size_t)e.Bmax * e.stride + (size_t)M * K * (TV + (size_t)g * na));

@@ -325,6 +325,7 @@ __device__ __noinline__ void row_B(const PassParams& p, int l, int r, float4* ro
         const float4 a = row[i];
         row[i] = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
     }
+    wbar();  // the GEMV below reads every worker's elements (lane-stride order of the per-layer kernel)
     // gate GEMV over the scratch chunks: per-thread partial dots, then a fixed-order reduction (lanes,
     // then the 4 worker warps in order)
     for (int e0 = 0; e0 < E; e0 += EC) {
