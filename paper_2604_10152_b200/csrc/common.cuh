@@ -87,6 +87,12 @@ __device__ __forceinline__ void axpy4(float4& acc, float w, const float4 y) {
 #endif
 // threads per row of the per-layer row kernels (and the virtual block the pass kernel emulates)
 __host__ __device__ inline int row_threads(int d) { return d >= 4096 ? 1024 : d >= 1024 ? 512 : 256; }
+// threads of the gate kernel (K4-K6): at least one warp per expert (up to 1024), so each warp computes one
+// gate logit instead of several in sequence (E=64 at d=2048: 1024 instead of 512)
+__host__ __device__ inline int gate_threads(int d, int E) {
+    const int t = E * 32 < 1024 ? E * 32 : 1024;
+    return t > row_threads(d) ? t : row_threads(d);
+}
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

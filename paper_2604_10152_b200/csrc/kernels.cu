@@ -417,7 +417,7 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
-    const int threads = row_threads(a.d);  // one row per block: enough loads in flight for the partials
+    const int threads = gate_threads(a.d, a.E);  // one row per block, a warp per expert for the GEMV
     if (a.op == kF32) launch_k(k_gate<float>, a.T, threads, smem, s, a);
     else launch_k(k_gate<__nv_bfloat16>, a.T, threads, smem, s, a);
 }

@@ -255,13 +255,14 @@ __device__ __forceinline__ void gate_add(const PassParams& p, int mo, int e0, Sc
     scratch_add(sc, 0, p.gate_w + ((size_t)mo * p.E + e0) * p.d, (uint32_t)n * p.d * 4);
 }
 
-// Sum of squares of a row exactly as the per-layer row kernels (kernels.cu, blockDim = row_threads(d))
+// Sum of squares of a row exactly as the per-layer row kernels with blockDim = VB compute it (kernels.cu:
+// row_threads(d), or gate_threads(d, E) for the gate kernel)
 // compute it: virtual thread v accumulates float4 columns v, v + VB, ... in order, each virtual warp
 // butterflies, and warp 0 butterflies the virtual-warp partials; thread 0's value is the result.  The
 // 128 workers play the VB virtual threads (worker wt = virtual threads wt + 128 m, which own columns
 // that the worker itself wrote to `row`).
-__device__ __forceinline__ float vblock_sumsq(const float4* row, int d4, RowSmem& rs, int wt) {
-    const int VB = row_threads(d4 * 4), nw = VB >> 5;
+__device__ __forceinline__ float vblock_sumsq(const float4* row, int d4, int VB, RowSmem& rs, int wt) {
+    const int nw = VB >> 5;
 #pragma unroll 1
     for (int v = wt; v < VB; v += kWorkers) {
         float t = 0.f;
@@ -312,7 +313,7 @@ __device__ __noinline__ void row_B(const PassParams& p, int l, int r, float4* ro
         reinterpret_cast<float4*>(xr)[i] = v;
         row[i] = v;
     }
-    const float ss = vblock_sumsq(row, d4, rs, wt);
+    const float ss = vblock_sumsq(row, d4, moe ? gate_threads(d, E) : row_threads(d), rs, wt);
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
     if (wt == 0) PEV(l, 9);
     if (!moe) {
@@ -425,7 +426,7 @@ __device__ __noinline__ void row_D(const PassParams& p, int l, int r, float4* ro
         reinterpret_cast<float4*>(xr)[i] = v;
         row[i] = v;
     }
-    const float ss = vblock_sumsq(row, d4, rs, wt);
+    const float ss = vblock_sumsq(row, d4, row_threads(d), rs, wt);
     const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
 #pragma unroll 1
     for (int i = wt; i < d4; i += kWorkers) store_bf16x4(p.xa + (long long)r * d + i * 4, row[i], inv);
