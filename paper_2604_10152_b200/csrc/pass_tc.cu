@@ -221,9 +221,6 @@ __device__ __forceinline__ int valid_C(const PassParams& p, int l) {
 __device__ __forceinline__ void add4(float4& a, const float4 b) {
     a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
 }
-__device__ __forceinline__ float dot4(const float4 a, const float4 b) {
-    return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
-}
 __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst, float4 a, float s) {
     __nv_bfloat162 lo = __floats2bfloat162_rn(a.x * s, a.y * s), hi = __floats2bfloat162_rn(a.z * s, a.w * s);
     uint2 pk;
