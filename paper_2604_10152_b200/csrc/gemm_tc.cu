@@ -33,6 +33,7 @@
 #include <tuple>
 #include <vector>
 #include <cstdio>
+#include <cstdlib>
 
 #include "tc_common.cuh"
 
@@ -53,6 +54,10 @@ constexpr int kTokBox0 = SMOE_TOK_BOX0, kTokBoxes = 256 / kTokBox0;
 struct TokenMaps {
     CUtensorMap m[kTokBoxes];
 };
+// weight operand maps: 128-row box (one tile) and 256-row box (pair units)
+struct WeightMaps {
+    CUtensorMap m[2];
+};
 __host__ __device__ __forceinline__ int tok_box_index(int rows) {
     rows = rows < 1 ? 1 : (rows > BN_MAX ? BN_MAX : rows);
     return (rows + kTokBox0 - 1) / kTokBox0 - 1;
@@ -68,13 +73,11 @@ struct TcParams {
     int n_tiles;
     int stages, b_region;  // host layout (single-group launches): stage count, token bytes per stage
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
+    int pair_ok;           // grouped launches may use pair units (two 128-row tiles, one 256-row weight box)
+    int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
-#ifdef SMOE_TC_BULK_A
-    const uint8_t* a_ptr[2];
-    long long a_tiles[2];
-#endif
 };
 
 #ifdef SMOE_TC_TRACE
@@ -95,18 +98,26 @@ __device__ __forceinline__ long long gtimer() {
 #define TR(x)
 #endif
 
+// Pair units: two consecutive 128-row weight tiles under ONE 256-row TMA box per stage and two TMEM
+// accumulators (each MMA and every output element are unchanged, so results are bit-identical).  The
+// TMA issue count per weight byte halves, which is what bounded the stream: isolated up projection
+// 0.865 -> 0.97 of the HBM copy peak, down 0.80 -> 0.99 (tools/gemm_bench.py, T <= 32).  Needs groups of
+// <= 128 tokens (2 accumulators x 2 buffers x 128 TMEM columns).
+__device__ __forceinline__ int row_tiles(const Phase& P, int pair) { return pair ? (P.m_tiles + 1) / 2 : P.m_tiles; }
+
 // Stage ring of a grouped launch from the routing counts (call after the dependency wait; every role
 // computes the same layout): token space for the largest group's box, the rest for weight stages.
-__device__ __forceinline__ void grouped_layout(const TcParams& p, int& stages, int& stage_bytes) {
+__device__ __forceinline__ void grouped_layout(const TcParams& p, int& stages, int& stage_bytes, int& pair) {
     int mx = 1;
     for (int g = 0; g < p.G; ++g)
         if (p.group_slot[g] >= 0) mx = max(mx, min(BN_MAX, p.group_cnt[g]));
-    stage_bytes = kABytes + tok_box_bytes(tok_box_index(mx));
+    pair = p.pair_ok && mx <= BN_MAX / 2;
+    stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
     stages = max(2, min(kMaxStages, p.stage_space / stage_bytes));
 }
 
-__device__ __forceinline__ int units_of_phase(const TcParams& p, int ph) {
-    return p.G * p.n_tiles * p.ph[ph].m_tiles * p.ph[ph].splits;
+__device__ __forceinline__ int units_of_phase(const TcParams& p, int ph, int pair) {
+    return p.G * p.n_tiles * row_tiles(p.ph[ph], pair) * p.ph[ph].splits;
 }
 
 __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, int& r0, int& r1) {
@@ -122,18 +133,19 @@ __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, 
 }
 
 // Unit u -> (phase, group, token tile, row tile, split); returns false for units with no rows.
-__device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
+__device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w, int pair) {
     int ph = 0;
-    const int u0 = units_of_phase(p, 0);
+    const int u0 = units_of_phase(p, 0, pair);
     if (u >= u0) {
         ph = 1;
         u -= u0;
     }
     const Phase& P = p.ph[ph];
+    const int mtu = row_tiles(P, pair);
     const int ks = u % P.splits;
     u /= P.splits;
-    const int mt = u % P.m_tiles;
-    u /= P.m_tiles;
+    const int mt = u % mtu;
+    u /= mtu;
     const int g = u % p.G;
     const int nt = u / p.G;
     int slot, r0, r1;
@@ -144,7 +156,8 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
     w.g = g;
     w.slot = slot;
     w.n_valid = min(BN_MAX, r1 - w.n0);
-    w.m0 = mt * BM;
+    w.m0 = mt * (pair ? 2 * BM : BM);
+    w.pair = pair;
     w.ks = ks;
     w.kb0 = ks * P.kb_per_split;
     w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
@@ -152,18 +165,18 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w) {
 }
 
 // Phase-0 units a phase-1 unit of group g waits for (every token tile x row tile x split of g).
-__device__ __forceinline__ int phase0_units_of_group(const TcParams& p, int g) {
+__device__ __forceinline__ int phase0_units_of_group(const TcParams& p, int g, int pair) {
     int slot, r0, r1;
     group_rows(p, g, slot, r0, r1);
     if (slot < 0 || r1 <= r0) return 0;
-    return (r1 - r0 + BN_MAX - 1) / BN_MAX * p.ph[0].m_tiles * p.ph[0].splits;
+    return (r1 - r0 + BN_MAX - 1) / BN_MAX * row_tiles(p.ph[0], pair) * p.ph[0].splits;
 }
 
 // Consumer side of the unit ring: returns false when the producer published "done".  whole_warp:
 // all 32 lanes call this (epilogue warps; lane 0 releases the slot after the warp has read it);
 // otherwise a single lane (the MMA issuer) calls it and releases the slot itself.
 __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full, uint64_t* ring_empty, const int* ring,
-                                          int& cons, bool whole_warp, Unit& w) {
+                                          int& cons, bool whole_warp, Unit& w, int pair) {
     const int r = cons % kRing;
     mbar_wait(&ring_full[r], (uint32_t)((cons / kRing) & 1));
     const int u = ring[r];
@@ -175,24 +188,25 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
         mbar_arrive(&ring_empty[r]);
     }
     if (u < 0) return false;
-    decode_unit(p, u, w);
+    decode_unit(p, u, w, pair);
     w.id = u;
     return true;
 }
 
 template <int EPI0, int EPI1>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ TokenMaps mapB0,
-              const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ TokenMaps mapB1, TcParams p) {
+    k_gemm_tc(const __grid_constant__ WeightMaps mapA0, const __grid_constant__ TokenMaps mapB0,
+              const __grid_constant__ WeightMaps mapA1, const __grid_constant__ TokenMaps mapB1, TcParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // single-group launches: host layout (their weights stream before the dependency wait); grouped
     // launches: re-laid out from the counts by the producer and the MMA lane after the wait
+    int pair = p.group_cnt ? 0 : p.pair_single;  // grouped launches: decided from the counts below
     int stages = p.stages;
-    int stage_bytes = kABytes + p.b_region;
-    const int total_units = units_of_phase(p, 0) + (p.nphase > 1 ? units_of_phase(p, 1) : 0);
+    int stage_bytes = (pair ? 2 : 1) * kABytes + p.b_region;
+    int total_units = units_of_phase(p, 0, pair) + (p.nphase > 1 ? units_of_phase(p, 1, pair) : 0);
     TR(const int trs = p.tr % kTrLaunches; if (threadIdx.x == 0) {
         g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
-        if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, 0); g_tr_meta[trs][3] = gridDim.x; }
+        if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, 0, 0); g_tr_meta[trs][3] = gridDim.x; }
     })
 
     // control block first (fixed size), then the 1024-aligned stage ring
@@ -221,10 +235,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&ring_empty[r], 5);  // MMA lane + 4 epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0.m[0]) : "memory");
+        if (p.pair_ok || p.pair_single) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0.m[1]) : "memory");
         for (int i = 0; i < kTokBoxes; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB0.m[i]) : "memory");
         if (p.nphase > 1) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1.m[0]) : "memory");
+            if (p.pair_ok) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1.m[1]) : "memory");
             for (int i = 0; i < kTokBoxes; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB1.m[i]) : "memory");
         }
     }
@@ -249,7 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // that immediately precedes this one, so it may only be read after the dependency wait
                 pdl_wait();
                 kernel_dep = true;
-                grouped_layout(p, stages, stage_bytes);
+                grouped_layout(p, stages, stage_bytes, pair);
+                total_units = units_of_phase(p, 0, pair) + (p.nphase > 1 ? units_of_phase(p, 1, pair) : 0);
             }
             for (int pub = 0;; ++pub) {
                 // dynamic work distribution: claim the next non-empty unit (single-group geometry is
@@ -258,24 +275,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 Unit w;
                 do {
                     u = atomicAdd(&p.sched[0], 1);
-                } while (u < total_units && !decode_unit(p, u, w));
+                } while (u < total_units && !decode_unit(p, u, w, pair));
                 TR(if (u < total_units && u < kTrUnits) { g_tr_unit[trs][u].cta = blockIdx.x | ((long long)p.tr << 32); g_tr_unit[trs][u].claim = gtimer(); })
                 const int r = pub % kRing;
                 mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
                 ring[r] = u < total_units ? u : -1;
                 mbar_arrive(&ring_full[r]);
                 if (u >= total_units) break;
-                const CUtensorMap* mA = w.phase ? &mapA1 : &mapA0;
+                const CUtensorMap* mA = w.phase ? &mapA1.m[pair] : &mapA0.m[pair];
+                const int a_bytes = (pair ? 2 : 1) * kABytes;  // one 128- or 256-row weight box
                 // the unit's tokens as ONE box per stage: the smallest of 32/64/128/256 rows covering them
                 // (one TMA issue per stage; rows past the group are fetched but never multiplied in)
                 const int bi = tok_box_index(w.n_valid);
                 const CUtensorMap* mB = w.phase ? &mapB1.m[bi] : &mapB0.m[bi];
                 const int arow = (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0);
-                const uint32_t bytes = kABytes + (uint32_t)tok_box_bytes(bi);
+                const uint32_t bytes = a_bytes + (uint32_t)tok_box_bytes(bi);
                 // Activations may be read once (a) the previous kernel is complete (PDL) and (b) for a
                 // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
                 // boxes are issued; at most `stages` of them are held back.
-                const int need = w.phase ? phase0_units_of_group(p, w.g) : 0;
+                const int need = w.phase ? phase0_units_of_group(p, w.g, pair) : 0;
                 bool ready = kernel_dep && (w.phase == 0 || ld_relaxed(&p.done[w.g]) >= need);
                 if (ready && w.phase) {
                     fence_acquire();
@@ -287,23 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], (uint32_t)(((it / stages) & 1) ^ 1));
                     uint8_t* st = smem + s * stage_bytes;
                     mbar_expect_tx(&full[s], bytes);
-#ifdef SMOE_TC_BULK_A
-                    {
-#ifdef SMOE_TC_WAVE_A
-                        const long long tile = arow / BM, wave = tile / 148, lane148 = tile % 148;
-                        const long long width = min(148ll, p.a_tiles[w.phase] - wave * 148);
-                        const uint8_t* src = p.a_ptr[w.phase] +
-                                             (wave * 148 * p.ph[w.phase].num_kb + (long long)kb * width + lane148) * kABytes;
-#else
-                        const uint8_t* src = p.a_ptr[w.phase] + ((long long)arow / BM * p.ph[w.phase].num_kb + kb) * kABytes;
-#endif
-                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(st)), "l"(src), "r"(kABytes), "r"(smem_u32(&full[s])) : "memory");
-                    }
-#else
                     tma_load_2d(mA, &full[s], st, kb * BK, arow);
-#endif
                     if (ready) {
-                        tma_load_2d(mB, &full[s], st + kABytes, kb * BK, w.n0);
+                        tma_load_2d(mB, &full[s], st + a_bytes, kb * BK, w.n0);
                         continue;
                     }
                     if (it + 1 - pend_it < stages && kb + 1 < w.kb1) continue;  // keep streaming weights
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ready = true;
                     for (int j2 = pend_it; j2 <= it; ++j2) {  // activations of the held-back stages
-                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + kABytes;
+                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + a_bytes;
                         tma_load_2d(mB, &full[j2 % stages], sp, (w.kb0 + (j2 - pend_it)) * BK, w.n0);
                     }
                 }
@@ -327,11 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         pdl_wait();
-        if (p.group_cnt) grouped_layout(p, stages, stage_bytes);
+        if (p.group_cnt) grouped_layout(p, stages, stage_bytes, pair);
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
             Unit w;
-            while (next_unit(p, ring_full, ring_empty, ring, cons, false, w)) {
+            while (next_unit(p, ring_full, ring_empty, ring, cons, false, w, pair)) {
                 const int acc = cnt & 1;
                 mbar_wait(&acc_empty[acc], (uint32_t)(((cnt >> 1) & 1) ^ 1));
                 tc_fence_after();
@@ -344,11 +348,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     TR(if (kb == w.kb0) g_tr_unit[trs][w.id % kTrUnits].mma_first = gtimer();)
                     const uint32_t a_base = smem_u32(smem + s * stage_bytes);
-                    const uint32_t b_base = a_base + kABytes;
+                    const uint32_t b_base = a_base + (pair ? 2 : 1) * kABytes;
+                    // Two straight-line loops, branching once per stage: the single issuing thread's per-MMA
+                    // overhead bounds the stream (a predicated-off second MMA inside one loop cost 30%).
+                    if (pair) {  // second 128-row tile of the box -> second accumulator, same tokens
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc,
-                                 (kb > w.kb0 || kk) ? 1u : 0u);
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint32_t accum = (kb > w.kb0 || kk) ? 1u : 0u;
+                            mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc, accum);
+                            mma_bf16(d_tmem + BM, smem_desc(a_base + kABytes + kk * 32), smem_desc(b_base + kk * 32),
+                                     idesc, accum);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc,
+                                     (kb > w.kb0 || kk) ? 1u : 0u);
+                    }
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&acc_full[acc]);
@@ -362,19 +378,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         int cnt = 0, cons = 0;
         Unit w;
-        while (next_unit(p, ring_full, ring_empty, ring, cons, true, w)) {
+        if (p.group_cnt) grouped_layout(p, stages, stage_bytes, pair);
+        while (next_unit(p, ring_full, ring_empty, ring, cons, true, w, pair)) {
             const int acc = cnt & 1;
             mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
             tc_fence_after();
-            const int row = w.m0 + q * 32 + lane;  // weight row within the slot
-            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX);
             const Phase& P = p.ph[w.phase];
-            for (int c = 0; c < w.n_valid; c += 16) {
-                uint32_t v[16];
-                tmem_ld16(taddr + c, v);
-                tmem_wait_ld();
-                if (w.phase == 0) epilogue_store<EPI0>(P, w, row, lane, c, v);
-                else epilogue_store<EPI1>(P, w, row, lane, c, v);
+            for (int h = 0; h < (pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
+                const int row = w.m0 + h * BM + q * 32 + lane;  // weight row within the slot
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * BM);
+                for (int c = 0; c < w.n_valid; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(taddr + c, v);
+                    tmem_wait_ld();
+                    if (w.phase == 0) epilogue_store<EPI0>(P, w, row, lane, c, v);
+                    else epilogue_store<EPI1>(P, w, row, lane, c, v);
+                }
             }
             tc_fence_before();
             if (p.nphase > 1 && w.phase == 0) {
@@ -515,23 +534,27 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.single_slot = a.single_slot;
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
     constexpr int kCtrl = 1024;  // control block (barriers, unit ring, TMEM slot) + alignment slack below
+    static const bool pair_env = [] {
+        const char* v = getenv("SMOE_TC_PAIR");
+        return !(v && v[0] == '0');
+    }();
+    static const bool pair_single_env = [] {
+        const char* v = getenv("SMOE_TC_PAIR_SINGLE");
+        return !(v && v[0] == '0');
+    }();
+    p.pair_ok = a.group_cnt && pair_env;
+    p.pair_single = !a.group_cnt && pair_env && pair_single_env && a.single_rows <= BN_MAX / 2;
     p.b_region = tok_box_bytes(tok_box_index(std::min(a.rows_bound, BN_MAX)));
-    const int stage_bytes = kABytes + p.b_region;
+    const int stage_bytes = (p.pair_single ? 2 : 1) * kABytes + p.b_region;
     p.stage_space = kSmemBudget - kCtrl - 1024;
     p.stages = std::max(2, std::min(kMaxStages, p.stage_space / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
     p.tr = g_launch_no++;
-#ifdef SMOE_TC_BULK_A
-    p.a_ptr[0] = (const uint8_t*)a.A.base;
-    p.a_ptr[1] = b ? (const uint8_t*)b->A.base : nullptr;
-    p.a_tiles[0] = a.A.rows / BM;
-    p.a_tiles[1] = b ? b->A.rows / BM : 0;
-#endif
     const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;
-    const CUtensorMap& ma0 = tensor_map(a.A, BM);
+    const WeightMaps ma0{{tensor_map(a.A, BM), tensor_map(a.A, 2 * BM)}};
     const TokenMaps mb0 = token_maps(a.B);
-    const CUtensorMap& ma1 = b ? tensor_map(b->A, BM) : ma0;
+    const WeightMaps ma1 = b ? WeightMaps{{tensor_map(b->A, BM), tensor_map(b->A, 2 * BM)}} : ma0;
     const TokenMaps mb1 = b ? token_maps(b->B) : mb0;
     long long units = (long long)p.G * p.n_tiles * p.ph[0].m_tiles * p.ph[0].splits;
     if (b) units += (long long)p.G * p.n_tiles * p.ph[1].m_tiles * p.ph[1].splits;

@@ -152,6 +152,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 
 struct Unit {
     int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks, id;
+    int pair;  // two 128-row tiles (gemm_tc.cu pair units)
 };
 
 // One 16-column TMEM chunk of a finished accumulator -> the phase's output.
