@@ -99,7 +99,9 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 // Programmatic dependent launch (PDL).  Every hot-path kernel starts with pdl_wait() (no-op when not
 // launched with the PDL attribute) before touching memory written by earlier kernels, then
 // pdl_trigger() so the next kernel's CTAs may be scheduled as SMs free up and run their prologue
-// (barrier init, TMEM alloc, static weight prefetch) under this kernel's tail.
+// (barrier init, TMEM alloc, static weight prefetch) under this kernel's tail.  Triggering before the
+// wait would let a kernel two launches later become resident while an earlier one still runs (the
+// GEMM launches alternate between two scheduler slots, which relies on at most two in flight).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

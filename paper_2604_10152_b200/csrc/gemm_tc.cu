@@ -73,7 +73,7 @@ struct TcParams {
     int n_tiles;
     int stages, b_region;  // host layout (single-group launches): stage count, token bytes per stage
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
-    int pair_ok;           // grouped launches may use pair units (two 128-row tiles, one 256-row weight box)
+    int pair_ok;           // grouped launches: phases (bit 0 up, bit 1 down) that may use pair units
     int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
@@ -111,13 +111,13 @@ __device__ __forceinline__ void grouped_layout(const TcParams& p, int& stages, i
     int mx = 1;
     for (int g = 0; g < p.G; ++g)
         if (p.group_slot[g] >= 0) mx = max(mx, min(BN_MAX, p.group_cnt[g]));
-    pair = p.pair_ok && mx <= BN_MAX / 2;
+    pair = p.pair_ok && mx <= BN_MAX / 2 ? p.pair_ok : 0;
     stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
     stages = max(2, min(kMaxStages, p.stage_space / stage_bytes));
 }
 
 __device__ __forceinline__ int units_of_phase(const TcParams& p, int ph, int pair) {
-    return p.G * p.n_tiles * row_tiles(p.ph[ph], pair) * p.ph[ph].splits;
+    return p.G * p.n_tiles * row_tiles(p.ph[ph], (pair >> ph) & 1) * p.ph[ph].splits;
 }
 
 __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, int& r0, int& r1) {
@@ -141,6 +141,7 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w, i
         u -= u0;
     }
     const Phase& P = p.ph[ph];
+    pair = (pair >> ph) & 1;
     const int mtu = row_tiles(P, pair);
     const int ks = u % P.splits;
     u /= P.splits;
@@ -169,7 +170,7 @@ __device__ __forceinline__ int phase0_units_of_group(const TcParams& p, int g, i
     int slot, r0, r1;
     group_rows(p, g, slot, r0, r1);
     if (slot < 0 || r1 <= r0) return 0;
-    return (r1 - r0 + BN_MAX - 1) / BN_MAX * row_tiles(p.ph[0], pair) * p.ph[0].splits;
+    return (r1 - r0 + BN_MAX - 1) / BN_MAX * row_tiles(p.ph[0], pair & 1) * p.ph[0].splits;
 }
 
 // Consumer side of the unit ring: returns false when the producer published "done".  whole_warp:
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ring[r] = u < total_units ? u : -1;
                 mbar_arrive(&ring_full[r]);
                 if (u >= total_units) break;
-                const CUtensorMap* mA = w.phase ? &mapA1.m[pair] : &mapA0.m[pair];
-                const int a_bytes = (pair ? 2 : 1) * kABytes;  // one 128- or 256-row weight box
+                const CUtensorMap* mA = w.phase ? &mapA1.m[w.pair] : &mapA0.m[w.pair];
+                const int a_space = (pair ? 2 : 1) * kABytes;  // weight space of a stage (tokens after it)
+                const int a_bytes = (w.pair ? 2 : 1) * kABytes;  // one 128- or 256-row weight box
                 // the unit's tokens as ONE box per stage: the smallest of 32/64/128/256 rows covering them
                 // (one TMA issue per stage; rows past the group are fetched but never multiplied in)
                 const int bi = tok_box_index(w.n_valid);
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_expect_tx(&full[s], bytes);
                     tma_load_2d(mA, &full[s], st, kb * BK, arow);
                     if (ready) {
-                        tma_load_2d(mB, &full[s], st + a_bytes, kb * BK, w.n0);
+                        tma_load_2d(mB, &full[s], st + a_space, kb * BK, w.n0);
                         continue;
                     }
                     if (it + 1 - pend_it < stages && kb + 1 < w.kb1) continue;  // keep streaming weights
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ready = true;
                     for (int j2 = pend_it; j2 <= it; ++j2) {  // activations of the held-back stages
-                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + a_bytes;
+                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + a_space;
                         tma_load_2d(mB, &full[j2 % stages], sp, (w.kb0 + (j2 - pend_it)) * BK, w.n0);
                     }
                 }
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_base = a_base + (pair ? 2 : 1) * kABytes;
                     // Two straight-line loops, branching once per stage: the single issuing thread's per-MMA
                     // overhead bounds the stream (a predicated-off second MMA inside one loop cost 30%).
-                    if (pair) {  // second 128-row tile of the box -> second accumulator, same tokens
+                    if (w.pair) {  // second 128-row tile of the box -> second accumulator, same tokens
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint32_t accum = (kb > w.kb0 || kk) ? 1u : 0u;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
             tc_fence_after();
             const Phase& P = p.ph[w.phase];
-            for (int h = 0; h < (pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
+            for (int h = 0; h < (w.pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
                 const int row = w.m0 + h * BM + q * 32 + lane;  // weight row within the slot
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * BM);
                 for (int c = 0; c < w.n_valid; c += 16) {
@@ -542,8 +544,18 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
         const char* v = getenv("SMOE_TC_PAIR_SINGLE");
         return !(v && v[0] == '0');
     }();
-    p.pair_ok = a.group_cnt && pair_env;
-    p.pair_single = !a.group_cnt && pair_env && pair_single_env && a.single_rows <= BN_MAX / 2;
+    static const bool pair_down_env = [] {
+        const char* v = getenv("SMOE_TC_PAIR_DOWN");
+        return !(v && v[0] == '0');
+    }();
+    // grouped launches: bit 0 pairs the first phase, bit 1 the second (applied when the counts allow)
+    p.pair_ok = a.group_cnt && pair_env ? (1 | (b && pair_down_env ? 2 : 0)) : 0;
+    // single-group launches pair only while the pair units still cover every SM (the C2 Mix launch at
+    // T=64 would otherwise run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us)
+    const long long paired_units = (long long)((a.rows_bound + BN_MAX - 1) / BN_MAX) *
+                                   ((p.ph[0].m_tiles + 1) / 2) * p.ph[0].splits;
+    p.pair_single = !a.group_cnt && pair_env && pair_single_env && a.single_rows <= BN_MAX / 2 &&
+                    paired_units >= sm_count();
     p.b_region = tok_box_bytes(tok_box_index(std::min(a.rows_bound, BN_MAX)));
     const int stage_bytes = (p.pair_single ? 2 : 1) * kABytes + p.b_region;
     p.stage_space = kSmemBudget - kCtrl - 1024;
@@ -556,7 +568,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     const TokenMaps mb0 = token_maps(a.B);
     const WeightMaps ma1 = b ? WeightMaps{{tensor_map(b->A, BM), tensor_map(b->A, 2 * BM)}} : ma0;
     const TokenMaps mb1 = b ? token_maps(b->B) : mb0;
-    long long units = (long long)p.G * p.n_tiles * p.ph[0].m_tiles * p.ph[0].splits;
+    long long units = (long long)p.G * p.n_tiles * (p.pair_single ? (p.ph[0].m_tiles + 1) / 2 : p.ph[0].m_tiles) *
+                      p.ph[0].splits;
     if (b) units += (long long)p.G * p.n_tiles * p.ph[1].m_tiles * p.ph[1].splits;
     const int grid = (int)std::max(1ll, std::min(units, (long long)sm_count()));
     launch_k(k_gemm_tc<EPI0, EPI1>, grid, kThreads, smem, s, ma0, mb0, ma1, mb1, p);

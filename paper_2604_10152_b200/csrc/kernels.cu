@@ -3,7 +3,10 @@
 // are latency-bound; they are written as single-pass, coalesced, 16-byte-vectorised kernels.
 #include <math.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.h"
 #include "gate_dev.cuh"
@@ -39,6 +42,36 @@ __device__ float block_sum(float v, float* red) {
     __syncthreads();
     return red[32];
 }
+
+// In-step timeline of the row kernels (SMOE_TC_TRACE builds, read by tools/tc_trace.py): one record per
+// block -- kernel id, block, entry, dependency wait released, end -- in a device ring.
+#ifdef SMOE_TC_TRACE
+struct RkRec {
+    int kid, blk;
+    long long t_in, t_wait, t_end;
+};
+constexpr int kRkRing = 1 << 18;
+__device__ RkRec g_rk[kRkRing];
+__device__ unsigned g_rk_n;
+__device__ __forceinline__ long long rk_now() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define RK_IN() const long long rk_t0 = rk_now()
+#define RK_WAITED() const long long rk_t1 = rk_now()
+#define RK_END(kid)                                                                  \
+    do {                                                                             \
+        if (threadIdx.x == 0) {                                                      \
+            const unsigned i = atomicAdd(&g_rk_n, 1u) % kRkRing;                     \
+            g_rk[i] = RkRec{kid, (int)blockIdx.x, rk_t0, rk_t1, rk_now()};           \
+        }                                                                            \
+    } while (0)
+#else
+#define RK_IN()
+#define RK_WAITED()
+#define RK_END(kid)
+#endif
 
 template <typename T>
 __device__ __forceinline__ void store_op(void* base, long long idx, float v) {
@@ -83,6 +116,76 @@ __device__ __forceinline__ void store_row_op(void* xa, long long base, const flo
     for (int i = threadIdx.x; i < d; i += blockDim.x) store_op<OT>(xa, base + i, row[i] * inv);
 }
 
+// ---- virtual-block row kernels (resid+rms, gate, combine+rms)
+// These kernels run RT = blockDim.x real threads per row (VB by default, or fewer: SMOE_ROW_THREADS) but
+// always evaluate exactly the reduction tree of a VB-thread block (VB = row_threads(d) or
+// gate_threads(d, E), the trees the pass kernel and the tests pin): real thread t plays virtual threads
+// t + j*RT (j < VB/RT), each accumulating its columns i = vt, vt + VB, ... in order, and the virtual
+// warps' butterflies feed the same final warp.  Split-K partials are loaded four or eight at a time (the
+// old loop issued one dependent load per partial).
+int row_rt(int vb) {
+    static const int rt = [] {
+        const char* v = std::getenv("SMOE_ROW_THREADS");
+        return v ? std::atoi(v) : 0;
+    }();
+    return rt >= 256 && rt < vb && vb % rt == 0 ? rt : vb;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+// sum_{s=0..S-1} P[s][off..off+4) in order from zero; loads issued B at a time
+template <int B>
+__device__ __forceinline__ float4 sum_splits(const float* __restrict__ P, long long pstride, int S, long long off) {
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < S; s0 += B) {
+        float4 q[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+            if (s0 + j < S) q[j] = ld4(P + (s0 + j) * pstride + off);
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+            if (s0 + j < S) add4(y, q[j]);
+    }
+    return y;
+}
+// Virtual-block reduction, stage 1: the butterfly of virtual warp (warp + j * RT/32) -> red[] (all lanes call)
+__device__ __forceinline__ void vwarp_put(float v, int j, float* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) + j * (blockDim.x >> 5)] = v;
+}
+// stage 2: warp 0 butterflies the nvw virtual-warp partials (block_sum's final step); every thread gets it
+__device__ __forceinline__ float vblock_final(int nvw, float* red) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float t = (int)threadIdx.x < nvw ? red[threadIdx.x] : 0.f;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+template <typename OT>
+__device__ __forceinline__ void store4_op(void* base, long long idx, const float4 v, float s);
+template <>
+__device__ __forceinline__ void store4_op<float>(void* base, long long idx, const float4 v, float s) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + idx) = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+}
+template <>
+__device__ __forceinline__ void store4_op<__nv_bfloat16>(void* base, long long idx, const float4 v, float s) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * s, v.y * s), hi = __floats2bfloat162_rn(v.z * s, v.w * s);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + idx) = u;
+}
+// dst row = row * s (the operand-type store of a finished row)
+template <typename OT>
+__device__ __forceinline__ void store_row4(void* dst, long long base, const float4* row, int d4, float s) {
+    for (int i = threadIdx.x; i < d4; i += blockDim.x) store4_op<OT>(dst, base + 4ll * i, row[i], s);
+}
+
 template <typename OT>
 __global__ void k_x0_rms(const double* __restrict__ emb, const double* __restrict__ ssum, const int* __restrict__ slen,
                          const int* __restrict__ pend, int pstride, const int* __restrict__ row_seq,
@@ -112,71 +215,75 @@ __global__ void k_x0_rms(const double* __restrict__ emb, const double* __restric
 }
 
 template <typename OT>
-__global__ void k_resid_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride, int d,
+__global__ void __launch_bounds__(1024) k_resid_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride, int d,
                             void* __restrict__ xa) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ float row[];
+    extern __shared__ float4 row4[];
     __shared__ float red[33];
     const long long base = (long long)blockIdx.x * d;
-    float ss = 0.f;
-    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
-        float4 v = *reinterpret_cast<const float4*>(x + base + i4);
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < S; ++s) {
-            const float4 p = *reinterpret_cast<const float4*>(P + s * pstride + base + i4);
-            a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
+    const int d4 = d >> 2, VB = row_threads(d), RT = blockDim.x, nv = VB / RT;
+#pragma unroll 1
+    for (int j = 0; j < nv; ++j) {
+        float ss = 0.f;
+        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+            float4 v = ld4(x + base + 4ll * i);
+            add4(v, sum_splits<8>(P, pstride, S, base + 4ll * i));
+            *reinterpret_cast<float4*>(x + base + 4ll * i) = v;
+            row4[i] = v;
+            ss = __fadd_rn(ss, sumsq4(v));
         }
-        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
-        *reinterpret_cast<float4*>(x + base + i4) = v;
-        *reinterpret_cast<float4*>(row + i4) = v;
-        ss = __fadd_rn(ss, sumsq4(v));
+        vwarp_put(ss, j, red);
     }
-    ss = block_sum(ss, red);
-    store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
+    const float tot = vblock_final(VB >> 5, red);
+    store_row4<OT>(xa, base, row4, d4, 1.0f / sqrtf(tot / (float)d + 1e-12f));
 }
 
 // ------------------------------------------------------------------ K4/K5 gate + remap
 template <typename OT>
-__global__ void k_gate(GateArgs a) {
+__global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
+    RK_IN();
     pdl_wait();
     pdl_trigger();
+    RK_WAITED();
     extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[8*32 + 33]
     float* xf = sm;
     float* gl = xf + a.d;
     float* red = gl + 2 * a.E;
-    const int r = blockIdx.x, d = a.d, E = a.E, K = a.K;
+    const int r = blockIdx.x, d = a.d, E = a.E, K = a.K, d4 = d >> 2;
+    const int VB = gate_threads(d, E), RT = blockDim.x, nv = VB / RT;
     const long long base = (long long)r * d;
+    float4* xf4 = reinterpret_cast<float4*>(xf);
     // residual add of the mix GEMM's split-K partials (model.cpp:224), then rms (model.cpp:226)
-    float ss = 0.f;
-    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
-        float4 v = *reinterpret_cast<const float4*>(a.x + base + i4);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < a.s_mix; ++s) {
-            const float4 q = *reinterpret_cast<const float4*>(a.pmix + s * a.pstride + base + i4);
-            acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+#pragma unroll 1
+    for (int j = 0; j < nv; ++j) {
+        float ss = 0.f;
+        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+            float4 v = ld4(a.x + base + 4ll * i);
+            add4(v, sum_splits<8>(a.pmix, a.pstride, a.s_mix, base + 4ll * i));
+            *reinterpret_cast<float4*>(a.x + base + 4ll * i) = v;
+            xf4[i] = v;
+            ss = __fadd_rn(ss, sumsq4(v));
         }
-        v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
-        *reinterpret_cast<float4*>(a.x + base + i4) = v;
-        *reinterpret_cast<float4*>(xf + i4) = v;
-        ss = __fadd_rn(ss, sumsq4(v));
+        vwarp_put(ss, j, red + 8 * 32);
     }
-    ss = block_sum(ss, red + 8 * 32);
-    const float inv = 1.0f / sqrtf(ss / (float)d + 1e-12f);
-    for (int i = threadIdx.x; i < d; i += blockDim.x) xf[i] *= inv;
+    const float inv = 1.0f / sqrtf(vblock_final(VB >> 5, red + 8 * 32) / (float)d + 1e-12f);
+    for (int i = threadIdx.x; i < d4; i += blockDim.x) {
+        const float4 v = xf4[i];
+        xf4[i] = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+    }
     __syncthreads();
-    // gate GEMV (model.cpp:229-230): warp w owns experts w, w+nw, ...; each lane strides d in float4s
-    // (fixed order, then a butterfly), so every row's logits are computed identically in any pass
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    {
-        const float4* xv = reinterpret_cast<const float4*>(xf);
-        const int d4 = d >> 2;
-        for (int e = w; e < E; e += nw) {
+    // gate GEMV (model.cpp:229-230): virtual warp vw owns experts vw, vw + VB/32, ...; each lane strides
+    // d in float4s (fixed order, then a butterfly), so every row's logits are computed identically in
+    // any pass.  Real warp w plays virtual warps w, w + RT/32, ...
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5, nvw = VB >> 5;
+    for (int vw = w; vw < nvw; vw += nw) {
+        for (int e = vw; e < E; e += nvw) {
             const float4* g = reinterpret_cast<const float4*>(a.gate_w + (long long)e * d);
             float acc = 0.f;
 #pragma unroll 8
             for (int i = lane; i < d4; i += 32) {
-                acc = __fadd_rn(acc, dot4f(g[i], xv[i]));
+                acc = __fadd_rn(acc, dot4f(g[i], xf4[i]));
             }
             acc = warp_sum(acc);
             if (lane == 0) gl[e] = acc + a.gate_b[e];
@@ -196,43 +303,55 @@ __global__ void k_gate(GateArgs a) {
             base = a.peer_x[e / a.ep_eo];
             row = (long long)(a.ep_me * a.ep_eo + e % a.ep_eo) * sg + (row - (long long)e * sg);
         }
-        store_row_op<OT>(base, row * d, xf, d, 1.0f);
+        store_row4<OT>(base, row * d, xf4, d4, 1.0f);
     }
     if (a.peer_x) __threadfence_system();
+    RK_END(1);
 }
 
 // ------------------------------------------------------------------ K9 combine (+ next rms)
 template <typename OT>
-__global__ void k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
+__global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
                               const int* __restrict__ pos, const float* __restrict__ wgt, int K, int d, int dense,
                               void* __restrict__ xa) {
+    RK_IN();
     pdl_wait();
     pdl_trigger();
-    extern __shared__ float row[];
+    RK_WAITED();
+    extern __shared__ float4 row4[];
     __shared__ float red[33];
-    const int t = blockIdx.x;
+    __shared__ long long src_s[16];
+    __shared__ float w_s[16];
+    const int t = blockIdx.x, d4 = d >> 2, VB = row_threads(d), RT = blockDim.x, nv = VB / RT;
+    const int nk = dense ? 1 : K;
     const long long base = (long long)t * d;
-    float ss = 0.f;
-    for (int i4 = threadIdx.x * 4; i4 < d; i4 += blockDim.x * 4) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int k = 0; k < (dense ? 1 : K); ++k) {
-            const long long src = (dense ? (long long)t : pos ? (long long)pos[t * K + k] : (long long)t * K + k) * d + i4;
-            float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s = 0; s < S; ++s) {
-                const float4 q = *reinterpret_cast<const float4*>(P + s * pstride + src);
-                y.x += q.x; y.y += q.y; y.z += q.z; y.w += q.w;
-            }
-            if (dense) acc = y;
-            else axpy4(acc, wgt[t * K + k], y);
-        }
-        float4 v = *reinterpret_cast<const float4*>(x + base + i4);
-        v.x += acc.x; v.y += acc.y; v.z += acc.z; v.w += acc.w;
-        *reinterpret_cast<float4*>(x + base + i4) = v;
-        *reinterpret_cast<float4*>(row + i4) = v;
-        ss = __fadd_rn(ss, sumsq4(v));
+    if (threadIdx.x < nk) {  // the K picks' partial rows and weights, read once per block
+        const int k = threadIdx.x;
+        src_s[k] = (dense ? (long long)t : pos ? (long long)pos[t * K + k] : (long long)t * K + k) * d;
+        w_s[k] = dense ? 1.f : wgt[t * K + k];
     }
-    ss = block_sum(ss, red);
-    store_row_op<OT>(xa, base, row, d, 1.0f / sqrtf(ss / (float)d + 1e-12f));
+    __syncthreads();
+#pragma unroll 1
+    for (int j = 0; j < nv; ++j) {
+        float ss = 0.f;
+        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < nk; ++k) {
+                const float4 y = sum_splits<4>(P, pstride, S, src_s[k] + 4ll * i);
+                if (dense) acc = y;
+                else axpy4(acc, w_s[k], y);
+            }
+            float4 v = ld4(x + base + 4ll * i);
+            add4(v, acc);
+            *reinterpret_cast<float4*>(x + base + 4ll * i) = v;
+            row4[i] = v;
+            ss = __fadd_rn(ss, sumsq4(v));
+        }
+        vwarp_put(ss, j, red);
+    }
+    const float tot = vblock_final(VB >> 5, red);
+    store_row4<OT>(xa, base, row4, d4, 1.0f / sqrtf(tot / (float)d + 1e-12f));
+    RK_END(2);
 }
 
 // ------------------------------------------------------------------ K10 argmax
@@ -404,8 +523,8 @@ void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T,
                       cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
-    if (op == kF32) launch_k(k_resid_rms<float>, T, row_threads(d), sm, s, x, P, S, pstride, d, xa);
-    else launch_k(k_resid_rms<__nv_bfloat16>, T, row_threads(d), sm, s, x, P, S, pstride, d, xa);
+    if (op == kF32) launch_k(k_resid_rms<float>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, d, xa);
+    else launch_k(k_resid_rms<__nv_bfloat16>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, d, xa);
 }
 
 void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s) {
@@ -417,7 +536,7 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
-    const int threads = gate_threads(a.d, a.E);  // one row per block, a warp per expert for the GEMV
+    const int threads = row_rt(gate_threads(a.d, a.E));  // one row per block, a (virtual) warp per expert
     if (a.op == kF32) launch_k(k_gate<float>, a.T, threads, smem, s, a);
     else launch_k(k_gate<__nv_bfloat16>, a.T, threads, smem, s, a);
 }
@@ -427,9 +546,9 @@ void launch_combine_rms(float* x, const float* P, int S, long long pstride, cons
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
     if (op == kF32)
-        launch_k(k_combine_rms<float>, T, row_threads(d), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_k(k_combine_rms<float>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
     else
-        launch_k(k_combine_rms<__nv_bfloat16>, T, row_threads(d), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_k(k_combine_rms<__nv_bfloat16>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
@@ -496,3 +615,24 @@ void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, lo
 }
 
 }  // namespace smoe
+
+extern "C" int smoe_rk_trace_dump(const char* path) {
+#ifdef SMOE_TC_TRACE
+    using namespace smoe;
+    std::vector<RkRec> r(kRkRing);
+    unsigned n = 0;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    cudaMemcpyFromSymbol(r.data(), g_rk, r.size() * sizeof(RkRec));
+    cudaMemcpyFromSymbol(&n, g_rk_n, sizeof(n));
+    FILE* fp = fopen(path, "wb");
+    if (!fp) return -3;
+    const int cnt = (int)std::min<unsigned>(n, kRkRing);
+    fwrite(&cnt, sizeof(int), 1, fp);
+    fwrite(r.data(), sizeof(RkRec), cnt, fp);
+    fclose(fp);
+    return 0;
+#else
+    (void)path;
+    return -1;
+#endif
+}

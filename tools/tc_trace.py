@@ -35,6 +35,24 @@ def run(B, gamma, out):
     lib.smoe_tc_trace_dump.argtypes = [C.c_char_p]
     rc = lib.smoe_tc_trace_dump(out.encode())
     assert rc == 0, rc
+    lib.smoe_rk_trace_dump.argtypes = [C.c_char_p]
+    lib.smoe_rk_trace_dump(out.replace(".bin", "_rk.bin").encode())  # row kernels (gate, combine)
+
+
+def row_kernel_launches(path):
+    """Row-kernel launches from the per-block records: kernel id -> [(entry, wait released, end)]."""
+    if not os.path.exists(path):
+        return {}
+    raw = open(path, "rb").read()
+    n = int(np.frombuffer(raw[:4], np.int32)[0])
+    rec = np.frombuffer(raw[4:4 + n * 32], dtype=np.dtype(
+        [("kid", np.int32), ("blk", np.int32), ("t_in", np.int64), ("t_wait", np.int64), ("t_end", np.int64)]))
+    out = {}
+    for kid in np.unique(rec["kid"]):
+        r = np.sort(rec[rec["kid"] == kid], order="t_in")
+        cut = np.nonzero(np.diff(r["t_in"]) > 30_000)[0] + 1  # launches of one kernel are >= ~250 us apart
+        out[int(kid)] = [(int(g["t_in"].min()), int(g["t_wait"].min()), int(g["t_end"].max())) for g in np.split(r, cut)]
+    return out
 
 
 def analyze(path):
@@ -72,7 +90,8 @@ def analyze(path):
                  up_unit_us=float(np.median(unit_us[up])) if up.any() else 0.0,
                  down_unit_us=float(np.median(unit_us[~up])) if (~up).any() else 0.0,
                  n_up=int(up.sum()), n_down=int((~up).sum()),
-                 cta_start_spread=float((cta[s, :grid, 0].max() - t0) / 1e3))
+                 cta_start_spread=float((cta[s, :grid, 0].max() - t0) / 1e3),
+                 t0=int(t0), t1=int(t1), first_stage=int(first_full.min()))
         rows.append(r)
     rows.sort(key=lambda r: r["launch"])
     # aggregate per class (moe launches split by their unit count: draft passes touch fewer experts)
@@ -85,6 +104,47 @@ def analyze(path):
         print(json.dumps(dict(kind=key[0], n_up=key[1], n_down=key[2], launches=len(rs), dur_us=f("dur_us"),
                               ramp_us=f("ramp_us"), tail_us=f("tail_us"), up_unit_us=f("up_unit_us"),
                               down_unit_us=f("down_unit_us"), cta_start_spread=f("cta_start_spread"))))
+    # in-step timeline between consecutive fused MoE launches: the previous MoE launch's end -> the
+    # mix launch (start, end) -> this MoE launch's first full weight stage
+    gaps = []
+    prev = None
+    mix = None
+    for r in rows:
+        if r["kind"] == "mix/head":
+            mix = r
+            continue
+        if prev is not None and mix is not None and mix["t0"] > prev["t1"] - 50_000:
+            gaps.append(dict(between_moe_us=(r["first_stage"] - prev["t1"]) / 1e3,
+                             mix_start_us=(mix["t0"] - prev["t1"]) / 1e3, mix_end_us=(mix["t1"] - prev["t1"]) / 1e3,
+                             moe_launch_us=(r["t0"] - prev["t1"]) / 1e3, moe_dur_us=r["dur_us"]))
+        prev, mix = r, None
+    rk = row_kernel_launches(path.replace(".bin", "_rk.bin"))
+    if rk:
+        # per MoE launch: the combine after it and the gate before the next one, relative to its end
+        moes = [r for r in rows if r["kind"] != "mix/head"]
+        mixes = [r for r in rows if r["kind"] == "mix/head"]
+        tl = {"draft": [], "verify": []}
+        for a, b in zip(moes, moes[1:]):
+            t1 = a["t1"]
+            comb = [c for c in rk.get(2, []) if t1 - 100_000 < c[0] and c[2] > t1 and c[2] < b["t0"] + 50_000]
+            gate = [c for c in rk.get(1, []) if a["t1"] - 100_000 < c[0] and c[2] < b["first_stage"] and c[2] > t1]
+            mix = [m for m in mixes if m["t1"] > t1 and m["t1"] < b["first_stage"]]
+            if len(comb) != 1 or len(gate) != 1 or len(mix) != 1:
+                continue
+            c, g, m = comb[0], gate[0], mix[0]
+            us = lambda t: (t - t1) / 1e3  # noqa: E731
+            tl["verify" if b["n_up"] > 1000 else "draft"].append(dict(
+                combine_in=us(c[0]), combine_waited=us(c[1]), combine_end=us(c[2]),
+                mix_start=us(m["t0"]), mix_first_stage=us(m["first_stage"]), mix_end=us(m["t1"]),
+                gate_in=us(g[0]), gate_waited=us(g[1]), gate_end=us(g[2]),
+                moe_launch=us(b["t0"]), moe_first_stage=us(b["first_stage"]), moe_end=us(b["t1"])))
+        for k, v in tl.items():
+            if v:
+                print(json.dumps({"timeline_after_moe_end_us": k, "n": len(v),
+                                  **{f: round(float(np.median([x[f] for x in v])), 2) for f in v[0]}}))
+    if gaps:
+        print(json.dumps({"between_moe_launches": {k: round(float(np.median([g[k] for g in gaps])), 2) for k in gaps[0]},
+                          "n": len(gaps)}))
     return rows
 
 
@@ -95,7 +155,7 @@ if __name__ == "__main__":
         B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
         g = int(sys.argv[2]) if len(sys.argv) > 2 else 4
         os.makedirs("gpurun_out", exist_ok=True)
-        out = f"gpurun_out/tc_trace_b{B}{os.environ.get('TAG', '')}.bin"
+        out = f"/tmp/tc_trace_b{B}{os.environ.get('TAG', '')}.bin"  # large; only the summary travels back
         run(B, g, out)
         rows = analyze(out)
-        json.dump(rows, open(out.replace(".bin", ".json"), "w"), indent=0)
+        json.dump(rows, open("gpurun_out/" + os.path.basename(out).replace(".bin", ".json"), "w"), indent=0)
