@@ -210,11 +210,12 @@ Engine::Engine(const smoe_engine_config& c) {
     seqs = dalloc<int>(Bmax);
     flags = dalloc<int>(1);
     SMOE_CUDA(cudaMemset(flags, 0, sizeof(int)));
-    sched = dalloc<int>(4);  // two counter slots: consecutive GEMM launches may overlap under PDL
-    SMOE_CUDA(cudaMemset(sched, 0, 4 * sizeof(int)));
+    sched = dalloc<int>(8);  // two counter slots: consecutive GEMM launches may overlap under PDL
+    SMOE_CUDA(cudaMemset(sched, 0, 8 * sizeof(int)));
     moe_done = dalloc<int>(128);
     SMOE_CUDA(cudaMemset(moe_done, 0, 128 * sizeof(int)));
     if (const char* v = getenv("SMOE_FUSED_MOE")) fuse_moe = atoi(v) != 0;
+    if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
     if (const char* v = getenv("SMOE_PASS_KERNEL")) pass_kernel = atoi(v) != 0;
     if (const char* v = getenv("SMOE_PASS_MAX_ROWS")) pass_kernel_max_rows = atoi(v);
     if (const char* v = getenv("SMOE_PASS_MIN_ROWS")) pass_kernel_min_rows = atoi(v);
@@ -643,7 +644,7 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
     if (use_tc) {
         if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
         TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, gcnt, gslot, G, seg, single_rows, single_slot, rows_bound,
-                     Y, ldy, epi, splits, split_stride, sched + 2 * (gemm_launches++ & 1)};
+                     Y, ldy, epi, splits, split_stride, sched + 4 * (gemm_launches++ & 1)};
         launch_gemm_tc(a, stream);
     } else {
         if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");
@@ -674,10 +675,14 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
     cudaEvent_t ev;
     prof_begin(cls, &ev);
     const unsigned slot = gemm_launches++ & 1;
-    TcGemmArgs up{op_up, U, *xop, f, d, cnt, slots, E, T, 0, 0, T, hbuf, f, up_epi, 1, 0, sched + 2 * slot,
+    TcGemmArgs up{op_up, U, *xop, f, d, cnt, slots, E, T, 0, 0, T, hbuf, f, up_epi, 1, 0, sched + 4 * slot,
                   moe_done + 64 * slot};
     TcGemmArgs dn{op_down, d, op_h, d, f, cnt, slots, E, T, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
-                  sched + 2 * slot, moe_done + 64 * slot};
+                  sched + 4 * slot, moe_done + 64 * slot};
+    if (l2_next && l2_prefetch) {
+        up.l2_next = l2_next;
+        up.l2_next_bytes = (long long)d * d * (long long)ws;
+    }
     if (peer_y) {
         dn.peer_y = peer_y;
         dn.peer_eo = E / ep_world;
@@ -748,7 +753,9 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             if (fetch) store_fetch_layer(mo, T, rl, cnt);  // expert store: migrate this layer's missing experts
             // weight slots: the store's table for this layer's fetch, else the resident slot map (draft
             // passes touch only pinned draft experts)
+            l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
             expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
+            l2_next = nullptr;
             if (fetch) store_finish_layer(mo);
             {
                 // K9 combine + residual + the next layer's (or the head's) rms

@@ -46,10 +46,13 @@ struct TcGemmArgs {
     Epi epi;
     int splits;               // K splits (kEpiStoreF32 only): partial ks written at Y + ks*split_stride
     long long split_stride;
-    int* sched;               // device [2] zero-initialised work counter (self-resetting)
+    int* sched;               // device [3] zero-initialised work counters (self-resetting)
     int* done = nullptr;      // device [64] zeroed per-group completion counters (fused launches)
     void* const* peer_y = nullptr;  // EP fused return (see tc::Phase): device table of the ranks' return buffers
     int peer_eo = 0, peer_me = 0;
+    // bytes to prefetch into L2 once the launch runs out of units (its tail): the next layer's Mix weights
+    const void* l2_next = nullptr;
+    long long l2_next_bytes = 0;
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
 // One launch for a MoE layer's grouped up- (tanh / SwiGLU) and down-projection (f32 split partials):
@@ -197,6 +200,7 @@ public:
     void* xperm = nullptr;  // [E*Tmax][d] expert segments of T rows (gate dispatch)
     void* hbuf = nullptr;   // [E*Tmax][f]
     float* ybuf = nullptr;  // [s_down][E*Tmax][d] split-K partials of the down projection
+    const void* l2_next = nullptr;  // next layer's Mix weights, prefetched into L2 in the MoE launch's tail
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
     int s_mix = 1, s_down = 1;
     float* logits = nullptr;  // [Tmax][V]
@@ -210,9 +214,10 @@ public:
     int* commit_take = nullptr;  // [Bmax]
     int* seqs = nullptr;         // [Bmax]
     int* flags = nullptr;
-    int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][2]
+    int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][4]
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
+    int l2_prefetch = 1;         // MoE launch tail prefetches the next Mix weights into L2 (env SMOE_L2_PREFETCH=0: off)
     // one persistent launch per pass (pass_tc.cu), opt-in with env SMOE_PASS_KERNEL=1: bit-identical to
     // the per-layer launches but 2-4% slower end to end at B = 1..64 (profiles/r02_pass_kernel.md)
     int pass_kernel = 0;

@@ -75,7 +75,9 @@ struct TcParams {
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
     int pair_ok;           // grouped launches: phases (bit 0 up, bit 1 down) that may use pair units
     int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
-    int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
+    int* sched;            // [3]: next-unit counter, finished-CTA counter, L2 prefetch chunk counter (self-resetting)
+    const uint8_t* pf;     // prefetched into L2 by the producers that run out of units (the launch's tail)
+    long long pf_bytes;
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
 };
@@ -103,6 +105,7 @@ __device__ __forceinline__ long long gtimer() {
 // TMA issue count per weight byte halves, which is what bounded the stream: isolated up projection
 // 0.865 -> 0.97 of the HBM copy peak, down 0.80 -> 0.99 (tools/gemm_bench.py, T <= 32).  Needs groups of
 // <= 128 tokens (2 accumulators x 2 buffers x 128 TMEM columns).
+constexpr long long kPfChunk = 256 * 1024;
 __device__ __forceinline__ int row_tiles(const Phase& P, int pair) { return pair ? (P.m_tiles + 1) / 2 : P.m_tiles; }
 
 // Stage ring of a grouped launch from the routing counts (call after the dependency wait; every role
@@ -282,7 +285,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
                 ring[r] = u < total_units ? u : -1;
                 mbar_arrive(&ring_full[r]);
-                if (u >= total_units) break;
+                if (u >= total_units) {
+                    // out of units: the launch's tail has begun and HBM has spare bandwidth; pull the next
+                    // launch's weights (the next layer's Mix, 32 MB at C2) into L2 in 256 KB chunks
+                    for (;;) {
+                        const long long off = (long long)atomicAdd(&p.sched[2], 1) * kPfChunk;
+                        if (off >= p.pf_bytes) break;
+                        const uint32_t n = (uint32_t)min((long long)kPfChunk, p.pf_bytes - off);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf + off), "r"(n) : "memory");
+                    }
+                    break;
+                }
                 const CUtensorMap* mA = w.phase ? &mapA1.m[w.pair] : &mapA0.m[w.pair];
                 const int a_space = (pair ? 2 : 1) * kABytes;  // weight space of a stage (tokens after it)
                 const int a_bytes = (w.pair ? 2 : 1) * kABytes;  // one 128- or 256-row weight box
@@ -419,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         if (atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1) {
             p.sched[0] = 0;
+            p.sched[2] = 0;
             if (p.nphase > 1)
                 for (int g = 0; g < p.G; ++g) p.done[g] = 0;
             p.sched[1] = 0;
@@ -562,6 +576,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.stages = std::max(2, std::min(kMaxStages, p.stage_space / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
+    p.pf = static_cast<const uint8_t*>(a.l2_next);
+    p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
     p.tr = g_launch_no++;
     const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;
     const WeightMaps ma0{{tensor_map(a.A, BM), tensor_map(a.A, 2 * BM)}};

@@ -1,6 +1,7 @@
 // kernels.cu -- state, normalisation, gating/routing, permutation, combine, argmax, accept and
 // commit kernels of the spec-decode hot path (sm_100a).  These move a few MB per pass, so they
 // are latency-bound; they are written as single-pass, coalesced, 16-byte-vectorised kernels.
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include <algorithm>
@@ -117,18 +118,32 @@ __device__ __forceinline__ void store_row_op(void* xa, long long base, const flo
 }
 
 // ---- virtual-block row kernels (resid+rms, gate, combine+rms)
-// These kernels run RT = blockDim.x real threads per row (VB by default, or fewer: SMOE_ROW_THREADS) but
-// always evaluate exactly the reduction tree of a VB-thread block (VB = row_threads(d) or
-// gate_threads(d, E), the trees the pass kernel and the tests pin): real thread t plays virtual threads
-// t + j*RT (j < VB/RT), each accumulating its columns i = vt, vt + VB, ... in order, and the virtual
-// warps' butterflies feed the same final warp.  Split-K partials are loaded four or eight at a time (the
-// old loop issued one dependent load per partial).
+// These kernels always evaluate exactly the reduction tree of a VB-thread block (VB = row_threads(d) or
+// gate_threads(d, E), the trees the pass kernel and the tests pin), whatever the launch shape: a row is
+// processed by a cluster of C CTAs of RT threads (RowCtx below), each real thread playing one or more
+// virtual threads that accumulate their columns in order, and the virtual warps' butterflies feed the
+// same final warp.  Default shape: C = VB/256 CTAs of 256 threads per row (SMOE_ROW_CLUSTER=0: one
+// VB-thread block per row, or SMOE_ROW_THREADS fewer threads).  Small CTAs sit beside a GEMM CTA on an
+// SM (a 1024-thread block at 64 registers fills the register file, so the next Mix launch's CTAs could
+// not start on the SMs of the combine), and spread a draft pass's 64 rows over 4x the SMs.  Split-K
+// partials are loaded four or eight at a time (the old loop issued one dependent load per partial).
 int row_rt(int vb) {
     static const int rt = [] {
         const char* v = std::getenv("SMOE_ROW_THREADS");
         return v ? std::atoi(v) : 0;
     }();
     return rt >= 256 && rt < vb && vb % rt == 0 ? rt : vb;
+}
+struct RowShape {
+    int C, RT;
+};
+RowShape row_shape(int vb) {
+    static const bool cl = [] {
+        const char* v = std::getenv("SMOE_ROW_CLUSTER");
+        return v && v[0] == '1';
+    }();
+    if (cl && vb > 256) return {vb / 256, 256};
+    return {1, row_rt(vb)};
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
@@ -150,21 +165,49 @@ __device__ __forceinline__ float4 sum_splits(const float* __restrict__ P, long l
     }
     return y;
 }
-// Virtual-block reduction, stage 1: the butterfly of virtual warp (warp + j * RT/32) -> red[] (all lanes call)
-__device__ __forceinline__ void vwarp_put(float v, int j, float* red) {
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) + j * (blockDim.x >> 5)] = v;
-}
-// stage 2: warp 0 butterflies the nvw virtual-warp partials (block_sum's final step); every thread gets it
-__device__ __forceinline__ float vblock_final(int nvw, float* red) {
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float t = (int)threadIdx.x < nvw ? red[threadIdx.x] : 0.f;
-        t = warp_sum(t);
-        if (threadIdx.x == 0) red[32] = t;
+// Row layout of these kernels: a row is processed by a cluster of C CTAs (C = 1: no cluster) of RT
+// threads each; CTA c, thread t plays virtual threads vt = c*RT + t + j*C*RT (j < VB / (C*RT)).
+struct RowCtx {
+    int C, c, RT, VB, nv;
+    __device__ RowCtx(int vb) : VB(vb) {
+        C = (int)cooperative_groups::this_cluster().num_blocks();
+        c = C > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+        RT = blockDim.x;
+        nv = VB / (C * RT);
     }
-    __syncthreads();
-    return red[32];
+    __device__ int vt(int j) const { return c * RT + (int)threadIdx.x + j * C * RT; }
+    __device__ int row() const { return (int)blockIdx.x / C; }
+    __device__ void sync() const {
+        if (C > 1) cooperative_groups::this_cluster().sync();
+        else __syncthreads();
+    }
+    // value v -> dst[idx] of every CTA of the row's cluster (shared memory)
+    template <typename V>
+    __device__ void put_all(V* dst, int idx, V v) const {
+        if (C == 1) {
+            dst[idx] = v;
+            return;
+        }
+        auto cl = cooperative_groups::this_cluster();
+        for (int q = 0; q < C; ++q) cl.map_shared_rank(dst, q)[idx] = v;
+    }
+    template <typename V>
+    __device__ void put0(V* dst, int idx, V v) const {  // -> CTA 0 of the cluster
+        if (C == 1) dst[idx] = v;
+        else cooperative_groups::this_cluster().map_shared_rank(dst, 0)[idx] = v;
+    }
+};
+// Virtual-block reduction (block_sum's tree over VB threads), stage 1: the butterfly of virtual warp
+// vt(j)/32 -> red[] in every CTA of the cluster (all lanes call)
+__device__ __forceinline__ void vwarp_put(const RowCtx& rc, float v, int j, float* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) rc.put_all(red, rc.vt(j) >> 5, v);
+}
+// stage 2 (after rc.sync()): block_sum's final butterfly over the VB/32 virtual-warp partials, evaluated
+// by every warp (identical inputs, identical result)
+__device__ __forceinline__ float vblock_total(int nvw, const float* red) {
+    const int lane = threadIdx.x & 31;
+    return warp_sum(lane < nvw ? red[lane] : 0.f);
 }
 template <typename OT>
 __device__ __forceinline__ void store4_op(void* base, long long idx, const float4 v, float s);
@@ -221,22 +264,26 @@ __global__ void __launch_bounds__(1024) k_resid_rms(float* __restrict__ x, const
     pdl_trigger();
     extern __shared__ float4 row4[];
     __shared__ float red[33];
-    const long long base = (long long)blockIdx.x * d;
-    const int d4 = d >> 2, VB = row_threads(d), RT = blockDim.x, nv = VB / RT;
+    const RowCtx rc(row_threads(d));
+    const long long base = (long long)rc.row() * d;
+    const int d4 = d >> 2;
 #pragma unroll 1
-    for (int j = 0; j < nv; ++j) {
+    for (int j = 0; j < rc.nv; ++j) {
         float ss = 0.f;
-        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+        for (int i = rc.vt(j); i < d4; i += rc.VB) {
             float4 v = ld4(x + base + 4ll * i);
             add4(v, sum_splits<8>(P, pstride, S, base + 4ll * i));
             *reinterpret_cast<float4*>(x + base + 4ll * i) = v;
             row4[i] = v;
             ss = __fadd_rn(ss, sumsq4(v));
         }
-        vwarp_put(ss, j, red);
+        vwarp_put(rc, ss, j, red);
     }
-    const float tot = vblock_final(VB >> 5, red);
-    store_row4<OT>(xa, base, row4, d4, 1.0f / sqrtf(tot / (float)d + 1e-12f));
+    rc.sync();
+    const float inv = 1.0f / sqrtf(vblock_total(rc.VB >> 5, red) / (float)d + 1e-12f);
+#pragma unroll 1
+    for (int j = 0; j < rc.nv; ++j)
+        for (int i = rc.vt(j); i < d4; i += rc.VB) store4_op<OT>(xa, base + 4ll * i, row4[i], inv);
 }
 
 // ------------------------------------------------------------------ K4/K5 gate + remap
@@ -249,36 +296,41 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[8*32 + 33]
     float* xf = sm;
     float* gl = xf + a.d;
-    float* red = gl + 2 * a.E;
-    const int r = blockIdx.x, d = a.d, E = a.E, K = a.K, d4 = d >> 2;
-    const int VB = gate_threads(d, E), RT = blockDim.x, nv = VB / RT;
+    float* red = gl + 2 * a.E + 8 * 32;
+    const RowCtx rc(gate_threads(a.d, a.E));
+    const int r = rc.row(), d = a.d, E = a.E, K = a.K, d4 = d >> 2;
     const long long base = (long long)r * d;
     float4* xf4 = reinterpret_cast<float4*>(xf);
     // residual add of the mix GEMM's split-K partials (model.cpp:224), then rms (model.cpp:226)
 #pragma unroll 1
-    for (int j = 0; j < nv; ++j) {
+    for (int j = 0; j < rc.nv; ++j) {
         float ss = 0.f;
-        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+        for (int i = rc.vt(j); i < d4; i += rc.VB) {
             float4 v = ld4(a.x + base + 4ll * i);
             add4(v, sum_splits<8>(a.pmix, a.pstride, a.s_mix, base + 4ll * i));
             *reinterpret_cast<float4*>(a.x + base + 4ll * i) = v;
             xf4[i] = v;
             ss = __fadd_rn(ss, sumsq4(v));
         }
-        vwarp_put(ss, j, red + 8 * 32);
+        vwarp_put(rc, ss, j, red);
     }
-    const float inv = 1.0f / sqrtf(vblock_final(VB >> 5, red + 8 * 32) / (float)d + 1e-12f);
-    for (int i = threadIdx.x; i < d4; i += blockDim.x) {
-        const float4 v = xf4[i];
-        xf4[i] = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
-    }
-    __syncthreads();
+    rc.sync();
+    const float inv = 1.0f / sqrtf(vblock_total(rc.VB >> 5, red) / (float)d + 1e-12f);
+    // the normalised row, whole, in every CTA of the cluster
+#pragma unroll 1
+    for (int j = 0; j < rc.nv; ++j)
+        for (int i = rc.vt(j); i < d4; i += rc.VB) {
+            const float4 v = xf4[i];
+            rc.put_all(xf4, i, make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv));
+        }
+    rc.sync();
     // gate GEMV (model.cpp:229-230): virtual warp vw owns experts vw, vw + VB/32, ...; each lane strides
     // d in float4s (fixed order, then a butterfly), so every row's logits are computed identically in
-    // any pass.  Real warp w plays virtual warps w, w + RT/32, ...
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5, nvw = VB >> 5;
-    for (int vw = w; vw < nvw; vw += nw) {
-        for (int e = vw; e < E; e += nvw) {
+    // any pass.  The logits are gathered in CTA 0 of the cluster.
+    const int lane = threadIdx.x & 31, nvw = rc.VB >> 5;
+#pragma unroll 1
+    for (int j = 0; j < rc.nv; ++j) {
+        for (int e = rc.vt(j) >> 5; e < E; e += nvw) {
             const float4* g = reinterpret_cast<const float4*>(a.gate_w + (long long)e * d);
             float acc = 0.f;
 #pragma unroll 8
@@ -286,10 +338,11 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
                 acc = __fadd_rn(acc, dot4f(g[i], xf4[i]));
             }
             acc = warp_sum(acc);
-            if (lane == 0) gl[e] = acc + a.gate_b[e];
+            if (lane == 0) rc.put0(gl, e, acc + a.gate_b[e]);
         }
     }
-    __syncthreads();
+    rc.sync();
+    if (rc.c != 0) return;  // CTA 0 selects and dispatches the row
     // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
     if (threadIdx.x < 32) gate_select_warp(a, r, gl, dst);
@@ -322,7 +375,8 @@ __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, con
     __shared__ float red[33];
     __shared__ long long src_s[16];
     __shared__ float w_s[16];
-    const int t = blockIdx.x, d4 = d >> 2, VB = row_threads(d), RT = blockDim.x, nv = VB / RT;
+    const RowCtx rc(row_threads(d));
+    const int t = rc.row(), d4 = d >> 2;
     const int nk = dense ? 1 : K;
     const long long base = (long long)t * d;
     if (threadIdx.x < nk) {  // the K picks' partial rows and weights, read once per block
@@ -332,9 +386,9 @@ __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, con
     }
     __syncthreads();
 #pragma unroll 1
-    for (int j = 0; j < nv; ++j) {
+    for (int j = 0; j < rc.nv; ++j) {
         float ss = 0.f;
-        for (int i = threadIdx.x + j * RT; i < d4; i += VB) {
+        for (int i = rc.vt(j); i < d4; i += rc.VB) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int k = 0; k < nk; ++k) {
                 const float4 y = sum_splits<4>(P, pstride, S, src_s[k] + 4ll * i);
@@ -347,10 +401,13 @@ __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, con
             row4[i] = v;
             ss = __fadd_rn(ss, sumsq4(v));
         }
-        vwarp_put(ss, j, red);
+        vwarp_put(rc, ss, j, red);
     }
-    const float tot = vblock_final(VB >> 5, red);
-    store_row4<OT>(xa, base, row4, d4, 1.0f / sqrtf(tot / (float)d + 1e-12f));
+    rc.sync();
+    const float inv = 1.0f / sqrtf(vblock_total(rc.VB >> 5, red) / (float)d + 1e-12f);
+#pragma unroll 1
+    for (int j = 0; j < rc.nv; ++j)
+        for (int i = rc.vt(j); i < d4; i += rc.VB) store4_op<OT>(xa, base + 4ll * i, row4[i], inv);
     RK_END(2);
 }
 
@@ -523,8 +580,9 @@ void launch_resid_rms(float* x, const float* P, int S, long long pstride, int T,
                       cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
-    if (op == kF32) launch_k(k_resid_rms<float>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, d, xa);
-    else launch_k(k_resid_rms<__nv_bfloat16>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, d, xa);
+    const RowShape rs = row_shape(row_threads(d));
+    if (op == kF32) launch_kc(k_resid_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, d, xa);
+    else launch_kc(k_resid_rms<__nv_bfloat16>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, d, xa);
 }
 
 void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s) {
@@ -536,19 +594,21 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_gate(const GateArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
-    const int threads = row_rt(gate_threads(a.d, a.E));  // one row per block, a (virtual) warp per expert
-    if (a.op == kF32) launch_k(k_gate<float>, a.T, threads, smem, s, a);
-    else launch_k(k_gate<__nv_bfloat16>, a.T, threads, smem, s, a);
+    const RowShape rs = row_shape(gate_threads(a.d, a.E));  // a row per cluster, a (virtual) warp per expert
+    if (a.op == kF32) launch_kc(k_gate<float>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
+    else launch_kc(k_gate<__nv_bfloat16>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
 }
 
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
                         int K, int d, int dense, void* xa, WType op, cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
+    const RowShape rs = row_shape(row_threads(d));
     if (op == kF32)
-        launch_k(k_combine_rms<float>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa);
     else
-        launch_k(k_combine_rms<__nv_bfloat16>, T, row_rt(row_threads(d)), sm, s, x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_kc(k_combine_rms<__nv_bfloat16>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense,
+                  xa);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
