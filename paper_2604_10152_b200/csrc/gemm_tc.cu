@@ -554,9 +554,9 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
         const char* v = getenv("SMOE_TC_PAIR");
         return !(v && v[0] == '0');
     }();
-    static const bool pair_single_env = [] {
+    static const int pair_single_env = [] {  // 0 off, 1 auto (default), 2 whenever rows allow
         const char* v = getenv("SMOE_TC_PAIR_SINGLE");
-        return !(v && v[0] == '0');
+        return v ? atoi(v) : 1;
     }();
     static const bool pair_down_env = [] {
         const char* v = getenv("SMOE_TC_PAIR_DOWN");
@@ -569,7 +569,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     const long long paired_units = (long long)((a.rows_bound + BN_MAX - 1) / BN_MAX) *
                                    ((p.ph[0].m_tiles + 1) / 2) * p.ph[0].splits;
     p.pair_single = !a.group_cnt && pair_env && pair_single_env && a.single_rows <= BN_MAX / 2 &&
-                    paired_units >= sm_count();
+                    (paired_units >= sm_count() || pair_single_env == 2);
     p.b_region = tok_box_bytes(tok_box_index(std::min(a.rows_bound, BN_MAX)));
     const int stage_bytes = (p.pair_single ? 2 : 1) * kABytes + p.b_region;
     p.stage_space = kSmemBudget - kCtrl - 1024;

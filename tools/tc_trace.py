@@ -83,6 +83,11 @@ def analyze(path):
         unit_us = (U[:, 4] - U[:, 3]) / 1e3
         up = ids < u0
         kind = "mix/head" if nphase == 1 else ("moe_T>256" if total > 2 * u0 * 1.2 else "moe")
+        # unit anatomy (us): claim -> producer issued its last stage -> last MMA done -> epilogue done
+        anat = dict(claim_to_issued=float(np.median((U[:, 2] - U[:, 1]) / 1e3)),
+                    mma_first_to_issued=float(np.median((U[:, 2] - U[:, 3]) / 1e3)),
+                    issued_to_mma_done=float(np.median((U[:, 4] - U[:, 2]) / 1e3)),
+                    epilogue=float(np.median((U[:, 5] - U[:, 4]) / 1e3)))
         r = dict(slot=int(s), launch=int(t), kind=kind, units=int(m.sum()), grid=grid,
                  dur_us=float((t1 - t0) / 1e3),
                  ramp_us=float(np.median((first_full - t0) / 1e3)),
@@ -91,7 +96,7 @@ def analyze(path):
                  down_unit_us=float(np.median(unit_us[~up])) if (~up).any() else 0.0,
                  n_up=int(up.sum()), n_down=int((~up).sum()),
                  cta_start_spread=float((cta[s, :grid, 0].max() - t0) / 1e3),
-                 t0=int(t0), t1=int(t1), first_stage=int(first_full.min()))
+                 t0=int(t0), t1=int(t1), first_stage=int(first_full.min()), **anat)
         rows.append(r)
     rows.sort(key=lambda r: r["launch"])
     # aggregate per class (moe launches split by their unit count: draft passes touch fewer experts)
@@ -103,7 +108,9 @@ def analyze(path):
         f = lambda k: round(float(np.mean([x[k] for x in rs])), 1)  # noqa: E731
         print(json.dumps(dict(kind=key[0], n_up=key[1], n_down=key[2], launches=len(rs), dur_us=f("dur_us"),
                               ramp_us=f("ramp_us"), tail_us=f("tail_us"), up_unit_us=f("up_unit_us"),
-                              down_unit_us=f("down_unit_us"), cta_start_spread=f("cta_start_spread"))))
+                              down_unit_us=f("down_unit_us"), cta_start_spread=f("cta_start_spread"),
+                              claim_to_issued=f("claim_to_issued"), mma_first_to_issued=f("mma_first_to_issued"),
+                              issued_to_mma_done=f("issued_to_mma_done"), epilogue=f("epilogue"))))
     # in-step timeline between consecutive fused MoE launches: the previous MoE launch's end -> the
     # mix launch (start, end) -> this MoE launch's first full weight stage
     gaps = []
