@@ -166,11 +166,13 @@ Engine::Engine(const smoe_engine_config& c) {
             return (nkb + per - 1) / per;
         };
         // mix: about one unit per SM at T <= 256 (measured best on the C2 shape: s_mix 4 > 8 > 2);
-        // down: 4 splits.  With pair units a 2-split down unit streams 3.7 MB, and a draft pass's last
-        // down units left a 44 us tail; C2 B=64 54.1 ms/step at 4 splits vs 57.0 at 2, 54.0-54.3 at
-        // 6/8, 56.2 at 16 (tools/ab_env.sh, same box)
+        // down: at least 2 splits, more until a pair unit (256 weight rows) streams <= 2 MB.  At C2 a
+        // 2-split down unit streams 3.7 MB and a draft pass's last down units left a 44 us tail: B=64
+        // 54.1 ms/step at 4 splits vs 57.0 at 2, 54.0-54.3 at 6/8, 56.2 at 16 (tools/ab_env.sh, same
+        // box).  C4 (f=1408): 2 splits, 16.8 vs 17.4 ms/step at 4.
+        const long long pair_unit_bytes = 256ll * f * 2;  // 256 weight rows x f bf16
         s_mix = pick(nkb_d, std::max(1, 148 / std::max(1, (d + 127) / 128)));
-        s_down = pick(nkb_f, 4);
+        s_down = pick(nkb_f, std::max(2, (int)((pair_unit_bytes + (2 << 20) - 1) / (2 << 20))));
         if (const char* v = getenv("SMOE_S_MIX")) s_mix = pick(nkb_d, atoi(v));    // tuning overrides
         if (const char* v = getenv("SMOE_S_DOWN")) s_down = pick(nkb_f, atoi(v));
     }

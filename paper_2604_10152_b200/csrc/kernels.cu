@@ -11,6 +11,7 @@
 
 #include "kernels.h"
 #include "gate_dev.cuh"
+#include "tc_common.cuh"
 
 namespace smoe {
 
@@ -290,13 +291,26 @@ __global__ void __launch_bounds__(1024) k_resid_rms(float* __restrict__ x, const
 template <typename OT>
 __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     RK_IN();
+    extern __shared__ float sm[];  // [gw[E*d] when staged], xf[d], gl[E], p[E], red[8*32 + 33]
+    __shared__ uint64_t gw_bar;
+    float* gw = sm;
+    float* xf = sm + (a.stage_gw ? (size_t)a.E * a.d : 0);
+    float* gl = xf + a.d;
+    float* red = gl + 2 * a.E + 8 * 32;
+    if (a.stage_gw && threadIdx.x == 0) {
+        // the layer's gate weights do not depend on earlier kernels: copy them into shared memory while
+        // this block waits for the Mix GEMM (the GEMV then reads shared memory, not four L2 round trips)
+        tc::mbar_init(&gw_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t total = (uint32_t)a.E * a.d * 4;
+        tc::mbar_expect_tx(&gw_bar, total);
+        for (uint32_t off = 0; off < total; off += 32768)
+            tc::bulk_g2s(reinterpret_cast<char*>(gw) + off, reinterpret_cast<const char*>(a.gate_w) + off,
+                         min(32768u, total - off), &gw_bar);
+    }
     pdl_wait();
     pdl_trigger();
     RK_WAITED();
-    extern __shared__ float sm[];  // xf[d], gl[E], p[E], red[8*32 + 33]
-    float* xf = sm;
-    float* gl = xf + a.d;
-    float* red = gl + 2 * a.E + 8 * 32;
     const RowCtx rc(gate_threads(a.d, a.E));
     const int r = rc.row(), d = a.d, E = a.E, K = a.K, d4 = d >> 2;
     const long long base = (long long)r * d;
@@ -328,10 +342,12 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     // d in float4s (fixed order, then a butterfly), so every row's logits are computed identically in
     // any pass.  The logits are gathered in CTA 0 of the cluster.
     const int lane = threadIdx.x & 31, nvw = rc.VB >> 5;
+    if (a.stage_gw) tc::mbar_wait(&gw_bar, 0);
+    const float* gsrc = a.stage_gw ? gw : a.gate_w;
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j) {
         for (int e = rc.vt(j) >> 5; e < E; e += nvw) {
-            const float4* g = reinterpret_cast<const float4*>(a.gate_w + (long long)e * d);
+            const float4* g = reinterpret_cast<const float4*>(gsrc + (long long)e * d);
             float acc = 0.f;
 #pragma unroll 8
             for (int i = lane; i < d4; i += 32) {
@@ -591,9 +607,23 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
     else k_rms<__nv_bfloat16><<<T, 256, 0, s>>>(x, d, xa);
 }
 
-void launch_gate(const GateArgs& a, cudaStream_t s) {
-    if (a.T <= 0) return;
-    size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33);
+void launch_gate(const GateArgs& a0, cudaStream_t s) {
+    if (a0.T <= 0) return;
+    GateArgs a = a0;
+    static const bool stage_env = [] {
+        const char* v = std::getenv("SMOE_GATE_STAGE");
+        return !(v && v[0] == '0');
+    }();
+    // stage the gate weights (E x d f32) in shared memory when they fit beside one row (C2: 128 KB)
+    const size_t gw_bytes = sizeof(float) * (size_t)a.E * a.d;
+    a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0;
+    size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0);
+    static bool configured = false;
+    if (!configured) {
+        SMOE_CUDA(cudaFuncSetAttribute(k_gate<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SMOE_CUDA(cudaFuncSetAttribute(k_gate<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
     const RowShape rs = row_shape(gate_threads(a.d, a.E));  // a row per cluster, a (virtual) warp per expert
     if (a.op == kF32) launch_kc(k_gate<float>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
     else launch_kc(k_gate<__nv_bfloat16>, a.T * rs.C, rs.RT, smem, s, rs.C, a);

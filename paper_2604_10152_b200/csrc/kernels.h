@@ -63,6 +63,7 @@ struct GateArgs {
     // (device table peer_x) at rows (ep_me * ep_eo + e % ep_eo) * seg + slot; nullptr = local xperm
     void* const* peer_x = nullptr;
     int ep_eo = 0, ep_me = 0;
+    int stage_gw = 0;  // set by launch_gate: gate weights staged into shared memory before the dependency wait
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 
