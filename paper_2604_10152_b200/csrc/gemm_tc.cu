@@ -564,12 +564,15 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     }();
     // grouped launches: bit 0 pairs the first phase, bit 1 the second (applied when the counts allow)
     p.pair_ok = a.group_cnt && pair_env ? (1 | (b && pair_down_env ? 2 : 0)) : 0;
-    // single-group launches pair only while the pair units still cover every SM (the C2 Mix launch at
-    // T=64 would otherwise run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us)
-    const long long paired_units = (long long)((a.rows_bound + BN_MAX - 1) / BN_MAX) *
-                                   ((p.ph[0].m_tiles + 1) / 2) * p.ph[0].splits;
+    // single-group launches pair only when that does not load the busiest SM with more weight bytes
+    // (the C2 Mix launch at T=64 would run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us; the head
+    // at T=64, 250 units = 2 waves of 1 MB, becomes 1 wave of 2 MB paired units)
+    const long long nt = (a.rows_bound + BN_MAX - 1) / BN_MAX, sms = sm_count();
+    const long long units1 = nt * p.ph[0].m_tiles * p.ph[0].splits;
+    const long long units2 = nt * ((p.ph[0].m_tiles + 1) / 2) * p.ph[0].splits;
+    const bool pair_pays = 2 * ((units2 + sms - 1) / sms) <= (units1 + sms - 1) / sms;
     p.pair_single = !a.group_cnt && pair_env && pair_single_env && a.single_rows <= BN_MAX / 2 &&
-                    (paired_units >= sm_count() || pair_single_env == 2);
+                    (pair_pays || pair_single_env == 2);
     p.b_region = tok_box_bytes(tok_box_index(std::min(a.rows_bound, BN_MAX)));
     const int stage_bytes = (p.pair_single ? 2 : 1) * kABytes + p.b_region;
     p.stage_space = kSmemBudget - kCtrl - 1024;
