@@ -534,3 +534,31 @@ def test_pass_kernel_agreement_with_oracle_margin_aware(port):
     assert worst <= 0.03
     assert route_bad == 0 and tok_bad == 0
     e.close()
+
+
+@pytest.mark.parametrize("env", ["SMOE_ROW_CLUSTER=1", "SMOE_ROW_THREADS=256", "SMOE_GATE_STAGE=0",
+                                 "SMOE_TC_PAIR=0", "SMOE_TC_PAIR_DOWN=0", "SMOE_TC_PAIR_SINGLE=2",
+                                 "SMOE_L2_PREFETCH=0", "SMOE_PDL=0"])
+def test_launch_shape_switches_bitexact(env):
+    """Launch-shape switches change how the work is laid out on the GPU (row clusters with DSMEM
+    reductions, fewer row threads playing the same reduction tree, gate weights staged in shared
+    memory, pair units, L2 prefetch, PDL) but never the arithmetic: logits, routing and token streams
+    are bit-identical to the default launch shapes."""
+    import subprocess
+    import sys
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "launch_digest.py")
+
+    def run(extra):
+        env_ = dict(os.environ)
+        env_.update(extra)
+        out = subprocess.run([sys.executable, script], env=env_, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads(out.stdout.strip().splitlines()[-1])
+
+    k, v = env.split("=")
+    if "base" not in _DIGEST_BASE:
+        _DIGEST_BASE["base"] = run({})
+    assert run({k: v}) == _DIGEST_BASE["base"]
+
+
+_DIGEST_BASE = {}
