@@ -437,10 +437,23 @@ __global__ void k_argmax(const float* __restrict__ lg, int V, int* __restrict__ 
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     bool fin = true;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
-        float v = row[i];
+    // (value, -index) is a total order, so the scan order does not matter: first max wins
+    auto upd = [&](float v, int i) {
         fin &= isfinite(v);
         if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    };
+    if ((V & 3) == 0) {  // 16-byte rows: float4 loads, four in flight per thread (was one dependent load per step)
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
+            const float4 q = r4[i];
+            upd(q.x, 4 * i);
+            upd(q.y, 4 * i + 1);
+            upd(q.z, 4 * i + 2);
+            upd(q.w, 4 * i + 3);
+        }
+    } else {
+        for (int i = threadIdx.x; i < V; i += blockDim.x) upd(row[i], i);
     }
     if (!fin) atomicOr(flags, kFlagNonFiniteLogits);
 #pragma unroll
@@ -491,7 +504,8 @@ __global__ void k_commit(double* ssum, int* slen, const double* emb, const int* 
     const int j = blockIdx.x;
     const int b = seqs[j];
     const int n = take[j];
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {  // columns independent; per column in token order
         double s = ssum[(long long)b * d + i];
         for (int t = 0; t < n; ++t) s += emb[(long long)toks[(long long)j * tstride + t] * d + i];
         ssum[(long long)b * d + i] = s;
@@ -661,7 +675,7 @@ void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, i
 void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
                    int tok_stride, const int* take, int na, int d, cudaStream_t s) {
     if (na <= 0) return;
-    launch_k(k_commit, na, 256, 0, s, seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
+    launch_k(k_commit, na, 1024, 0, s, seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
 }
 
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
