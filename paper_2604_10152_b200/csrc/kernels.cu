@@ -315,6 +315,16 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     const int r = rc.row(), d = a.d, E = a.E, K = a.K, d4 = d >> 2;
     const long long base = (long long)r * d;
     float4* xf4 = reinterpret_cast<float4*>(xf);
+    // restricted passes: the draft tables the remap reads per pick (two dependent global loads per pick
+    // otherwise) go to shared memory now, next to the row loads below
+    int* s_rank = reinterpret_cast<int*>(red + 33);
+    int* s_sorted = s_rank + E * a.N;
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_sorted + a.N);
+    if (a.in_draft) {
+        for (int i = threadIdx.x; i < E * a.N; i += blockDim.x) s_rank[i] = a.rank[i];
+        for (int i = threadIdx.x; i < a.N; i += blockDim.x) s_sorted[i] = a.draft_sorted[i];
+        for (int i = threadIdx.x; i < E; i += blockDim.x) s_in[i] = a.in_draft[i];
+    }
     // residual add of the mix GEMM's split-K partials (model.cpp:224), then rms (model.cpp:226)
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j) {
@@ -361,7 +371,15 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     if (rc.c != 0) return;  // CTA 0 selects and dispatches the row
     // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
-    if (threadIdx.x < 32) gate_select_warp(a, r, gl, dst);
+    if (threadIdx.x < 32) {
+        GateArgs sa = a;
+        if (a.in_draft) {
+            sa.rank = s_rank;
+            sa.draft_sorted = s_sorted;
+            sa.in_draft = s_in;
+        }
+        gate_select_warp(sa, r, gl, dst);
+    }
     __syncthreads();
     const int sg = a.seg > 0 ? a.seg : a.T;
     for (int k = 0; k < K; ++k) {
@@ -631,7 +649,8 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
     // stage the gate weights (E x d f32) in shared memory when they fit beside one row (C2: 128 KB)
     const size_t gw_bytes = sizeof(float) * (size_t)a.E * a.d;
     a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0;
-    size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0);
+    size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0) +
+                  (a.in_draft ? sizeof(int) * ((size_t)a.E * a.N + a.N) + a.E : 0);
     static bool configured = false;
     if (!configured) {
         SMOE_CUDA(cudaFuncSetAttribute(k_gate<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
