@@ -53,6 +53,10 @@ struct TcGemmArgs {
     // bytes to prefetch into L2 once the launch runs out of units (its tail): the next layer's Mix weights
     const void* l2_next = nullptr;
     long long l2_next_bytes = 0;
+    // grouped launches: wait for *dep_ctr to reach dep_target (the gate blocks' completion count)
+    // instead of the previous grid's completion (nullptr: griddepcontrol.wait)
+    const unsigned* dep_ctr = nullptr;
+    unsigned dep_target = 0;
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
 // One launch for a MoE layer's grouped up- (tanh / SwiGLU) and down-projection (f32 split partials):
@@ -218,6 +222,10 @@ public:
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
     int l2_prefetch = 1;         // MoE launch tail prefetches the next Mix weights into L2 (env SMOE_L2_PREFETCH=0: off)
+    int gate_flag = 0;           // MoE launch waits on the gate blocks' counter, not the gate grid (env SMOE_GATE_FLAG)
+    unsigned* gate_ctr = nullptr;  // device: gate blocks finished (monotonic)
+    unsigned gate_epoch = 0;       // host: gate blocks launched so far
+    const unsigned* moe_dep = nullptr;  // the next fused MoE launch's hand-off counter (gate_flag)
     // one persistent launch per pass (pass_tc.cu), opt-in with env SMOE_PASS_KERNEL=1: bit-identical to
     // the per-layer launches but 2-4% slower end to end at B = 1..64 (profiles/r02_pass_kernel.md)
     int pass_kernel = 0;

@@ -78,6 +78,8 @@ struct TcParams {
     int* sched;            // [3]: next-unit counter, finished-CTA counter, L2 prefetch chunk counter (self-resetting)
     const uint8_t* pf;     // prefetched into L2 by the producers that run out of units (the launch's tail)
     long long pf_bytes;
+    const unsigned* dep_ctr;  // grouped launches: wait for *dep_ctr >= dep_target instead of the previous grid
+    unsigned dep_target;
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
 };
@@ -197,6 +199,26 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
     return true;
 }
 
+// The dependency wait of a launch: the previous grid's completion (PDL), or, when the launch carries a
+// hand-off counter, that counter reaching its target (the gate blocks count themselves after their
+// dispatch stores), which a resident CTA sees ~2 us before the grid-completion signal.
+__device__ __forceinline__ void dep_wait(const TcParams& p) {
+    if (!p.dep_ctr) {
+        pdl_wait();
+        return;
+    }
+    const long long t0 = clock64();
+    while ((int)((unsigned)ld_relaxed(reinterpret_cast<const int*>(p.dep_ctr)) - p.dep_target) < 0) {
+        __nanosleep(64);
+        if (clock64() - t0 > 4000000000ll) {
+            printf("smoe dep_wait timeout: block %d\n", (int)blockIdx.x);
+            __trap();
+        }
+    }
+    fence_acquire();
+    proxy_fence_async();  // the gate's generic stores (xperm rows) before this launch's TMA reads
+}
+
 template <int EPI0, int EPI1>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ WeightMaps mapA0, const __grid_constant__ TokenMaps mapB0,
@@ -267,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.group_cnt) {
                 // grouped launches: the unit geometry (rows per expert) is written by the gate kernel
                 // that immediately precedes this one, so it may only be read after the dependency wait
-                pdl_wait();
+                dep_wait(p);
                 kernel_dep = true;
                 grouped_layout(p, stages, stage_bytes, pair);
                 total_units = units_of_phase(p, 0, pair) + (p.nphase > 1 ? units_of_phase(p, 1, pair) : 0);
@@ -345,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!kernel_dep) pdl_wait();
         }
     } else if (warp == 1) {
-        pdl_wait();
+        dep_wait(p);
         if (p.group_cnt) grouped_layout(p, stages, stage_bytes, pair);
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
@@ -389,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
-        pdl_wait();
+        dep_wait(p);
         const int q = warp & 3;
         int cnt = 0, cons = 0;
         Unit w;
@@ -581,6 +603,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.done = a.done;
     p.pf = static_cast<const uint8_t*>(a.l2_next);
     p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
+    p.dep_ctr = a.group_cnt ? a.dep_ctr : nullptr;
+    p.dep_target = a.dep_target;
     p.tr = g_launch_no++;
     const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;
     const WeightMaps ma0{{tensor_map(a.A, BM), tensor_map(a.A, 2 * BM)}};

@@ -393,6 +393,11 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
         store_row4<OT>(base, row * d, xf4, d4, 1.0f);
     }
     if (a.peer_x) __threadfence_system();
+    if (a.done_ctr) {  // hand-off to the MoE launch: every thread's stores, then one count per row
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(a.done_ctr, 1u);
+    }
     RK_END(1);
 }
 

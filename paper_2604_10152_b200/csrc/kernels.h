@@ -64,6 +64,7 @@ struct GateArgs {
     void* const* peer_x = nullptr;
     int ep_eo = 0, ep_me = 0;
     int stage_gw = 0;  // set by launch_gate: gate weights staged into shared memory before the dependency wait
+    unsigned* done_ctr = nullptr;  // incremented once per row after its dispatch stores (MoE launch hand-off)
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 
