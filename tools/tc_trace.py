@@ -84,6 +84,15 @@ def analyze(path):
         up = ids < u0
         kind = "mix/head" if nphase == 1 else ("moe_T>256" if total > 2 * u0 * 1.2 else "moe")
         # unit anatomy (us): claim -> producer issued its last stage -> last MMA done -> epilogue done
+        epi_us = (U[:, 5] - U[:, 4]) / 1e3
+        last = np.zeros(len(U), bool)
+        for c in np.unique(cta_id):
+            k = np.nonzero(cta_id == c)[0]
+            last[k[np.argmax(U[k, 5])]] = True
+        anat_x = dict(epi_up=float(np.median(epi_us[up])) if up.any() else 0.0,
+                      epi_down=float(np.median(epi_us[~up])) if (~up).any() else 0.0,
+                      epi_last=float(np.median(epi_us[last])),
+                      mma_first_to_done_last=float(np.median((U[last, 4] - U[last, 3]) / 1e3)))
         anat = dict(claim_to_issued=float(np.median((U[:, 2] - U[:, 1]) / 1e3)),
                     mma_first_to_issued=float(np.median((U[:, 2] - U[:, 3]) / 1e3)),
                     issued_to_mma_done=float(np.median((U[:, 4] - U[:, 2]) / 1e3)),
@@ -96,7 +105,7 @@ def analyze(path):
                  down_unit_us=float(np.median(unit_us[~up])) if (~up).any() else 0.0,
                  n_up=int(up.sum()), n_down=int((~up).sum()),
                  cta_start_spread=float((cta[s, :grid, 0].max() - t0) / 1e3),
-                 t0=int(t0), t1=int(t1), first_stage=int(first_full.min()), **anat)
+                 t0=int(t0), t1=int(t1), first_stage=int(first_full.min()), **anat, **anat_x)
         rows.append(r)
     rows.sort(key=lambda r: r["launch"])
     # aggregate per class (moe launches split by their unit count: draft passes touch fewer experts)
@@ -110,7 +119,8 @@ def analyze(path):
                               ramp_us=f("ramp_us"), tail_us=f("tail_us"), up_unit_us=f("up_unit_us"),
                               down_unit_us=f("down_unit_us"), cta_start_spread=f("cta_start_spread"),
                               claim_to_issued=f("claim_to_issued"), mma_first_to_issued=f("mma_first_to_issued"),
-                              issued_to_mma_done=f("issued_to_mma_done"), epilogue=f("epilogue"))))
+                              issued_to_mma_done=f("issued_to_mma_done"), epilogue=f("epilogue"),
+                              epi_up=f("epi_up"), epi_down=f("epi_down"), epi_last=f("epi_last"))))
     # in-step timeline between consecutive fused MoE launches: the previous MoE launch's end -> the
     # mix launch (start, end) -> this MoE launch's first full weight stage
     gaps = []
