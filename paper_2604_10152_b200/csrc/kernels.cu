@@ -50,7 +50,7 @@ __device__ float block_sum(float v, float* red) {
 #ifdef SMOE_TC_TRACE
 struct RkRec {
     int kid, blk;
-    long long t_in, t_wait, t_end;
+    long long t_in, t_wait, t_end, t_m[3];  // t_m: kernel-specific marks (gate: rms done, GEMV done, selected)
 };
 constexpr int kRkRing = 1 << 18;
 __device__ RkRec g_rk[kRkRing];
@@ -60,18 +60,22 @@ __device__ __forceinline__ long long rk_now() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define RK_IN() const long long rk_t0 = rk_now()
+#define RK_IN() \
+    const long long rk_t0 = rk_now(); \
+    long long rk_m[3] = {0, 0, 0}
 #define RK_WAITED() const long long rk_t1 = rk_now()
-#define RK_END(kid)                                                                  \
-    do {                                                                             \
-        if (threadIdx.x == 0) {                                                      \
-            const unsigned i = atomicAdd(&g_rk_n, 1u) % kRkRing;                     \
-            g_rk[i] = RkRec{kid, (int)blockIdx.x, rk_t0, rk_t1, rk_now()};           \
-        }                                                                            \
+#define RK_MARK(n) rk_m[n] = rk_now()
+#define RK_END(kid)                                                                                      \
+    do {                                                                                                 \
+        if (threadIdx.x == 0) {                                                                          \
+            const unsigned i = atomicAdd(&g_rk_n, 1u) % kRkRing;                                         \
+            g_rk[i] = RkRec{kid, (int)blockIdx.x, rk_t0, rk_t1, rk_now(), {rk_m[0], rk_m[1], rk_m[2]}};  \
+        }                                                                                                \
     } while (0)
 #else
 #define RK_IN()
 #define RK_WAITED()
+#define RK_MARK(n)
 #define RK_END(kid)
 #endif
 
@@ -340,6 +344,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     }
     rc.sync();
     const float inv = 1.0f / sqrtf(vblock_total(rc.VB >> 5, red) / (float)d + 1e-12f);
+    RK_MARK(0);
     // the normalised row, whole, in every CTA of the cluster
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j)
@@ -368,6 +373,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
         }
     }
     rc.sync();
+    RK_MARK(1);
     if (rc.c != 0) return;  // CTA 0 selects and dispatches the row
     // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
@@ -381,6 +387,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
         gate_select_warp(sa, r, gl, dst);
     }
     __syncthreads();
+    RK_MARK(2);
     const int sg = a.seg > 0 ? a.seg : a.T;
     for (int k = 0; k < K; ++k) {
         void* base = a.xperm;

@@ -45,8 +45,19 @@ def row_kernel_launches(path):
         return {}
     raw = open(path, "rb").read()
     n = int(np.frombuffer(raw[:4], np.int32)[0])
-    rec = np.frombuffer(raw[4:4 + n * 32], dtype=np.dtype(
-        [("kid", np.int32), ("blk", np.int32), ("t_in", np.int64), ("t_wait", np.int64), ("t_end", np.int64)]))
+    rec = np.frombuffer(raw[4:4 + n * 56], dtype=np.dtype(
+        [("kid", np.int32), ("blk", np.int32), ("t_in", np.int64), ("t_wait", np.int64), ("t_end", np.int64),
+         ("t_m", np.int64, (3,))]))
+    g = rec[rec["kid"] == 1]
+    if len(g):  # gate anatomy per block (us after its wait released): rms done, GEMV done, selected, end
+        w = g["t_wait"]
+        print(json.dumps({"gate_block_anatomy_us": {
+            "rms_done": round(float(np.median((g["t_m"][:, 0] - w) / 1e3)), 2),
+            "gemv_done": round(float(np.median((g["t_m"][:, 1] - w) / 1e3)), 2),
+            "selected": round(float(np.median((g["t_m"][:, 2] - w) / 1e3)), 2),
+            "end": round(float(np.median((g["t_end"] - w) / 1e3)), 2),
+            "end_p90": round(float(np.percentile((g["t_end"] - w) / 1e3, 90)), 2),
+            "wait_spread_p90": round(float(np.percentile((w - np.min(w)) / 1e3, 90)), 2)}}))
     out = {}
     for kid in np.unique(rec["kid"]):
         r = np.sort(rec[rec["kid"] == kid], order="t_in")
