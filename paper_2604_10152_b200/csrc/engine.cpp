@@ -218,9 +218,12 @@ Engine::Engine(const smoe_engine_config& c) {
     SMOE_CUDA(cudaMemset(moe_done, 0, 128 * sizeof(int)));
     gate_ctr = dalloc<unsigned>(1);
     SMOE_CUDA(cudaMemset(gate_ctr, 0, sizeof(unsigned)));
+    comb_ctr = dalloc<unsigned>(1);
+    SMOE_CUDA(cudaMemset(comb_ctr, 0, sizeof(unsigned)));
     if (const char* v = getenv("SMOE_FUSED_MOE")) fuse_moe = atoi(v) != 0;
     if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
     if (const char* v = getenv("SMOE_GATE_FLAG")) gate_flag = atoi(v) != 0;
+    if (const char* v = getenv("SMOE_COMBINE_FLAG")) combine_flag = atoi(v) != 0;
     if (const char* v = getenv("SMOE_PASS_KERNEL")) pass_kernel = atoi(v) != 0;
     if (const char* v = getenv("SMOE_PASS_MAX_ROWS")) pass_kernel_max_rows = atoi(v);
     if (const char* v = getenv("SMOE_PASS_MIN_ROWS")) pass_kernel_min_rows = atoi(v);
@@ -248,7 +251,7 @@ Engine::~Engine() {
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
     fr(ep_flags); fr(ep_peer);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
-    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(scratch64); fr(pass_ctr);
+    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(comb_ctr); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
     fr(stage_up); fr(stage_down);
@@ -650,6 +653,11 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
         if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
         TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, gcnt, gslot, G, seg, single_rows, single_slot, rows_bound,
                      Y, ldy, epi, splits, split_stride, sched + 4 * (gemm_launches++ & 1)};
+        if (gemm_dep) {
+            a.dep_ctr = gemm_dep;
+            a.dep_target = comb_epoch;
+            gemm_dep = nullptr;
+        }
         launch_gemm_tc(a, stream);
     } else {
         if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");
@@ -777,7 +785,11 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             {
                 // K9 combine + residual + the next layer's (or the head's) rms
                 ProfScope ps(*this, "combine");
-                launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
+                const bool cflag = combine_flag && !profiling && use_tc;
+                if (cflag) comb_epoch += (unsigned)T * (unsigned)combine_blocks_per_row(d);
+                launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream,
+                                   cflag ? comb_ctr : nullptr);
+                gemm_dep = cflag ? comb_ctr : nullptr;  // the next Mix (or head) launch
             }
         } else {
             launch_resid_rms(x, pmix, s_mix, pm_stride, T, d, xa, wt, stream);

@@ -226,6 +226,10 @@ public:
     unsigned* gate_ctr = nullptr;  // device: gate blocks finished (monotonic)
     unsigned gate_epoch = 0;       // host: gate blocks launched so far
     const unsigned* moe_dep = nullptr;  // the next fused MoE launch's hand-off counter (gate_flag)
+    int combine_flag = 0;        // the next Mix/head launch waits on the combine blocks' counter (env SMOE_COMBINE_FLAG)
+    unsigned* comb_ctr = nullptr;  // device: combine blocks finished (monotonic)
+    unsigned comb_epoch = 0;
+    const unsigned* gemm_dep = nullptr;  // hand-off counter of the next gemm() launch
     // one persistent launch per pass (pass_tc.cu), opt-in with env SMOE_PASS_KERNEL=1: bit-identical to
     // the per-layer launches but 2-4% slower end to end at B = 1..64 (profiles/r02_pass_kernel.md)
     int pass_kernel = 0;

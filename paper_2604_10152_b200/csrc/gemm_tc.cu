@@ -78,7 +78,7 @@ struct TcParams {
     int* sched;            // [3]: next-unit counter, finished-CTA counter, L2 prefetch chunk counter (self-resetting)
     const uint8_t* pf;     // prefetched into L2 by the producers that run out of units (the launch's tail)
     long long pf_bytes;
-    const unsigned* dep_ctr;  // grouped launches: wait for *dep_ctr >= dep_target instead of the previous grid
+    const unsigned* dep_ctr;  // wait for *dep_ctr >= dep_target instead of the previous grid's completion
     unsigned dep_target;
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
@@ -200,8 +200,8 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
 }
 
 // The dependency wait of a launch: the previous grid's completion (PDL), or, when the launch carries a
-// hand-off counter, that counter reaching its target (the gate blocks count themselves after their
-// dispatch stores), which a resident CTA sees ~2 us before the grid-completion signal.
+// hand-off counter, that counter reaching its target (the gate / combine blocks count themselves after
+// their stores), which a resident CTA sees ~2 us before the grid-completion signal.
 __device__ __forceinline__ void dep_wait(const TcParams& p) {
     if (!p.dep_ctr) {
         pdl_wait();
@@ -216,7 +216,7 @@ __device__ __forceinline__ void dep_wait(const TcParams& p) {
         }
     }
     fence_acquire();
-    proxy_fence_async();  // the gate's generic stores (xperm rows) before this launch's TMA reads
+    proxy_fence_async();  // the producer kernel's generic stores before this launch's TMA reads
 }
 
 template <int EPI0, int EPI1>
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (it + 1 - pend_it < stages && kb + 1 < w.kb1) continue;  // keep streaming weights
                     if (!kernel_dep) {
-                        pdl_wait();
+                        dep_wait(p);
                         kernel_dep = true;
                     }
                     if (w.phase) {
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 TR(if (u < kTrUnits) g_tr_unit[trs][u].tma_done = gtimer();)
             }
-            if (!kernel_dep) pdl_wait();
+            if (!kernel_dep) dep_wait(p);
         }
     } else if (warp == 1) {
         dep_wait(p);
@@ -603,7 +603,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.done = a.done;
     p.pf = static_cast<const uint8_t*>(a.l2_next);
     p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
-    p.dep_ctr = a.group_cnt ? a.dep_ctr : nullptr;
+    p.dep_ctr = a.dep_ctr;
     p.dep_target = a.dep_target;
     p.tr = g_launch_no++;
     const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;

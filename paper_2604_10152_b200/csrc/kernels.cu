@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
 template <typename OT>
 __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
                               const int* __restrict__ pos, const float* __restrict__ wgt, int K, int d, int dense,
-                              void* __restrict__ xa) {
+                              void* __restrict__ xa, unsigned* done_ctr) {
     RK_IN();
     pdl_wait();
     pdl_trigger();
@@ -454,6 +454,11 @@ __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, con
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j)
         for (int i = rc.vt(j); i < d4; i += rc.VB) store4_op<OT>(xa, base + 4ll * i, row4[i], inv);
+    if (done_ctr) {  // hand-off to the next GEMM launch: every thread's stores, then one count per block
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(done_ctr, 1u);
+    }
     RK_END(2);
 }
 
@@ -674,16 +679,19 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
     else launch_kc(k_gate<__nv_bfloat16>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
 }
 
+int combine_blocks_per_row(int d) { return row_shape(row_threads(d)).C; }
+
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
-                        int K, int d, int dense, void* xa, WType op, cudaStream_t s) {
+                        int K, int d, int dense, void* xa, WType op, cudaStream_t s, unsigned* done_ctr) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
     const RowShape rs = row_shape(row_threads(d));
     if (op == kF32)
-        launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa);
+        launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa,
+                  done_ctr);
     else
         launch_kc(k_combine_rms<__nv_bfloat16>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense,
-                  xa);
+                  xa, done_ctr);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {
