@@ -42,3 +42,7 @@ oracle-ref:
 clean:
 	rm -rf build $(OUT)/libspecmoe_b200.so $(BIN)
 .PHONY: all clean oracle-port oracle-ref
+
+# HBM/PCIe streaming probe used by profiles/r01_bw_probe.md (not part of the product)
+tools/bw_probe: tools/bw_probe.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<

@@ -153,9 +153,18 @@ int smoe_get_affinity(smoe_engine* h, double* out) {
     });
 }
 
+// A stepped run (smoe_spec_begin .. smoe_spec_end) owns the engine's per-sequence state and draft
+// tables; any other entry point that resets them would silently corrupt the stepped run.
+static void no_stepped_run(smoe_engine* h) {
+    if (h->e->st) throw smoe::Error(SMOE_INVARIANT, "stepped run in progress; call smoe_spec_end first");
+}
+
 int smoe_forward(smoe_engine* h, const int* prefix, int n, const int* restricted, int n_draft, int use_affinity,
                  float* logits_out, int* raw_out, int* final_out) {
     return guarded([&] {
+        no_stepped_run(h);
+        if (restricted && (n_draft < 0 || n_draft > h->e->E))
+            throw smoe::Error(SMOE_INVARIANT, "forward: restricted set larger than experts_per_block");
         std::vector<int> p(prefix, prefix + std::max(0, n));
         for (int t : p)
             if (t < 0 || t >= h->e->V) throw smoe::Error(SMOE_INVARIANT, "forward: token out of range");
@@ -166,6 +175,7 @@ int smoe_forward(smoe_engine* h, const int* prefix, int n, const int* restricted
 int smoe_run_specmoe(smoe_engine* h, const smoe_run_config* cfg, const int* prompts, int B, int plen,
                      smoe_run_result** out) {
     return guarded([&] {
+        no_stepped_run(h);
         if (B < 1) throw smoe::Error(SMOE_CONFIG, "run_specmoe: no prompts");
         auto r = smoe::run_specmoe(*h->e, cfg_of(cfg), prompts_of(prompts, B, plen));
         *out = flatten(r, h->e->M, h->e->E, h->e->K);
@@ -175,6 +185,7 @@ int smoe_run_specmoe(smoe_engine* h, const smoe_run_config* cfg, const int* prom
 int smoe_run_ondemand(smoe_engine* h, const smoe_run_config* cfg, const int* prompts, int B, int plen,
                       smoe_run_result** out) {
     return guarded([&] {
+        no_stepped_run(h);
         auto r = smoe::run_ondemand(*h->e, cfg_of(cfg), prompts_of(prompts, B, plen));
         *out = flatten(r, h->e->M, h->e->E, h->e->K);
     });
@@ -189,6 +200,7 @@ void smoe_free_result(smoe_run_result* r) {
 
 int smoe_spec_begin(smoe_engine* h, const smoe_run_config* cfg, const int* prompts, int B, int plen) {
     return guarded([&] {
+        no_stepped_run(h);
         if (B < 1) throw smoe::Error(SMOE_CONFIG, "run_specmoe: no prompts");
         smoe::spec_begin(*h->e, cfg_of(cfg), prompts_of(prompts, B, plen));
     });

@@ -575,9 +575,15 @@ void Engine::build_affinity_device() {
 void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft) {
     if ((int)sets.size() != M) throw Error(kInvariant, "forward: restricted set count != MoE layer count");
     // per-layer sizes may differ (RestrictedExperts allows it); rows are padded with -1 to the widest
+    // Duplicates are kept: the reference's candidate lists are multisets (drafting.cpp:140-151 sizes
+    // the surrogate's modulus by them), and the device walks the sorted multiset the same way.  The
+    // per-layer tables hold E entries, so a set longer than E (necessarily with repeats) is refused.
     int nmax = 0;
     for (const auto& st : sets) {
         if ((int)st.size() < K) throw Error(kInvariant, "forward: restricted set smaller than top_k");
+        if ((int)st.size() > E) throw Error(kInvariant, "forward: restricted set larger than experts_per_block");
+        for (int x : st)
+            if (x < 0 || x >= E) throw Error(kInvariant, "forward: draft expert out of range");
         nmax = std::max(nmax, (int)st.size());
     }
     (void)n_draft;
