@@ -126,6 +126,12 @@ int smoe_spec_end(smoe_engine* e, smoe_run_result** out);
  * NCCL: rank 0 calls smoe_ep_nccl_unique_id, the id is broadcast out of band, every rank attaches.
  * Loopback: G engines on one device driven by G host threads (validation without a multi-GPU box). */
 typedef struct smoe_ep_loopback smoe_ep_loopback;
+/* Host transport: one process per rank and a blocking host all-gather supplied by the caller
+ * (torch.distributed/gloo, MPI, sockets): recv[r * bytes ..) = rank r's send[0 .. bytes), return 0 on
+ * success.  Collectives are staged through host memory; the fused exchange's peer buffers are CUDA IPC
+ * handles all-gathered the same way, so ranks may share one GPU (tests) or sit on different GPUs. */
+typedef int (*smoe_host_allgather_fn)(void* user, const void* send, void* recv, uint64_t bytes);
+int smoe_ep_attach_host(smoe_engine* e, smoe_host_allgather_fn fn, void* user);
 int smoe_ep_nccl_unique_id(void* out, int len);
 int smoe_ep_attach_nccl(smoe_engine* e, const void* id, int len);
 smoe_ep_loopback* smoe_ep_loopback_create(int world);

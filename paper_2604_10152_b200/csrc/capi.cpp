@@ -253,6 +253,13 @@ int smoe_ep_attach_nccl(smoe_engine* h, const void* id, int len) {
         e.comm = smoe::make_nccl_comm(e.ep_rank, e.ep_world, id, len, e.device);
     });
 }
+int smoe_ep_attach_host(smoe_engine* h, smoe_host_allgather_fn fn, void* user) {
+    return guarded([&] {
+        auto& e = *h->e;
+        if (e.ep_world < 2) throw smoe::Error(SMOE_CONFIG, "engine was not created with ep_world > 1");
+        e.comm = smoe::make_host_comm(e.ep_rank, e.ep_world, fn, user);
+    });
+}
 smoe_ep_loopback* smoe_ep_loopback_create(int world) {
     smoe::LoopbackGroup* g = nullptr;
     guarded([&] { g = smoe::loopback_create(world); });

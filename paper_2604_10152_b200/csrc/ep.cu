@@ -293,6 +293,73 @@ private:
 };
 }  // namespace
 
+// ---------------------------------------------------------------- host transport (caller's all-gather)
+// One process per rank, any device placement (several processes may share one GPU): the only thing the
+// caller provides is a blocking host all-gather (gloo, MPI, sockets ...).  Every collective is staged
+// through host memory, and the fused exchange's peer tables are CUDA IPC handles all-gathered the same
+// way.  Unlike the loopback group there is no host fence: the device-side flag protocol (k_ep_signal /
+// k_ep_wait) is what orders the ranks.
+namespace {
+class HostComm : public Comm {
+public:
+    HostComm(int rank, int world, HostAllgatherFn fn, void* user) : rank_(rank), world_(world), fn_(fn), user_(user) {}
+    int rank() const override { return rank_; }
+    int world() const override { return world_; }
+    void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        std::vector<char> hs(bytes), hr(bytes * world_);
+        SMOE_CUDA(cudaMemcpyAsync(hs.data(), send, bytes, cudaMemcpyDeviceToHost, s));
+        SMOE_CUDA(cudaStreamSynchronize(s));
+        host_allgather(hs.data(), hr.data(), bytes);
+        SMOE_CUDA(cudaMemcpyAsync(recv, hr.data(), bytes * world_, cudaMemcpyHostToDevice, s));
+        SMOE_CUDA(cudaStreamSynchronize(s));
+    }
+    void alltoall(const void* send, void* recv, size_t chunk, cudaStream_t s) override {
+        // every rank's whole send buffer travels to every rank; each keeps the chunks addressed to it
+        const size_t row = chunk * world_;
+        std::vector<char> hs(row), hr(row * world_);
+        SMOE_CUDA(cudaMemcpyAsync(hs.data(), send, row, cudaMemcpyDeviceToHost, s));
+        SMOE_CUDA(cudaStreamSynchronize(s));
+        host_allgather(hs.data(), hr.data(), row);
+        for (int r = 0; r < world_; ++r)
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + r * chunk, hr.data() + r * row + rank_ * chunk, chunk,
+                                      cudaMemcpyHostToDevice, s));
+        SMOE_CUDA(cudaStreamSynchronize(s));
+    }
+    void share_buffers(void* const* mine, int n, std::vector<void*>& all, std::vector<void*>& opened) override {
+        std::vector<cudaIpcMemHandle_t> h(n), every((size_t)n * world_);
+        for (int i = 0; i < n; ++i) SMOE_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
+        host_allgather(h.data(), every.data(), sizeof(cudaIpcMemHandle_t) * n);
+        all.assign((size_t)n * world_, nullptr);
+        for (int r = 0; r < world_; ++r)
+            for (int i = 0; i < n; ++i) {
+                if (r == rank_) {
+                    all[(size_t)r * n + i] = mine[i];
+                    continue;
+                }
+                void* p = nullptr;
+                SMOE_CUDA(cudaIpcOpenMemHandle(&p, every[(size_t)r * n + i], cudaIpcMemLazyEnablePeerAccess));
+                all[(size_t)r * n + i] = p;
+                opened.push_back(p);
+            }
+    }
+
+private:
+    void host_allgather(const void* send, void* recv, size_t bytes) {
+        const int rc = fn_(user_, send, recv, (uint64_t)bytes);
+        if (rc != 0) throw Error(kCuda, "host transport: all-gather callback failed (" + std::to_string(rc) + ")");
+    }
+    int rank_, world_;
+    HostAllgatherFn fn_;
+    void* user_;
+};
+}  // namespace
+
+std::unique_ptr<Comm> make_host_comm(int rank, int world, HostAllgatherFn fn, void* user) {
+    if (!fn) throw Error(kConfig, "host transport: no all-gather callback");
+    if (world < 2 || rank < 0 || rank >= world) throw Error(kConfig, "host transport: rank out of range");
+    return std::make_unique<HostComm>(rank, world, fn, user);
+}
+
 std::unique_ptr<Comm> make_loopback_comm(LoopbackGroup* g, int rank) {
     if (!g || rank < 0 || rank >= g->world) throw Error(kConfig, "loopback rank out of range");
     return std::make_unique<LoopbackComm>(g, rank);

@@ -13,6 +13,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <stdint.h>
 
 #include <memory>
 #include <vector>
@@ -42,6 +43,11 @@ public:
 // NCCL (dlopen'ed libnccl.so.2, so the engine shares whichever NCCL the process already loaded)
 int nccl_unique_id(void* out, int len);
 std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const void* id, int len, int device);
+
+// One process per rank with a caller-provided blocking host all-gather (recv[r * bytes ..) = rank r's
+// send); device placement is free, several ranks may share a GPU.  Returns non-zero on failure.
+typedef int (*HostAllgatherFn)(void* user, const void* send, void* recv, uint64_t bytes);
+std::unique_ptr<Comm> make_host_comm(int rank, int world, HostAllgatherFn fn, void* user);
 
 // G virtual ranks on one device (tests): each rank is an engine driven by its own host thread.
 struct LoopbackGroup;

@@ -29,7 +29,8 @@ EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
            "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters", "smoe_bench_expert_gemm",
            "smoe_profile_reset", "smoe_profile_read", "smoe_ep_nccl_unique_id", "smoe_ep_attach_nccl",
-           "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback", "smoe_make_prompts"]
+           "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback", "smoe_ep_attach_host",
+           "smoe_make_prompts"]
 
 
 class EngineError(RuntimeError):
@@ -126,6 +127,7 @@ def lib():
     L.smoe_ep_loopback_create.argtypes = [C.c_int]
     L.smoe_ep_loopback_destroy.argtypes = [vp]
     L.smoe_ep_attach_loopback.argtypes = [vp, vp]
+    L.smoe_ep_attach_host.argtypes = [vp, HOST_ALLGATHER, vp]
     L.smoe_profile_reset.argtypes = [vp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
     L.smoe_make_prompts.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, ip]
@@ -232,6 +234,46 @@ def nccl_unique_id() -> bytes:
     if n <= 0:
         raise EngineError(-n if n < 0 else 3, lib().smoe_last_error().decode(errors="replace"))
     return buf.raw[:n]
+
+
+# int (*)(void* user, const void* send, void* recv, uint64_t bytes) -- include/specmoe_b200.h
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class HostTransport:
+    """One process per EP rank; the engine's collectives go through `allgather(data: bytes) -> list[bytes]`
+    (rank order), e.g. a torch.distributed gloo all-gather.  The fused exchange's peer buffers are CUDA
+    IPC handles all-gathered the same way, so ranks may share one GPU."""
+
+    def __init__(self, allgather):
+        self._fn = allgather
+
+        def cb(user, send, recv, nbytes):
+            try:
+                parts = self._fn(C.string_at(send, nbytes))
+                for r, blob in enumerate(parts):
+                    if len(blob) != nbytes:
+                        return 2
+                    C.memmove(recv + r * nbytes, blob, nbytes)
+                return 0
+            except Exception:  # never unwind through the C++ engine
+                import traceback
+                traceback.print_exc()
+                return 1
+        self.cfunc = HOST_ALLGATHER(cb)  # kept alive as long as the transport
+
+
+def gloo_allgather(group=None):
+    """A HostTransport all-gather over torch.distributed (any backend with CPU tensors, e.g. gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(data: bytes):
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(out, t, group=group)
+        return [o.numpy().tobytes() for o in out]
+    return ag
 
 
 class LoopbackGroup:
@@ -374,6 +416,10 @@ class Engine:
     def attach_nccl(self, unique_id: bytes):
         buf = C.create_string_buffer(unique_id, len(unique_id))
         _check(lib().smoe_ep_attach_nccl(self.h, buf, len(unique_id)))
+
+    def attach_host(self, transport: "HostTransport"):
+        self._transport = transport  # the callback must outlive the engine's use of it
+        _check(lib().smoe_ep_attach_host(self.h, transport.cfunc, None))
 
     def attach_loopback(self, group: "LoopbackGroup"):
         _check(lib().smoe_ep_attach_loopback(self.h, group.h))

@@ -45,3 +45,33 @@ def test_gloo_world2_rank_reduction():
         assert ms == 11.0 and toks == 201        # replicas: max time, summed tokens
         assert ms2 == 10.0 and toks2 == 7        # expert parallel: max time, rank-0 tokens
         assert oid == b"id-bytes"
+
+
+def _host_worker(rank, world, port, q):
+    """The C ABI's host transport callback (what the engine calls for every EP collective) over gloo."""
+    import ctypes as C
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2604_10152_b200.engine import HostTransport, gloo_allgather
+    t = HostTransport(gloo_allgather())
+    ok = []
+    for n in (1, 40, 4099):
+        send = (C.c_ubyte * n)(*[(rank * 31 + i) % 251 for i in range(n)])
+        recv = (C.c_ubyte * (n * world))()
+        rc = t.cfunc(None, C.addressof(send), C.addressof(recv), n)
+        want = [(r * 31 + i) % 251 for r in range(world) for i in range(n)]
+        ok.append(rc == 0 and list(recv) == want)
+    q.put((rank, all(ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_host_transport_allgather_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_worker, args=(r, 2, port, q)) for r in range(2)]
+    [p.start() for p in procs]
+    [p.join(timeout=120) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    assert sorted(q.get() for _ in range(2)) == [(0, True), (1, True)]
