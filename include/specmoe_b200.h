@@ -37,7 +37,7 @@ typedef struct {
     int gemm_backend;        /* SMOE_GEMM_* ; AUTO = tcgen05 for bf16, SIMT for f32 */
     int device;
     int offload;             /* 0: all experts HBM-resident; 1: pinned host pool + HBM slots (C3) */
-    int hbm_expert_slots;    /* offload: HBM slot count (0 = pinned draft sets + one layer's transients) */
+    int hbm_expert_slots;    /* offload: HBM slot count (0 = 4 pinned draft experts per layer + two layers' transients) */
     int ep_rank, ep_world;   /* expert parallelism: this rank holds experts [r*E/G, (r+1)*E/G) of every layer
                                 (0, 0 or 0, 1 = single GPU); attach a transport before running */
 } smoe_engine_config;
@@ -76,6 +76,8 @@ typedef struct {
     double gpu_s;           /* CUDA-event time of the loop on the engine stream */
     uint64_t h2d_expert_bytes; /* real bytes migrated by the expert store (offload mode) */
     double h2d_s;           /* CUDA-event time spent in expert migration copies */
+    uint64_t prefetch_bytes;        /* overlap baseline: bytes the store prefetched for the next layer */
+    uint64_t prefetch_wasted_bytes; /* ... of which the next layer never routed to */
 } smoe_run_result;
 
 const char* smoe_last_error(void);
@@ -108,6 +110,15 @@ int smoe_run_specmoe(smoe_engine* e, const smoe_run_config* cfg, const int* prom
                      smoe_run_result** out);
 int smoe_run_ondemand(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len,
                       smoe_run_result** out);
+/* run_overlap (baselines.hpp:30-34): the on-demand token stream and ledger; on the offloaded store each
+ * layer's fetch is followed by a prefetch of the next layer's experts of the previous step, so the copy
+ * engine streams while the layer computes (misses are fetched on demand; unused prefetches counted).
+ * run_caching (baselines.hpp:36-41): top ceil(cache_fraction*E) experts per layer by a hot_global
+ * on-demand warmup profile (cfg->warmup_steps) pinned in HBM, then on-demand decoding. */
+int smoe_run_overlap(smoe_engine* e, const smoe_run_config* cfg, const int* prompts, int B, int prompt_len,
+                     smoe_run_result** out);
+int smoe_run_caching(smoe_engine* e, const smoe_run_config* cfg, double cache_fraction, const int* prompts, int B,
+                     int prompt_len, smoe_run_result** out);
 void smoe_free_result(smoe_run_result* r);
 
 /* Stepped interface for benchmarking one speculative phase at a time (a "step" = draft pass of
@@ -144,14 +155,22 @@ int smoe_ep_attach_loopback(smoe_engine* e, smoe_ep_loopback* g);
 int smoe_counters(smoe_engine* e, uint64_t* launches, double* alg_expert_bytes, double* alg_dense_bytes,
                   uint64_t* ctl_h2d, uint64_t* ctl_d2h, int reset);
 
+/* Named counters since the last smoe_counters(reset): "alg_expert_bytes:draft" / ":verify" (the split of
+ * alg_expert_bytes by pass kind) and "expert_flops:draft" / ":verify" (2 * (U*d + d*f) per routed
+ * (row, pick) on this rank's experts).  Unknown names read 0. */
+int smoe_counter(smoe_engine* e, const char* name, double* value);
+
 /* Expert GEMMs timed alone (bench.py roofline): T tokens routed round-robin over every expert of
  * MoE layer 0; average CUDA-event ms per up (w1/w3 or up) and down launch, and the algorithmic bytes
  * each launch must move (weights of touched experts + activations). */
 int smoe_bench_expert_gemm(smoe_engine* e, int T, int iters, double* up_ms, double* down_ms, double* bytes_up,
                            double* bytes_down);
 
-/* Kernel timing hooks for bench.py: events recorded around the dominant kernel class. */
-int smoe_profile_reset(smoe_engine* e);
+/* Kernel timing hooks for bench.py: events recorded around each launch of a kernel class ("expert_gemm",
+ * "dense_gemm", "head_gemm", "gate", "combine", "pass"), each also counted under "<class>:draft" or
+ * "<class>:verify" by the kind of pass that launched it. */
+int smoe_profile_reset(smoe_engine* e);  /* clears the records and starts recording */
+int smoe_profile_stop(smoe_engine* e);   /* stops recording (records stay readable) */
 int smoe_profile_read(smoe_engine* e, const char* kernel_class, double* total_ms, long long* launches,
                       double* bytes);
 

@@ -163,6 +163,10 @@ class Oracle:
         L.om_run_specmoe.argtypes = [vp, C.POINTER(OmRunCfg), ip, C.c_int, C.c_int, vp, C.c_char_p, C.c_int]
         L.om_run_ondemand.restype = C.POINTER(OmResult)
         L.om_run_ondemand.argtypes = [vp, C.POINTER(OmRunCfg), ip, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.om_run_overlap.restype = C.POINTER(OmResult)
+        L.om_run_overlap.argtypes = [vp, C.POINTER(OmRunCfg), ip, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.om_run_caching.restype = C.POINTER(OmResult)
+        L.om_run_caching.argtypes = [vp, C.POINTER(OmRunCfg), C.c_double, ip, C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.om_free_result.argtypes = [C.POINTER(OmResult)]
         L.om_route_topk.argtypes = [dp, C.c_int, C.c_int, ip]
         L.om_greedy_next.argtypes = [dp, C.c_int]
@@ -298,6 +302,23 @@ class OracleModel:
         p, pp = _iarr(P.reshape(-1))
         err = C.create_string_buffer(256)
         r = self.o.lib.om_run_ondemand(self.h, C.byref(c), pp, P.shape[0], P.shape[1], err, 256)
+        return self._collect(r, err)
+
+    def run_overlap(self, cfg: RunCfg, prompts) -> RunResult:
+        P = np.asarray(prompts, dtype=np.int32)
+        c = self._cfg(cfg)
+        p, pp = _iarr(P.reshape(-1))
+        err = C.create_string_buffer(256)
+        r = self.o.lib.om_run_overlap(self.h, C.byref(c), pp, P.shape[0], P.shape[1], err, 256)
+        return self._collect(r, err)
+
+    def run_caching(self, cfg: RunCfg, prompts, cache_fraction: float = 0.10) -> RunResult:
+        """run_caching with BaselineConfig{caching, cache_fraction, warmup_steps = cfg.warmup_steps}."""
+        P = np.asarray(prompts, dtype=np.int32)
+        c = self._cfg(cfg)
+        p, pp = _iarr(P.reshape(-1))
+        err = C.create_string_buffer(256)
+        r = self.o.lib.om_run_caching(self.h, C.byref(c), cache_fraction, pp, P.shape[0], P.shape[1], err, 256)
         return self._collect(r, err)
 
     def _collect(self, rp, err) -> RunResult:

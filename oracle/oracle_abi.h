@@ -94,6 +94,12 @@ om_result* om_run_specmoe(void* model, const om_run_cfg* cfg, const int* prompts
                           void* aff, char* err, int errlen);
 om_result* om_run_ondemand(void* model, const om_run_cfg* cfg, const int* prompts, int B, int prompt_len,
                            char* err, int errlen);
+/* run_overlap (baselines.hpp:30-34) and run_caching (baselines.hpp:36-41; BaselineConfig.warmup_steps =
+ * cfg->warmup_steps). */
+om_result* om_run_overlap(void* model, const om_run_cfg* cfg, const int* prompts, int B, int prompt_len,
+                          char* err, int errlen);
+om_result* om_run_caching(void* model, const om_run_cfg* cfg, double cache_fraction, const int* prompts, int B,
+                          int prompt_len, char* err, int errlen);
 void om_free_result(om_result* r);
 
 /* CPU-baseline timing (bench.py): `threads` host threads each run `iters` forward() calls on the

@@ -231,6 +231,42 @@ om_result* om_run_ondemand(void* model, const om_run_cfg* c, const int* prompts,
     }
 }
 
+om_result* om_run_overlap(void* model, const om_run_cfg* c, const int* prompts, int B, int plen, char* err,
+                          int errlen) {
+    try {
+        const ModelWeights& w = *static_cast<ModelWeights*>(model);
+        auto t0 = std::chrono::steady_clock::now();
+        RunResult rr = run_overlap(w, prompts_of(prompts, B, plen), spec_of(c, B, plen), tier_of(c), c->run_seed,
+                                   c->collect_trace != 0);
+        double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return flatten(rr, B, c->max_new_tokens, w.spec.moe_layer_count(), w.spec.experts_per_block, w.spec.top_k, 0,
+                       wall);
+    } catch (const std::exception& e) {
+        report(e, err, errlen);
+        return nullptr;
+    }
+}
+
+om_result* om_run_caching(void* model, const om_run_cfg* c, double cache_fraction, const int* prompts, int B,
+                          int plen, char* err, int errlen) {
+    try {
+        const ModelWeights& w = *static_cast<ModelWeights*>(model);
+        BaselineConfig bc;
+        bc.kind = BaselineKind::caching;
+        bc.cache_fraction = cache_fraction;
+        bc.warmup_steps = c->warmup_steps;
+        auto t0 = std::chrono::steady_clock::now();
+        RunResult rr = run_caching(w, prompts_of(prompts, B, plen), spec_of(c, B, plen), tier_of(c), bc, c->run_seed,
+                                   c->collect_trace != 0);
+        double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return flatten(rr, B, c->max_new_tokens, w.spec.moe_layer_count(), w.spec.experts_per_block, w.spec.top_k, 0,
+                       wall);
+    } catch (const std::exception& e) {
+        report(e, err, errlen);
+        return nullptr;
+    }
+}
+
 double om_time_forward(void* model, const int* prefix, int n, int threads, int iters) {
     try {
         const ModelWeights& w = *static_cast<ModelWeights*>(model);

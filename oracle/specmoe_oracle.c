@@ -916,8 +916,10 @@ static om_result* run_spec_(omodel* m, const om_run_cfg* cfg, const int* prompts
     return R;
 }
 
-/* baselines.cpp:29-99 (run_stepwise, greedy, no pinned set, no overlap) */
-static om_result* run_ondemand_(omodel* m, const om_run_cfg* cfg, const int* prompts, int B, int plen) {
+/* baselines.cpp:29-99 (run_stepwise, greedy).  overlap: modeled step time max(compute, migration)
+ * (baselines.cpp:101-105); pinned [M][npin] sets pinned before the loop (run_caching, 41-46). */
+static om_result* run_stepwise_(omodel* m, const om_run_cfg* cfg, const int* prompts, int B, int plen, int overlap,
+                                const int* pinned, int npin) {
     validate_decode(cfg);
     if (B < 1) fail(1, "baseline run: no prompts");
     const int M = m->M, E = m->E, K = m->K;
@@ -928,6 +930,11 @@ static om_result* run_ondemand_(omodel* m, const om_run_cfg* cfg, const int* pro
     res_init(&res, M, E, cfg);
     oledger* L = &g_lg;
     memset(L, 0, sizeof *L);
+    if (pinned) {
+        pin(&res, pinned, M, npin, L, 2, -1);
+        R->setup_bytes = L->total;
+        ledger_reset(L);
+    }
     seqv* seq = (seqv*)amalloc(sizeof(seqv) * (size_t)B);
     for (int b = 0; b < B; ++b)
         for (int i = 0; i < plen; ++i) spush(&seq[b], prompts[(size_t)b * plen + i]);
@@ -956,7 +963,7 @@ static om_result* run_ondemand_(omodel* m, const om_run_cfg* cfg, const int* pro
             for (int q = 0; q < M * K; ++q) R->hotness[(q / K) * E + raw[q]]++;
         }
         uint64_t bytes = ensure(&res, need, 2, st, L);
-        modeled += step_lat((uint64_t)B, n_need, bytes, cfg, 0);
+        modeled += step_lat((uint64_t)B, n_need, bytes, cfg, overlap);
         flush(&res);
     }
     R->wall_s = now_s() - t0;
@@ -978,6 +985,50 @@ static om_result* run_ondemand_(omodel* m, const om_run_cfg* cfg, const int* pro
     return R;
 }
 
+static om_result* run_ondemand_(omodel* m, const om_run_cfg* cfg, const int* prompts, int B, int plen) {
+    return run_stepwise_(m, cfg, prompts, B, plen, 0, NULL, 0);
+}
+
+/* baselines.cpp:113-157: greedy on-demand profiling warmup over the same prompts (its ledger reported
+ * as warmup_bytes), top ceil(cache_fraction * E) experts per block by hot_global, pinned, on-demand. */
+static om_result* run_caching_(omodel* m, const om_run_cfg* cfg, double cache_fraction, const int* prompts, int B,
+                               int plen) {
+    if (!(cache_fraction > 0.0 && cache_fraction < 1.0)) fail(1, "baseline: 0 < cache_fraction < 1 violated");
+    if (cfg->warmup_steps < 1) fail(1, "baseline: warmup_steps >= 1 violated");
+    const int M = m->M, E = m->E, K = m->K;
+    uint64_t* wc = (uint64_t*)amalloc(sizeof(uint64_t) * (size_t)M * E);
+    oledger wl = {0};
+    ores wr;
+    res_init(&wr, M, E, cfg);
+    seqv* work = (seqv*)amalloc(sizeof(seqv) * (size_t)B);
+    for (int b = 0; b < B; ++b)
+        for (int i = 0; i < plen; ++i) spush(&work[b], prompts[(size_t)b * plen + i]);
+    double* lg = (double*)amalloc(sizeof(double) * m->V);
+    int* raw = (int*)amalloc(sizeof(int) * (size_t)M * K);
+    uint8_t* need = (uint8_t*)amalloc((size_t)M * E);
+    for (int st = 0; st < cfg->warmup_steps; ++st) {
+        memset(need, 0, (size_t)M * E);
+        for (int b = 0; b < B; ++b) {
+            fwd(m, work[b].t, work[b].n, NULL, 0, NULL, lg, raw, NULL);
+            for (int i = 0; i < M * K; ++i) need[(i / K) * E + raw[i]] = 1;
+            spush(&work[b], greedy_(lg, m->V));
+            for (int i = 0; i < M * K; ++i) wc[(i / K) * E + raw[i]]++;
+        }
+        ensure(&wr, need, 2, st, &wl);
+        flush(&wr);
+    }
+    const uint64_t warm = wl.total;
+    free(wl.e);
+    const int cpl = (int)ceil(cache_fraction * (double)E);
+    if ((uint64_t)cpl * (uint64_t)M * cfg->bytes_per_expert > cfg->device_capacity_bytes)
+        fail(1, "caching: cached experts exceed device capacity");
+    int* cached = (int*)amalloc(sizeof(int) * (size_t)M * cpl);
+    select_sets(1, wc, M, E, NULL, 0, cpl, NULL, cached);
+    om_result* R = run_stepwise_(m, cfg, prompts, B, plen, 0, cached, cpl);
+    R->warmup_bytes = warm;
+    return R;
+}
+
 om_result* om_run_specmoe(void* model, const om_run_cfg* cfg, const int* prompts, int B, int plen, void* aff,
                           char* err, int errlen) {
     ENTER(err, errlen, (pending_cleanup(), (om_result*)NULL));
@@ -989,6 +1040,21 @@ om_result* om_run_ondemand(void* model, const om_run_cfg* cfg, const int* prompt
                            int errlen) {
     ENTER(err, errlen, (pending_cleanup(), (om_result*)NULL));
     om_result* r = run_ondemand_((omodel*)model, cfg, prompts, B, plen);
+    LEAVE();
+    return r;
+}
+
+om_result* om_run_overlap(void* model, const om_run_cfg* cfg, const int* prompts, int B, int plen, char* err,
+                          int errlen) {
+    ENTER(err, errlen, (pending_cleanup(), (om_result*)NULL));
+    om_result* r = run_stepwise_((omodel*)model, cfg, prompts, B, plen, 1, NULL, 0);
+    LEAVE();
+    return r;
+}
+om_result* om_run_caching(void* model, const om_run_cfg* cfg, double cache_fraction, const int* prompts, int B,
+                          int plen, char* err, int errlen) {
+    ENTER(err, errlen, (pending_cleanup(), (om_result*)NULL));
+    om_result* r = run_caching_((omodel*)model, cfg, cache_fraction, prompts, B, plen);
     LEAVE();
     return r;
 }

@@ -97,6 +97,7 @@ smoe_run_result* flatten(const smoe::RunOut& r, int M, int E, int K) {
     o->bytes_baseline = r.bytes_baseline; o->bytes_total = r.bytes_total; o->setup_bytes = r.setup_bytes;
     o->warmup_bytes = r.warmup_bytes; o->lambda = r.lambda; o->c_measured = r.c_measured; o->wall_s = r.wall_s;
     o->gpu_s = r.gpu_s; o->h2d_expert_bytes = r.h2d_expert_bytes; o->h2d_s = r.h2d_s;
+    o->prefetch_bytes = r.prefetch_bytes; o->prefetch_wasted_bytes = r.prefetch_wasted_bytes;
     return o;
 }
 
@@ -191,6 +192,34 @@ int smoe_run_ondemand(smoe_engine* h, const smoe_run_config* cfg, const int* pro
     });
 }
 
+int smoe_run_overlap(smoe_engine* h, const smoe_run_config* cfg, const int* prompts, int B, int plen,
+                     smoe_run_result** out) {
+    return guarded([&] {
+        no_stepped_run(h);
+        smoe::RunCfg c = cfg_of(cfg);
+        c.overlap = 1;
+        auto r = smoe::run_ondemand(*h->e, c, prompts_of(prompts, B, plen));
+        *out = flatten(r, h->e->M, h->e->E, h->e->K);
+    });
+}
+
+int smoe_run_caching(smoe_engine* h, const smoe_run_config* cfg, double cache_fraction, const int* prompts, int B,
+                     int plen, smoe_run_result** out) {
+    return guarded([&] {
+        no_stepped_run(h);
+        if (!(cache_fraction > 0.0 && cache_fraction < 1.0))
+            throw smoe::Error(SMOE_CONFIG, "baseline: 0 < cache_fraction < 1 violated");
+        const auto P = prompts_of(prompts, B, plen);
+        smoe::RunCfg c = cfg_of(cfg);
+        c.policy = 1;  // hot_global profiling (baselines.cpp:119-145)
+        uint64_t warm = 0;
+        const auto cached = smoe::caching_sets(*h->e, c, P, cache_fraction, &warm);
+        auto r = smoe::run_ondemand(*h->e, cfg_of(cfg), P, &cached);
+        r.warmup_bytes = warm;
+        *out = flatten(r, h->e->M, h->e->E, h->e->K);
+    });
+}
+
 void smoe_free_result(smoe_run_result* r) {
     if (!r) return;
     std::free(r->tokens); std::free(r->n_tokens); std::free(r->ledger); std::free(r->outcomes);
@@ -232,6 +261,7 @@ int smoe_counters(smoe_engine* h, uint64_t* launches, double* alg_expert_bytes, 
         if (reset) {
             e.launches = e.ctl_h2d = e.ctl_d2h = 0;
             e.alg_expert_bytes = e.alg_dense_bytes = 0;
+            e.named.clear();
         }
     });
 }
@@ -279,6 +309,18 @@ int smoe_profile_reset(smoe_engine* h) {
         h->e->prof_collect();
         h->e->prof.clear();
         h->e->profiling = true;
+    });
+}
+int smoe_counter(smoe_engine* h, const char* name, double* value) {
+    return guarded([&] {
+        auto it = h->e->named.find(name);
+        *value = it == h->e->named.end() ? 0.0 : it->second;
+    });
+}
+int smoe_profile_stop(smoe_engine* h) {
+    return guarded([&] {
+        h->e->prof_collect();
+        h->e->profiling = false;
     });
 }
 int smoe_profile_read(smoe_engine* h, const char* cls, double* total_ms, long long* launches, double* bytes) {

@@ -107,7 +107,7 @@ Engine::Engine(const smoe_engine_config& c) {
     e_hi = e_lo + E / ep_world;
     int exp_slots = M * (E / ep_world);
     if (offload) {
-        exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * E, M * 4 + E);
+        exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * E, M * 4 + 2 * E);
         if (exp_slots < E) throw Error(kConfig, "engine: hbm_expert_slots must be >= experts_per_block");
     }
     n_slots = exp_slots + n_dense;
@@ -630,20 +630,29 @@ void Engine::prof_end(const char* cls, cudaEvent_t a, double bytes) {
     SMOE_CUDA(cudaEventRecord(b, stream));
     Prof& p = prof[cls];
     p.ev.emplace_back(a, b);
+    p.sub.push_back(prof_pass);
     p.n += 1;
     p.bytes += bytes;
+    if (prof_pass) {
+        Prof& q = prof[std::string(cls) + ":" + prof_pass];
+        q.n += 1;
+        q.bytes += bytes;
+    }
 }
 void Engine::prof_collect() {
     sync();
     for (auto& kv : prof) {
-        for (auto& pr : kv.second.ev) {
+        for (size_t i = 0; i < kv.second.ev.size(); ++i) {
+            auto& pr = kv.second.ev[i];
             float ms = 0.f;
             SMOE_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
             kv.second.ms += ms;
+            if (kv.second.sub[i]) prof[kv.first + ":" + kv.second.sub[i]].ms += ms;  // inserts never invalidate kv
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
         kv.second.ev.clear();
+        kv.second.sub.clear();
     }
 }
 
@@ -731,6 +740,11 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     if (T <= 0) return;
     NvtxRange nv(restricted ? "smoe draft pass" : "smoe pass");
     if (T > Tmax) throw Error(kConfig, "engine: rows per pass exceed max_batch*(max_gamma+1)");
+    struct PassKind {
+        const char*& slot;
+        PassKind(const char*& s, bool restricted) : slot(s) { slot = restricted ? "draft" : "verify"; }
+        ~PassKind() { slot = nullptr; }
+    } pass_kind(prof_pass, restricted);
     if (ep_world > 1) return pass_ep(T, rseq, rextra, extra_uniform, restricted, use_aff, log_slot);
     const size_t ws = wt == kF32 ? 4 : 2;
     const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)E * Tmax * d;

@@ -92,6 +92,7 @@ struct RunOut {
     double lambda = 1.0, c_measured = 0.0;
     double wall_s = 0, gpu_s = 0, h2d_s = 0;
     uint64_t h2d_expert_bytes = 0;
+    uint64_t prefetch_bytes = 0, prefetch_wasted_bytes = 0;  // overlap baseline (store prefetch)
     std::vector<uint64_t> lambda_inputs;  // 4 per phase: verify tokens, verify experts, step tokens, step experts
 };
 
@@ -174,6 +175,11 @@ public:
     std::vector<int> free_slots;
     int* h_store = nullptr;          // pinned: slot_of mirror [M*E], group sizes, group slots, raw picks
     int store_last_T = 0;
+    // overlap baseline (run_overlap): prefetch of the next layer's previous-step experts
+    bool store_prefetch = false;
+    std::vector<uint8_t> key_prefetched;  // [M*E] resident because of a prefetch, not yet routed to
+    std::vector<uint8_t> prev_need;       // [M*E] keys the previous step routed to
+    uint64_t prefetch_bytes = 0, prefetch_wasted = 0, prefetch_hits = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev;
     // hot_temporal re-pin decided per layer during a verify pass: (layer, raw picks [T][K], T) -> next set
     std::function<bool(int, const int*, int, std::vector<int>&)> repin_hook;
@@ -248,8 +254,16 @@ public:
 
     // ---- profiling (CUDA events around kernel classes)
     bool profiling = false;
-    struct Prof { double ms = 0; long long n = 0; double bytes = 0; std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
+    struct Prof {
+        double ms = 0;
+        long long n = 0;
+        double bytes = 0;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+        std::vector<const char*> sub;  // per event pair: the pass kind it also counts under ("cls:draft" ...)
+    };
     std::map<std::string, Prof> prof;
+    std::map<std::string, double> named;  // named counters (smoe_counter), reset with smoe_counters(reset)
+    const char* prof_pass = nullptr;  // "draft" / "verify" while a pass runs (sub-class of every record)
     void prof_begin(const char* cls, cudaEvent_t* a);
     void prof_end(const char* cls, cudaEvent_t a, double bytes);
     void prof_collect();

@@ -402,16 +402,33 @@ int spec_step(Engine& e, int* accepted_tokens) {
         // (this rank's experts only under expert parallelism)
         const double bpe = (double)e.real_bytes_per_expert();
         const uint64_t mine = (e.e_hi - e.e_lo >= 64 ? ~0ull : ((1ull << (e.e_hi - e.e_lo)) - 1)) << e.e_lo;
+        // and every routed (row, pick) on this rank's experts costs 2 * (U*d + d*f) flops
+        const double fpp = 2.0 * ((double)e.U * e.d + (double)e.d * e.f);
+        auto& ctr = e.named;
         for (int t = 0; t < g; ++t)
             for (int m = 0; m < M; ++m) {
                 uint64_t seen = 0;
-                for (int q = 0; q < na * K; ++q) seen |= 1ull << dfin[t][(size_t)m * na * K + q];
+                long long picks = 0;
+                for (int q = 0; q < na * K; ++q) {
+                    const int x = dfin[t][(size_t)m * na * K + q];
+                    seen |= 1ull << x;
+                    picks += x >= e.e_lo && x < e.e_hi;
+                }
                 e.alg_expert_bytes += bpe * __builtin_popcountll(seen & mine);
+                ctr["alg_expert_bytes:draft"] += bpe * __builtin_popcountll(seen & mine);
+                ctr["expert_flops:draft"] += fpp * (double)picks;
             }
         for (int m = 0; m < M; ++m) {
             uint64_t seen = 0;
-            for (int q = 0; q < TV * K; ++q) seen |= 1ull << S.vraw[(size_t)m * TV * K + q];
+            long long picks = 0;
+            for (int q = 0; q < TV * K; ++q) {
+                const int x = S.vraw[(size_t)m * TV * K + q];
+                seen |= 1ull << x;
+                picks += x >= e.e_lo && x < e.e_hi;
+            }
             e.alg_expert_bytes += bpe * __builtin_popcountll(seen & mine);
+            ctr["alg_expert_bytes:verify"] += bpe * __builtin_popcountll(seen & mine);
+            ctr["expert_flops:verify"] += fpp * (double)picks;
         }
     }
 
@@ -589,6 +606,9 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     }
     e.h2d_bytes = 0;
     e.h2d_ms = 0;
+    // overlap baseline on the physical store: prefetch the next layer's previous-step experts behind each
+    // layer's fetch (the reference's oracle overlap, baselines.cpp:101-111, is a cost-model max())
+    e.store_prefetch = e.offload && c.overlap != 0;
     e.reset_sequences(prompts);
     std::vector<int> rs(B), one(B, 1), raw, am(B);
     for (int b = 0; b < B; ++b) rs[b] = b;
@@ -625,8 +645,10 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
         const uint64_t bytes = res.ensure(need, 2, step, led);
         modeled += step_cost((uint64_t)B, n_need, bytes, c, c.overlap != 0);
         res.flush();
+        if (e.store_prefetch) e.prev_need = need;
     }
     tm.stop(e.stream, &R.gpu_s, &R.wall_s);
+    e.store_prefetch = false;
     R.phases = c.max_new_tokens;
     R.tau_mean = 1.0;
     R.tokens_total = (uint64_t)B * c.max_new_tokens;
@@ -643,6 +665,8 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     e.collect_h2d();
     R.h2d_expert_bytes = e.h2d_bytes;
     R.h2d_s = e.h2d_ms * 1e-3;
+    R.prefetch_bytes = e.prefetch_bytes;
+    R.prefetch_wasted_bytes = e.prefetch_wasted;
     return R;
 }
 

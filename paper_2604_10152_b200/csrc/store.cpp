@@ -25,6 +25,7 @@ void Engine::store_alloc(int exp_slots) {
     n_exp_slots = exp_slots;
     slot_key.assign(n_exp_slots, -1);
     key_pinned.assign((size_t)M * E, 0);
+    key_prefetched.assign((size_t)M * E, 0);
     h_slot_of.assign((size_t)M * E, -1);
     free_slots.clear();
     for (int s = n_exp_slots - 1; s >= 0; --s) free_slots.push_back(s);
@@ -38,6 +39,10 @@ void Engine::store_alloc(int exp_slots) {
 void Engine::store_reset() {
     std::fill(slot_key.begin(), slot_key.end(), -1);
     std::fill(key_pinned.begin(), key_pinned.end(), 0);
+    std::fill(key_prefetched.begin(), key_prefetched.end(), 0);
+    prev_need.clear();
+    prefetch_bytes = prefetch_wasted = 0;
+    prefetch_hits = 0;
     std::fill(h_slot_of.begin(), h_slot_of.end(), -1);
     free_slots.clear();
     for (int s = n_exp_slots - 1; s >= 0; --s) free_slots.push_back(s);
@@ -107,7 +112,11 @@ void Engine::store_pin_sets(const std::vector<std::vector<int>>& sets) {
     sync();
 }
 
-// Inside an unrestricted pass, after route(mo): fetch this layer's missing experts.
+// Inside an unrestricted pass, after route(mo): fetch this layer's missing experts.  With the
+// overlap baseline's prefetch on (store_prefetch), the next layer's experts of the previous step are
+// queued right behind them, so the copy engine keeps streaming while this layer computes and the host
+// waits for the next gate; the next layer then copies only what the prefetch missed.  Prefetched
+// experts the next layer does not route to are released unused at its finish (wasted bytes, counted).
 void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt_dev) {
     int* cnt = h_store + (size_t)M * E;
     int* gslot = cnt + E + 1;
@@ -121,12 +130,36 @@ void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt
     SMOE_CUDA(cudaEventRecord(a, copy_stream));
     for (int e = 0; e < E; ++e) {
         const int key = mo * E + e;
-        if (cnt[e] > 0 && h_slot_of[key] < 0) store_copy_in(key, store_take_slot(key));
+        if (cnt[e] > 0) {
+            if (h_slot_of[key] < 0) store_copy_in(key, store_take_slot(key));
+            else if (key_prefetched[key]) ++prefetch_hits;
+        } else if (key_prefetched[key]) {
+            prefetch_wasted += expert_bytes(0) + expert_bytes(1);  // released unused at the layer's finish
+        }
+        key_prefetched[key] = 0;
         gslot[e] = cnt[e] > 0 ? h_slot_of[key] : -1;
     }
+    // the copy stream is in order: this event also covers every earlier prefetch of this layer
     SMOE_CUDA(cudaEventRecord(b, copy_stream));
     SMOE_CUDA(cudaStreamWaitEvent(stream, b, 0));
     h2d_ev.emplace_back(a, b);
+    if (store_prefetch && mo + 1 < M) {
+        cudaEvent_t pa, pb;
+        SMOE_CUDA(cudaEventCreate(&pa));
+        SMOE_CUDA(cudaEventCreate(&pb));
+        SMOE_CUDA(cudaEventRecord(pa, copy_stream));
+        for (int e = 0; e < E; ++e) {
+            const int key = (mo + 1) * E + e;
+            if (!prev_need.empty() && prev_need[key] && h_slot_of[key] < 0 && !free_slots.empty()) {
+                const uint64_t before = h2d_bytes;
+                store_copy_in(key, store_take_slot(key));
+                prefetch_bytes += h2d_bytes - before;
+                key_prefetched[key] = 1;
+            }
+        }
+        SMOE_CUDA(cudaEventRecord(pb, copy_stream));
+        h2d_ev.emplace_back(pa, pb);
+    }
     SMOE_CUDA(cudaMemcpyAsync(group_slot, gslot, sizeof(int) * E, cudaMemcpyHostToDevice, stream));
     store_last_T = T;
 }

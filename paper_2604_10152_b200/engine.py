@@ -27,8 +27,9 @@ PHASES = {0: "speculation", 1: "verification", 2: "baseline-step"}
 EXPORTS = ["smoe_last_error", "smoe_engine_create", "smoe_engine_destroy", "smoe_engine_info", "smoe_engine_stream",
            "smoe_init_weights_exact", "smoe_init_weights_device", "smoe_upload_tensor", "smoe_set_affinity",
            "smoe_build_affinity_device", "smoe_get_affinity", "smoe_forward", "smoe_run_specmoe", "smoe_run_ondemand",
+           "smoe_run_overlap", "smoe_run_caching",
            "smoe_free_result", "smoe_spec_begin", "smoe_spec_step", "smoe_spec_end", "smoe_counters", "smoe_bench_expert_gemm",
-           "smoe_profile_reset", "smoe_profile_read", "smoe_ep_nccl_unique_id", "smoe_ep_attach_nccl",
+           "smoe_profile_reset", "smoe_profile_stop", "smoe_profile_read", "smoe_counter", "smoe_ep_nccl_unique_id", "smoe_ep_attach_nccl",
            "smoe_ep_loopback_create", "smoe_ep_loopback_destroy", "smoe_ep_attach_loopback", "smoe_ep_attach_host",
            "smoe_make_prompts"]
 
@@ -77,7 +78,8 @@ class RunResultC(C.Structure):
                 ("bytes_spec", C.c_uint64), ("bytes_verify", C.c_uint64), ("bytes_baseline", C.c_uint64),
                 ("bytes_total", C.c_uint64), ("setup_bytes", C.c_uint64), ("warmup_bytes", C.c_uint64),
                 ("lambda_", C.c_double), ("c_measured", C.c_double), ("wall_s", C.c_double), ("gpu_s", C.c_double),
-                ("h2d_expert_bytes", C.c_uint64), ("h2d_s", C.c_double)]
+                ("h2d_expert_bytes", C.c_uint64), ("h2d_s", C.c_double),
+                ("prefetch_bytes", C.c_uint64), ("prefetch_wasted_bytes", C.c_uint64)]
 
 
 _LIB = None
@@ -114,6 +116,9 @@ def lib():
     L.smoe_forward.argtypes = [vp, ip, C.c_int, ip, C.c_int, C.c_int, fp, ip, ip]
     L.smoe_run_specmoe.argtypes = [vp, C.POINTER(RunConfig), ip, C.c_int, C.c_int, C.POINTER(C.POINTER(RunResultC))]
     L.smoe_run_ondemand.argtypes = [vp, C.POINTER(RunConfig), ip, C.c_int, C.c_int, C.POINTER(C.POINTER(RunResultC))]
+    L.smoe_run_overlap.argtypes = [vp, C.POINTER(RunConfig), ip, C.c_int, C.c_int, C.POINTER(C.POINTER(RunResultC))]
+    L.smoe_run_caching.argtypes = [vp, C.POINTER(RunConfig), C.c_double, ip, C.c_int, C.c_int,
+                                   C.POINTER(C.POINTER(RunResultC))]
     L.smoe_free_result.argtypes = [C.POINTER(RunResultC)]
     L.smoe_spec_begin.argtypes = [vp, C.POINTER(RunConfig), ip, C.c_int, C.c_int]
     L.smoe_spec_step.argtypes = [vp, ip, ip]
@@ -129,6 +134,8 @@ def lib():
     L.smoe_ep_attach_loopback.argtypes = [vp, vp]
     L.smoe_ep_attach_host.argtypes = [vp, HOST_ALLGATHER, vp]
     L.smoe_profile_reset.argtypes = [vp]
+    L.smoe_profile_stop.argtypes = [vp]
+    L.smoe_counter.argtypes = [vp, C.c_char_p, dp]
     L.smoe_profile_read.argtypes = [vp, C.c_char_p, dp, C.POINTER(C.c_longlong), dp]
     L.smoe_make_prompts.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, ip]
     _LIB = L
@@ -221,7 +228,8 @@ def _collect(rp) -> RunResult:
         met = {k: getattr(r, k) for k in ("tau_mean", "tokens_total", "phases", "speculation_s", "verification_s",
                                           "modeled_seconds", "tokens_per_sec", "bytes_spec", "bytes_verify",
                                           "bytes_baseline", "bytes_total", "setup_bytes", "warmup_bytes",
-                                          "c_measured", "wall_s", "gpu_s", "h2d_expert_bytes", "h2d_s")}
+                                          "c_measured", "wall_s", "gpu_s", "h2d_expert_bytes", "h2d_s",
+                                          "prefetch_bytes", "prefetch_wasted_bytes")}
         met["lambda"] = r.lambda_
         return RunResult(toks, led, outc, tr, hot.reshape(r.moe_layers, r.experts), met)
     finally:
@@ -395,6 +403,24 @@ class Engine:
         _check(lib().smoe_run_ondemand(self.h, C.byref(c), pp, P.shape[0], P.shape[1], C.byref(out)))
         return _collect(out)
 
+    def run_overlap(self, cfg: RunCfg, prompts) -> RunResult:
+        """baselines.hpp:30-34 on the physical store (next-layer prefetch overlapping each layer)."""
+        P = np.asarray(prompts, dtype=np.int32)
+        c = cfg.to_c(self.spec)
+        p, pp = _iarr(P.reshape(-1))
+        out = C.POINTER(RunResultC)()
+        _check(lib().smoe_run_overlap(self.h, C.byref(c), pp, P.shape[0], P.shape[1], C.byref(out)))
+        return _collect(out)
+
+    def run_caching(self, cfg: RunCfg, prompts, cache_fraction: float = 0.10) -> RunResult:
+        """baselines.hpp:36-41: top ceil(cache_fraction*E) hot experts per layer pinned, then on-demand."""
+        P = np.asarray(prompts, dtype=np.int32)
+        c = cfg.to_c(self.spec)
+        p, pp = _iarr(P.reshape(-1))
+        out = C.POINTER(RunResultC)()
+        _check(lib().smoe_run_caching(self.h, C.byref(c), cache_fraction, pp, P.shape[0], P.shape[1], C.byref(out)))
+        return _collect(out)
+
     # ---- stepped loop (bench)
     def spec_begin(self, cfg: RunCfg, prompts):
         P = np.asarray(prompts, dtype=np.int32)
@@ -441,6 +467,14 @@ class Engine:
 
     def profile_reset(self):
         _check(lib().smoe_profile_reset(self.h))
+
+    def counter(self, name: str) -> float:
+        v = C.c_double()
+        _check(lib().smoe_counter(self.h, name.encode(), C.byref(v)))
+        return v.value
+
+    def profile_stop(self):
+        _check(lib().smoe_profile_stop(self.h))
 
     def profile_read(self, cls: str):
         ms, n, by = C.c_double(), C.c_longlong(), C.c_double()

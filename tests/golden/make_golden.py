@@ -74,6 +74,19 @@ def main():
                   "forward_logits": lg.tolist(), "forward_raw": raw.tolist(),
                   "affinity": m.affinity().tolist(), "weights": weights_digest(m, s)}
 
+    # the comparators (baselines.cpp:100-157): oracle overlap and caching, incl. an eviction-bound tier
+    base = []
+    for seed, B, frac, warm, cap in [(5, 3, 0.25, 6, 0), (6, 2, 0.10, 4, 0), (7, 2, 0.20, 16, 40 * 2 * 32 * 64 * 4)]:
+        s = ModelSpec(num_layers=4, experts=16, top_k=2, hidden=32, ffn=64, vocab=64, gate_skew=1.5, seed=seed)
+        m = ref.build(s)
+        prompts = make_prompts(seed, B, 8, s.vocab)
+        cfg = RunCfg(max_new_tokens=12, warmup_steps=warm, collect_trace=True, run_seed=seed,
+                     device_capacity_bytes=cap)
+        base.append({"spec": s.__dict__, "cfg": cfg.__dict__, "prompts": prompts, "cache_fraction": frac,
+                     "overlap": run_dict(m.run_overlap(cfg, prompts)),
+                     "caching": run_dict(m.run_caching(cfg, prompts, frac))})
+    gold["baselines"] = base
+
     # the reference-API caller (tests/cpp/caller.cpp) compiled against the reference itself
     import subprocess
     exe = os.path.join(ROOT, "oracle", "_ref", "caller_ref")
