@@ -9,9 +9,17 @@ pass over B*(gamma+1) positions, accept/rollback, hotness + re-pin + ledger.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--shape c1|c2|c4|c5] [--batch B]
 
-N > 1 (torchrun): one replica per GPU with independent sequences (weak scaling); time = max over
-ranks, value = tokens of all ranks / that time.  --impl reference times the reference's own CPU
-implementation (oracle/_ref, compiled from /root/reference) on the host cores.
+N > 1 (torchrun): expert parallelism -- every rank holds E/N experts of every layer and a
+replica of the dense weights, the rows of each pass are split over the ranks, and per MoE layer the
+gate / down-projection epilogues exchange routed rows through NVLink peer memory (SMOE_EP_MODE=a2a:
+NCCL all-to-alls instead); the global batch is fixed (strong scaling); time = max over ranks, value =
+the global batch's tokens / that time.  --replicas: independent replicas instead (weak scaling).
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
+/root/reference) on the host cores.
+
+The default C2 run adds sections to the same JSON line: the batch sweep 1-32 (the metric is quoted over
+batch 1-64), the on-demand comparator, gamma=8, gate_skew=2.0 and C4, the C3 offloaded store (with the
+on-demand, overlap and caching comparators) and the CPU reference.
 """
 from __future__ import annotations
 
@@ -57,6 +65,8 @@ def args_parse():
     p.add_argument("--offload-batch", type=int, default=64)
     p.add_argument("--offload-steps", type=int, default=2)
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of expert parallelism")
+    p.add_argument("--no-sections", action="store_true", help="skip the batch sweep / on-demand / gamma=8 / "
+                   "gate_skew=2 / C4 sections of the default C2 run")
     a = p.parse_args()
     if a.n_draft == 0:
         a.n_draft = 8 if a.shape == "c4" else 4
@@ -271,14 +281,184 @@ def offload_section(a, dev: int, batch: int, steps: int, warmup: int, gammas=(4,
             "pcie_busy_frac": (hs * 1e3) / ms if ms else None,
             "ledger_bytes_per_token_reference_units": r.metrics["bytes_total"] / max(1, r.metrics["tokens_total"])}
         del base_bytes
-    od = eng.run_ondemand(RunCfg(gamma=max(gammas), n_draft=a.n_draft, max_new_tokens=max(2, steps)), prompts)
-    od_tps = od.metrics["tokens_total"] / od.metrics["gpu_s"]
-    out["ondemand"] = {"tokens_per_s": od_tps, "pcie_bytes_per_token": od.metrics["h2d_expert_bytes"] / max(1, od.metrics["tokens_total"]),
-                       "h2d_gbs": od.metrics["h2d_expert_bytes"] / od.metrics["h2d_s"] / 1e9 if od.metrics["h2d_s"] else None}
+    # the comparators on the same physical store (baselines.cpp:29-157): on-demand, overlap (next-layer
+    # prefetch behind each layer's fetch) and caching (top ceil(0.1 E) = 1 expert per layer pinned from a
+    # hot_global on-demand warm-up of 4 steps; the reference's default warm-up is 64 steps)
+    ncomp = max(2, steps)
+    runs = {"ondemand": lambda c: eng.run_ondemand(c, prompts), "overlap": lambda c: eng.run_overlap(c, prompts),
+            "caching": lambda c: eng.run_caching(c, prompts, 0.10)}
+    for name, fn in runs.items():
+        r = fn(RunCfg(gamma=max(gammas), n_draft=a.n_draft, max_new_tokens=ncomp, warmup_steps=4))
+        tps = r.metrics["tokens_total"] / r.metrics["gpu_s"]
+        out[name] = {"tokens_per_s": tps, "ms_per_step": 1e3 * r.metrics["gpu_s"] / ncomp,
+                     "pcie_bytes_per_token": r.metrics["h2d_expert_bytes"] / max(1, r.metrics["tokens_total"]),
+                     "h2d_gbs": r.metrics["h2d_expert_bytes"] / r.metrics["h2d_s"] / 1e9 if r.metrics["h2d_s"] else None,
+                     "pcie_busy_frac": r.metrics["h2d_s"] / r.metrics["gpu_s"] if r.metrics["gpu_s"] else None,
+                     "ledger_bytes_per_token_reference_units": r.metrics["bytes_total"] / max(1, r.metrics["tokens_total"])}
+        if name == "overlap":
+            out[name]["prefetch_bytes"] = r.metrics["prefetch_bytes"]
+            out[name]["prefetch_wasted_bytes"] = r.metrics["prefetch_wasted_bytes"]
+    od_tps = out["ondemand"]["tokens_per_s"]
+    od_bpt = out["ondemand"]["pcie_bytes_per_token"]
+    for name in ("overlap", "caching"):
+        out[name]["speedup_vs_ondemand"] = out[name]["tokens_per_s"] / od_tps
+        out[name]["transfer_reduction_vs_ondemand"] = 1.0 - out[name]["pcie_bytes_per_token"] / max(1e-9, od_bpt)
     for g, v in out["gamma"].items():
         v["speedup_vs_ondemand"] = v["tokens_per_s"] / od_tps if od_tps else None
-        v["transfer_reduction_vs_ondemand"] = 1.0 - v["pcie_bytes_per_token"] / max(1e-9, out["ondemand"]["pcie_bytes_per_token"])
+        v["transfer_reduction_vs_ondemand"] = 1.0 - v["pcie_bytes_per_token"] / max(1e-9, od_bpt)
+        v["speedup_vs_best_baseline"] = v["tokens_per_s"] / max(out[n]["tokens_per_s"] for n in runs)
+        v["transfer_reduction_vs_caching"] = 1.0 - v["pcie_bytes_per_token"] / max(1e-9, out["caching"]["pcie_bytes_per_token"])
     eng.close()
+    return out
+
+
+def spec_measure(eng, stream, cfg, prompts, steps: int, warmup: int, profile: bool = True, clocks=None) -> dict:
+    """Stepped speculative phases on one engine: `warmup` untimed, `steps` timed by CUDA events on the
+    engine stream (nothing else recorded in between); then, with profile, the same number of steps again
+    with events around every launch (per kernel class, split by draft / verify pass)."""
+    import torch
+    eng.spec_begin(cfg, prompts)
+    for _ in range(warmup):
+        eng.spec_step()
+    eng.counters(reset=True)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    tokens = 0
+    for _ in range(steps):
+        tokens += eng.spec_step()[0]
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    out = {"ms": ev0.elapsed_time(ev1), "tokens": tokens, "clocks": clocks.stop() if clocks else None}
+    cnt = eng.counters(reset=True)
+    out["launches"] = cnt["launches"]
+    out["alg_expert_bytes"] = cnt["alg_expert_bytes"]
+    if profile:
+        eng.profile_reset()
+        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2.record(stream)
+        tp = 0
+        for _ in range(steps):
+            tp += eng.spec_step()[0]
+        ev3.record(stream)
+        ev3.synchronize()
+        eng.profile_stop()
+        out["ms_prof"] = ev2.elapsed_time(ev3)
+        out["tokens_prof"] = tp
+        out["cnt_prof"] = eng.counters()
+        out["named"] = {k: eng.counter(k) for k in ("alg_expert_bytes:draft", "alg_expert_bytes:verify",
+                                                     "expert_flops:draft", "expert_flops:verify")}
+        eng.counters(reset=True)
+        out["prof"] = {c: eng.profile_read(c) for c in (
+            "expert_gemm", "expert_gemm:draft", "expert_gemm:verify", "dense_gemm", "head_gemm", "pass", "gate",
+            "combine")}
+    res = eng.spec_end()
+    out["tau"] = res.metrics["tau_mean"]
+    out["res"] = res
+    return out
+
+
+def expert_roofline(m: dict, pk: dict) -> dict:
+    """Expert GEMM (fused MoE launch) roofline from a profiled spec_measure: algorithmic weight bytes of
+    the distinct experts each pass touches / CUDA-event time of those launches, against the HBM peak;
+    split by draft and verify pass, with the tensor-pipe fraction (algorithmic flops / time / bf16 peak)."""
+    pr, nm = m["prof"], m["named"]
+    out = {}
+    for kind in ("draft", "verify"):
+        t = pr[f"expert_gemm:{kind}"]
+        if t["launches"] and t["ms"] > 0:
+            gbs = nm[f"alg_expert_bytes:{kind}"] / (t["ms"] * 1e-3) / 1e9
+            tfs = nm[f"expert_flops:{kind}"] / (t["ms"] * 1e-3) / 1e12
+            out[kind] = {"launches": t["launches"], "avg_launch_us": 1e3 * t["ms"] / t["launches"],
+                         "achieved_GBps": gbs, "hbm_frac": gbs / pk["hbm_gbs"], "achieved_TFLOPs": tfs,
+                         "tensor_frac": tfs / pk["bf16_tflops"],
+                         "flop_per_byte": nm[f"expert_flops:{kind}"] / max(1.0, nm[f"alg_expert_bytes:{kind}"])}
+    t = pr["expert_gemm"]
+    gbs = m["cnt_prof"]["alg_expert_bytes"] / (t["ms"] * 1e-3) / 1e9 if t["ms"] > 0 else 0.0
+    out.update({"achieved_GBps": gbs, "frac": gbs / pk["hbm_gbs"], "launches": t["launches"],
+                "share_of_step": t["ms"] / m["ms_prof"] if m.get("ms_prof") else None})
+    return out
+
+
+def c2_engine(a, spec, dev, max_batch, max_gamma, rank=0, world=1, ep=False):
+    from paper_2604_10152_b200.engine import BF16, Engine
+    eng = Engine(spec, weight_type=BF16, max_batch=max_batch, max_gamma=max_gamma, device=dev,
+                 ep_rank=rank if ep else 0, ep_world=world if ep else 1)
+    if ep:
+        eng.attach_nccl(share_nccl_id(rank))
+    eng.init_device(0)
+    eng.build_affinity_device()
+    return eng
+
+
+def section_sweep(eng, stream, a, spec, pk) -> dict:
+    """BASELINE's metric is quoted over batch 1-64: every batch size on the headline engine."""
+    from paper_2604_10152_b200.engine import RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    rows = {}
+    for B in (1, 2, 4, 8, 16, 32):
+        m = spec_measure(eng, stream, RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30),
+                         make_prompts(1000, B, 8, spec.vocab), steps=4, warmup=2)
+        r = expert_roofline(m, pk)
+        rows[str(B)] = {"tokens_per_s": m["tokens"] / (m["ms"] * 1e-3), "ms_per_step": m["ms"] / 4, "tau": m["tau"],
+                        "expert_gemm_hbm_frac": r["frac"], "expert_gemm_share_of_step": r["share_of_step"],
+                        "hbm_expert_bytes_per_token": m["alg_expert_bytes"] / max(1, m["tokens"])}
+    return rows
+
+
+def section_ondemand(eng, a, spec, B: int, new_tokens: int = 6) -> dict:
+    """The non-speculative comparator (baselines.cpp:29-105) on the same HBM-resident engine: one target
+    pass per token.  HBM expert bytes/token = distinct experts touched per step (the ledger's keys: the
+    reference flushes every step) x real bytes per expert."""
+    from paper_2604_10152_b200.engine import RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    od = eng.run_ondemand(RunCfg(gamma=a.gamma, max_new_tokens=new_tokens), make_prompts(1000, B, 8, spec.vocab))
+    bpe = eng.info()["bytes_per_expert"]
+    toks = od.metrics["tokens_total"]
+    return {"workload": f"on-demand greedy decode (run_ondemand), B={B}, {new_tokens} tokens per sequence",
+            "tokens_per_s": toks / od.metrics["gpu_s"], "ms_per_token_step": 1e3 * od.metrics["gpu_s"] / new_tokens,
+            "hbm_expert_bytes_per_token": len(od.ledger) * bpe / max(1, toks)}
+
+
+def section_gamma(eng, stream, a, spec, pk, gamma: int, B: int) -> dict:
+    """C2 B=64 at a deeper speculation depth: gamma=8 puts n_e = B*(gamma+1)*K/E = 144 tokens per expert in
+    the verify pass, the only C2 point where the north_star's tensor-pipe target is reachable."""
+    from paper_2604_10152_b200.engine import RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    m = spec_measure(eng, stream, RunCfg(gamma=gamma, n_draft=a.n_draft, max_new_tokens=1 << 30),
+                     make_prompts(1000, B, 8, spec.vocab), steps=4, warmup=2)
+    r = expert_roofline(m, pk)
+    out = {"workload": f"C2 B={B} gamma={gamma} N={a.n_draft}", "tokens_per_s": m["tokens"] / (m["ms"] * 1e-3),
+           "ms_per_step": m["ms"] / 4, "tau": m["tau"], "expert_gemm": r,
+           "tensor_target": "north_star: expert GEMMs >= 60% of tcgen05 peak at batch >= 32; verify-pass AI here is "
+                            f"{r.get('verify', {}).get('flop_per_byte', 0):.0f} flop/B vs the ridge "
+                            f"{pk['bf16_tflops'] * 1e3 / pk['hbm_gbs']:.0f}"}
+    prof = os.path.join(ROOT, "profiles", "r03_ncu_gamma8_verify.json")
+    if os.path.exists(prof):
+        out["ncu_verify_launch"] = json.load(open(prof)).get("launches", [None])[0]
+    return out
+
+
+def section_shape(a, dev, shape: str, B: int, n_draft: int, pk, skew: float = 0.0, steps: int = 4) -> dict:
+    """A separate engine for another config of BASELINE.json (C4 fine-grained, or C2 with gate_skew)."""
+    import torch
+    from paper_2604_10152_b200.engine import SWIGLU3, ModelSpec, RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    spec = ModelSpec(**SHAPES[shape], seed=0, gate_skew=skew, expert_kind=SWIGLU3)
+    eng = c2_engine(a, spec, dev, B, a.gamma)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", dev))
+    m = spec_measure(eng, stream, RunCfg(gamma=a.gamma, n_draft=n_draft, max_new_tokens=1 << 30),
+                     make_prompts(1000, B, 8, spec.vocab), steps=steps, warmup=3)
+    r = expert_roofline(m, pk)
+    eng.close()
+    out = {"workload": f"{SHAPE_NAMES[shape]}, swiglu3 bf16 HBM-resident, B={B}, gamma={a.gamma}, N={n_draft}, "
+                       f"gate_skew={skew}", "tokens_per_s": m["tokens"] / (m["ms"] * 1e-3), "ms_per_step": m["ms"] / steps,
+           "tau": m["tau"], "hbm_expert_bytes_per_token": m["alg_expert_bytes"] / max(1, m["tokens"]),
+           "expert_gemm": r, "gpu_launches_per_step": m["launches"] / steps,
+           "breakdown_ms_per_step": {k: v["ms"] / steps for k, v in m["prof"].items() if v["launches"]}}
     return out
 
 
@@ -289,7 +469,7 @@ def run_b200(a) -> None:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    from paper_2604_10152_b200.engine import BF16, SWIGLU3, TANH2, Engine, ModelSpec, RunCfg
+    from paper_2604_10152_b200.engine import SWIGLU3, TANH2, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
 
     if a.shape == "c5" and (world < 2 or a.replicas):
@@ -312,58 +492,27 @@ def run_b200(a) -> None:
         return
     shp = dict(SHAPES[a.shape])
     spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
-    ep = world > 1 and not a.replicas  # N > 1: experts sharded, rows split, NCCL all-to-all dispatch/combine
-    eng = Engine(spec, weight_type=BF16, max_batch=a.batch, max_gamma=a.gamma, device=local,
-                 ep_rank=rank if ep else 0, ep_world=world if ep else 1)
-    if ep:
-        eng.attach_nccl(share_nccl_id(rank))
-    eng.init_device(0)
-    eng.build_affinity_device()
+    ep = world > 1 and not a.replicas  # N > 1: experts sharded over the GPUs, rows split
+    default_sections = world == 1 and a.shape == "c2" and not a.no_sections
+    eng = c2_engine(a, spec, local, a.batch, max(a.gamma, 8 if default_sections else a.gamma), rank, world, ep)
     seq_seed = 1000 if ep else 1000 + rank
     prompts = make_prompts(seq_seed, a.batch, 8, spec.vocab)
     cfg = RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30, run_seed=0 if ep else rank)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-
-    eng.spec_begin(cfg, prompts)
-    for _ in range(a.warmup):
-        eng.spec_step()
-    eng.counters(reset=True)
     if world > 1:
+        # every rank finishes its warm-up before the timed region starts (barrier inside the warm-up
+        # region of spec_measure is not possible; warm up here, then measure with warmup=0)
+        eng.spec_begin(cfg, prompts)
+        for _ in range(a.warmup):
+            eng.spec_step()
+        eng.spec_end()
         dist.barrier()
-    torch.cuda.synchronize()
-    clk = Clocks(local)
-    clk.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    tokens = 0
-    for _ in range(a.steps):
-        t, _act = eng.spec_step()
-        tokens += t
-    ev1.record(stream)
-    ev1.synchronize()
-    torch.cuda.synchronize()
-    clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
-    launches_timed = eng.counters(reset=True)["launches"]
-    # profiled copy of the timed region (same steps, same stream): CUDA events around every GEMM launch.
-    # Events between launches serialise the programmatic-dependent-launch overlap, so the step time
-    # above is taken without them.
-    eng.profile_reset()
-    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev2.record(stream)
-    tokens_prof = 0
-    for _ in range(a.steps):
-        tokens_prof += eng.spec_step()[0]
-    ev3.record(stream)
-    ev3.synchronize()
-    ms_prof = ev2.elapsed_time(ev3)
-    cnt = eng.counters(reset=True)
-    prof = eng.profile_read("expert_gemm")
-    dense = eng.profile_read("dense_gemm")
-    head = eng.profile_read("head_gemm")
-    pas = eng.profile_read("pass")
-    res = eng.spec_end()
-    ms, tokens = reduce_over_ranks(ms, tokens, sum_tokens=not ep)
+    m = spec_measure(eng, stream, cfg, prompts, a.steps, a.warmup if world == 1 else 1, profile=True,
+                     clocks=Clocks(local))
+    ms, tokens = reduce_over_ranks(m["ms"], m["tokens"], sum_tokens=not ep)
+    res = m["res"]
+    pk = peaks()
+    roof = expert_roofline(m, pk)
 
     # ---- e2e through the public API (host prompts in, host tokens out; per-phase H2D/D2H inside)
     eng.counters(reset=True)
@@ -384,33 +533,40 @@ def run_b200(a) -> None:
             dist.barrier()
             dist.destroy_process_group()
         return
-    pk = peaks()
+    pas = m["prof"]["pass"]
     if pas["launches"] > 0:
         # persistent pass kernel (every layer of a pass in one launch): its algorithmic bytes are the
         # touched expert weights plus the Mix (and dense-FFN) weights of every pass; the head GEMM is a
         # separate launch
+        head = m["prof"]["head_gemm"]
         head_bytes = float(head["launches"]) * spec.vocab * spec.hidden * 2
-        alg_bytes = cnt["alg_expert_bytes"] + cnt["alg_dense_bytes"] - head_bytes
+        alg_bytes = m["cnt_prof"]["alg_expert_bytes"] + m["cnt_prof"]["alg_dense_bytes"] - head_bytes
         dom = pas
-        roof_kernel = "k_pass_tc (persistent pass kernel: Mix GEMM, gate/top-K/remap/dispatch, fused SwiGLU expert GEMMs, combine+rms for all 32 layers; tcgen05/TMEM/TMA)"
+        roof_kernel = "k_pass_tc (persistent pass kernel; tcgen05/TMEM/TMA)"
         roof_alg = "per pass: distinct (layer, expert) touched x 3*d*f*2 B + L*d*d*2 B Mix weights (bf16)"
-        traffic = ncu_traffic(a.gamma, "r02_ncu_pass.json") if a.shape == "c2" and a.batch == 64 else None
-        traffic_src = "ncu --set full, profiles/r02_ncu_pass.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
+        traffic, traffic_src = None, "no capture for the pass kernel in this round"
     else:
-        alg_bytes = cnt["alg_expert_bytes"]
-        dom = prof
-        roof_kernel = "k_gemm_tc (tcgen05 grouped expert GEMM)"
+        dom = m["prof"]["expert_gemm"]
+        alg_bytes = m["cnt_prof"]["alg_expert_bytes"]
+        roof_kernel = "k_gemm_tc<SwiGLU, StoreF32> (fused MoE up+down: tcgen05 grouped expert GEMM)"
         roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
-        traffic = ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 else None
-        traffic_src = "ncu --set full, profiles/r02_ncu_fused_moe.json: dram read+write of one draft-pass and one verify-pass launch, weighted gamma:1 like the step"
+        traffic = ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 and a.gamma == 4 else None
+        traffic_src = ("ncu --set full, profiles/r02_ncu_fused_moe.json: dram read+write of one draft-pass and one "
+                       "verify-pass launch, weighted gamma:1 like the step (committed capture of this kernel)")
+        if a.shape == "c4":
+            traffic = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
+            traffic_src = "ncu --set full, profiles/r03_ncu_c4_moe.json (committed capture), weighted gamma:1"
     achieved = alg_bytes / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
+    ep_mode = os.environ.get("SMOE_EP_MODE", "p2p")
+    exch = ("gate/down-projection epilogues store rows into peer memory over NVLink (fused dispatch/combine)"
+            if ep_mode != "a2a" else "NCCL all-to-all dispatch/combine")
     line = {
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
         "scaling": "strong" if ep else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init N(0,1/sqrt(d)) weights, synthetic prompts)",
         "config": {"workload": f"{SHAPE_NAMES[a.shape]} spec-decode, {a.expert} experts HBM-resident, "
-                               f"B={a.batch}{'' if ep else '/GPU'}{f', experts sharded over {world} GPUs, rows split, NCCL all-to-all dispatch/combine' if ep else ''}, "
+                               f"B={a.batch}{'' if ep else '/GPU'}{f', experts sharded over {world} GPUs, rows split, {exch}' if ep else ''}, "
                                f"gamma={a.gamma}, N={a.n_draft}, hot_temporal+affinity, greedy",
                    "model": f"{a.shape} L{spec.num_layers} E{spec.experts} K{spec.top_k} d{spec.hidden} f{spec.ffn} "
                             f"V{spec.vocab}",
@@ -418,32 +574,56 @@ def run_b200(a) -> None:
                    "parallelism": f"ep{world}" if ep else f"replicas{world}",
                    "l2": "inputs larger than L2: every verify pass streams all touched expert weights "
                          "(>= 10 GB) from HBM"},
-        "tau": res.metrics["tau_mean"],
+        "tau": m["tau"],
         "expert_bytes_per_token": {
-            "hbm": cnt["alg_expert_bytes"] * world / max(1, tokens_prof),  # rank 0's share x G
-            "pcie": 0, "pcie_note": "HBM-resident config: no migration (see C3 offload)",
+            "hbm": m["cnt_prof"]["alg_expert_bytes"] * world / max(1, m["tokens_prof"]),  # rank 0's share x G
+            "pcie": 0, "pcie_note": "HBM-resident config: no migration (see offload_c3)",
             "ledger_reference_units": res.metrics["bytes_total"] / max(1, res.metrics["tokens_total"])},
         "e2e": {"value": e2e_tokens / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(c2["ctl_h2d"] / phases2), "d2h_bytes_per_step": int(c2["ctl_d2h"] / phases2),
                 "note": f"run_specmoe via the C ABI, {a.e2e_tokens} new tokens per sequence, host prompts in / host "
                         f"tokens out, per-phase control copies inside"},
-        "gpu_launches": int(launches_timed),
+        "gpu_launches": int(m["launches"]),
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "traffic": traffic, "traffic_source": traffic_src,
                      "launches": dom["launches"],
                      "avg_launch_ms": dom["ms"] / max(1, dom["launches"]),
                      "algorithmic_bytes_per_launch": alg_bytes / max(1, dom["launches"]),
-                     "share_of_step": dom["ms"] / ms_prof if ms_prof else None,
+                     "share_of_step": dom["ms"] / m["ms_prof"] if m.get("ms_prof") else None,
+                     "by_pass": {k: roof[k] for k in ("draft", "verify") if k in roof},
                      "measured_over": "profiled copy of the timed steps (CUDA events around each launch on the engine stream)",
                      "algorithmic_bytes": roof_alg,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
-        "breakdown_ms": {"pass_kernel": pas["ms"], "expert_gemm": prof["ms"], "dense_gemm": dense["ms"], "head_gemm": head["ms"],
-                         "profiled_steps_total": ms_prof, "timed_steps_total": ms},
-        "clocks": clocks,
+        "breakdown_ms": {k: v["ms"] for k, v in m["prof"].items() if v["launches"]},
+        "clocks": m["clocks"],
     }
-    if not a.no_offload_section and world == 1:
+    line["breakdown_ms"].update({"profiled_steps_total": m["ms_prof"], "timed_steps_total": m["ms"]})
+    if default_sections:
+        for key, fn in (("batch_sweep", lambda: section_sweep(eng, stream, a, spec, pk)),
+                        ("ondemand_c2", lambda: section_ondemand(eng, a, spec, a.batch)),
+                        ("gamma8_c2", lambda: section_gamma(eng, stream, a, spec, pk, 8, a.batch))):
+            try:
+                line[key] = fn()
+            except Exception as ex:  # reported, never fatal
+                line[key] = {"error": str(ex)[:300]}
+        od = line["ondemand_c2"]
+        if "tokens_per_s" in od:
+            od["speculative_vs_ondemand_tokens_per_s"] = line["value"] / od["tokens_per_s"]
+            od["speculative_vs_ondemand_expert_bytes_per_token"] = (line["expert_bytes_per_token"]["hbm"] /
+                                                                    od["hbm_expert_bytes_per_token"])
+    if world == 1:
         eng.close()
+    if default_sections:
+        for key, kw in (("hot_skew2_c2", dict(shape="c2", B=a.batch, n_draft=a.n_draft, skew=2.0)),
+                        ("c4", dict(shape="c4", B=32, n_draft=8))):
+            try:
+                line[key] = section_shape(a, local, pk=pk, **kw)
+            except Exception as ex:
+                line[key] = {"error": str(ex)[:300]}
+        if "expert_gemm" in line["c4"]:
+            line["c4"]["expert_gemm"]["traffic"] = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
+    if not a.no_offload_section and world == 1:
         try:
             line["offload_c3"] = offload_section(a, local, a.offload_batch, a.offload_steps, 1, gammas=(2, 4, 8))
         except Exception as ex:

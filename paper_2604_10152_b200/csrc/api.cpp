@@ -17,6 +17,8 @@
 #include <mutex>
 #include <numeric>
 #include <sstream>
+#include <thread>
+#include <atomic>
 
 #include "engine.h"
 
@@ -185,29 +187,48 @@ struct EngineSlot {
 std::mutex g_mu;
 std::map<const ModelWeights*, EngineSlot> g_engines;
 
+// Content hash of every weight tensor (the drop-in API takes ModelWeights by reference every call, so a
+// caller may refill it in place between calls; the device copy is rebuilt whenever any value changed).
+// Four independent multiply-xor lanes per tensor, tensors hashed on all host threads, combined in order.
+uint64_t hash_doubles(const std::vector<double>& v) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(v.data());
+    const size_t n = v.size();
+    uint64_t h[4] = {0x9e3779b97f4a7c15ull, 0xc2b2ae3d27d4eb4full, 0x165667b19e3779f9ull, 0x27d4eb2f165667c5ull};
+    size_t i = 0;
+    for (; i + 4 <= n; i += 4)
+        for (int j = 0; j < 4; ++j) h[j] = ((h[j] ^ w[i + j]) * 0x100000001b3ull) ^ (h[j] >> 29);
+    for (; i < n; ++i) h[0] = ((h[0] ^ w[i]) * 0x100000001b3ull) ^ (h[0] >> 29);
+    uint64_t out = n;
+    for (int j = 0; j < 4; ++j) out = fnv1a64(&h[j], sizeof h[j], out);
+    return out;
+}
+
 uint64_t fingerprint(const ModelWeights& w) {
-    uint64_t h = 0xcbf29ce484222325ull;
-    auto mix = [&](const std::vector<double>& v) {
-        const size_t n = v.size();
-        h = fnv1a64(&n, sizeof n, h);
-        const size_t probes[4] = {0, n / 3, n / 2, n ? n - 1 : 0};
-        for (size_t p : probes)
-            if (p < n) h = fnv1a64(&v[p], sizeof(double), h);
+    std::vector<const std::vector<double>*> ts{&w.embedding, &w.head};
+    for (const auto& L : w.layers) {
+        ts.push_back(&L.mix);
+        ts.push_back(&L.gate);
+        for (const auto& x : L.experts) { ts.push_back(&x.up); ts.push_back(&x.down); }
+        ts.push_back(&L.ffn.up);
+        ts.push_back(&L.ffn.down);
+    }
+    std::vector<uint64_t> hs(ts.size());
+    const size_t nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t i; (i = next.fetch_add(1)) < ts.size();) hs[i] = hash_doubles(*ts[i]);
     };
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nth; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    uint64_t h = 0xcbf29ce484222325ull;
     const ModelSpec& s = w.spec;
     const int dims[7] = {s.num_layers, s.experts_per_block, s.top_k, s.hidden_dim, s.ffn_dim, s.vocab_size,
                          (int)s.moe_layer_mask.size()};
     h = fnv1a64(dims, sizeof dims, h);
     h = fnv1a64(&s.gate_skew, sizeof s.gate_skew, h);
-    mix(w.embedding);
-    mix(w.head);
-    for (const auto& L : w.layers) {
-        mix(L.mix);
-        mix(L.gate);
-        for (const auto& x : L.experts) { mix(x.up); mix(x.down); }
-        mix(L.ffn.up);
-    }
-    return h;
+    return fnv1a64(hs.data(), hs.size() * sizeof(uint64_t), h);
 }
 
 uint64_t aff_fingerprint(const AffinityTable& a) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -95,6 +96,17 @@ __host__ __device__ inline int gate_threads(int d, int E) {
 }
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Kernel attributes (cudaFuncSetAttribute) are per device: true the first time the calling thread's
+// current device asks, so a launch helper configures each kernel once on every device it runs on.
+inline bool first_use_on_device(std::atomic<uint64_t>& seen) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (seen.load(std::memory_order_acquire) & bit) return false;
+    seen.fetch_or(bit, std::memory_order_acq_rel);
+    return true;
+}
 
 // Programmatic dependent launch (PDL).  Every hot-path kernel starts with pdl_wait() (no-op when not
 // launched with the PDL attribute) before touching memory written by earlier kernels, then

@@ -110,19 +110,53 @@ __device__ __forceinline__ long long gtimer() {
 constexpr long long kPfChunk = 256 * 1024;
 __device__ __forceinline__ int row_tiles(const Phase& P, int pair) { return pair ? (P.m_tiles + 1) / 2 : P.m_tiles; }
 
-// Stage ring of a grouped launch from the routing counts (call after the dependency wait; every role
-// computes the same layout): token space for the largest group's box, the rest for weight stages.
-__device__ __forceinline__ void grouped_layout(const TcParams& p, int& stages, int& stage_bytes, int& pair) {
-    int mx = 1;
-    for (int g = 0; g < p.G; ++g)
-        if (p.group_slot[g] >= 0) mx = max(mx, min(BN_MAX, p.group_cnt[g]));
-    pair = p.pair_ok && mx <= BN_MAX / 2 ? p.pair_ok : 0;
-    stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
-    stages = max(2, min(kMaxStages, p.stage_space / stage_bytes));
+// Grouped launches enumerate their units over a compacted list of work items = the (group, token tile)
+// pairs that have rows, built once per CTA from the routing counts after the dependency wait (warp 0,
+// one ballot pass over the groups) and kept in shared memory.  A draft pass routes to N of E experts
+// (C4: 8 of 64), so enumerating every (group, tile) would make most unit claims land on empty groups:
+// each such claim is one more round trip of the global unit counter for the claiming producer.
+// Single-group launches have one implicit group (item i = token tile i).
+constexpr int kMaxItems = 256;
+struct Plan {
+    int n_items, stages, stage_bytes, pair;
+};
+__device__ __forceinline__ int item_group(const int16_t* items, int i) { return items ? (items[i] & 0xff) : 0; }
+__device__ __forceinline__ int item_tile(const int16_t* items, int i) { return items ? (items[i] >> 8) : i; }
+
+// Warp 0 (all lanes), after the dependency wait: the item list and the stage ring of a grouped launch
+// (token space for the largest group's box, every other byte of shared memory for weight stages).
+__device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Plan* plan) {
+    const int lane = threadIdx.x & 31;
+    int n = 0, mx = 1;
+    for (int g0 = 0; g0 < p.G; g0 += 32) {
+        const int g = g0 + lane;
+        int cnt = 0;
+        if (g < p.G && p.group_slot[g] >= 0) cnt = p.group_cnt[g];
+        const int nt = min(p.n_tiles, (cnt + BN_MAX - 1) / BN_MAX);
+        mx = max(mx, min(BN_MAX, cnt));
+        int incl = nt;  // inclusive prefix of the tile counts over the lanes (groups stay in order)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        for (int t = 0; t < nt; ++t) items[n + incl - nt + t] = (int16_t)(g | (t << 8));
+        n += __shfl_sync(0xffffffffu, incl, 31);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+        const int pair = p.pair_ok && mx <= BN_MAX / 2 ? p.pair_ok : 0;
+        const int stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
+        plan->n_items = n;
+        plan->pair = pair;
+        plan->stage_bytes = stage_bytes;
+        plan->stages = max(2, min(kMaxStages, p.stage_space / stage_bytes));
+    }
 }
 
-__device__ __forceinline__ int units_of_phase(const TcParams& p, int ph, int pair) {
-    return p.G * p.n_tiles * row_tiles(p.ph[ph], (pair >> ph) & 1) * p.ph[ph].splits;
+__device__ __forceinline__ int units_of_phase(const TcParams& p, int n_items, int ph, int pair) {
+    return n_items * row_tiles(p.ph[ph], (pair >> ph) & 1) * p.ph[ph].splits;
 }
 
 __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, int& r0, int& r1) {
@@ -137,10 +171,12 @@ __device__ __forceinline__ void group_rows(const TcParams& p, int g, int& slot, 
     }
 }
 
-// Unit u -> (phase, group, token tile, row tile, split); returns false for units with no rows.
-__device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w, int pair) {
+// Unit u -> (phase, item = (group, token tile), row tile, split); returns false for units with no rows
+// (single-group launches: token tiles past the rows).
+__device__ __forceinline__ bool decode_unit(const TcParams& p, const int16_t* items, int n_items, int u, Unit& w,
+                                           int pair) {
     int ph = 0;
-    const int u0 = units_of_phase(p, 0, pair);
+    const int u0 = units_of_phase(p, n_items, 0, pair);
     if (u >= u0) {
         ph = 1;
         u -= u0;
@@ -152,8 +188,8 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int u, Unit& w, i
     u /= P.splits;
     const int mt = u % mtu;
     u /= mtu;
-    const int g = u % p.G;
-    const int nt = u / p.G;
+    const int g = item_group(items, u);
+    const int nt = item_tile(items, u);
     int slot, r0, r1;
     group_rows(p, g, slot, r0, r1);
     w.n0 = r0 + nt * BN_MAX;
@@ -175,14 +211,15 @@ __device__ __forceinline__ int phase0_units_of_group(const TcParams& p, int g, i
     int slot, r0, r1;
     group_rows(p, g, slot, r0, r1);
     if (slot < 0 || r1 <= r0) return 0;
-    return (r1 - r0 + BN_MAX - 1) / BN_MAX * row_tiles(p.ph[0], pair & 1) * p.ph[0].splits;
+    return min(p.n_tiles, (r1 - r0 + BN_MAX - 1) / BN_MAX) * row_tiles(p.ph[0], pair & 1) * p.ph[0].splits;
 }
 
 // Consumer side of the unit ring: returns false when the producer published "done".  whole_warp:
 // all 32 lanes call this (epilogue warps; lane 0 releases the slot after the warp has read it);
 // otherwise a single lane (the MMA issuer) calls it and releases the slot itself.
-__device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full, uint64_t* ring_empty, const int* ring,
-                                          int& cons, bool whole_warp, Unit& w, int pair) {
+__device__ __forceinline__ bool next_unit(const TcParams& p, const int16_t* items, int n_items, uint64_t* ring_full,
+                                          uint64_t* ring_empty, const int* ring, int& cons, bool whole_warp, Unit& w,
+                                          int pair) {
     const int r = cons % kRing;
     mbar_wait(&ring_full[r], (uint32_t)((cons / kRing) & 1));
     const int u = ring[r];
@@ -194,7 +231,7 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, uint64_t* ring_full
         mbar_arrive(&ring_empty[r]);
     }
     if (u < 0) return false;
-    decode_unit(p, u, w, pair);
+    decode_unit(p, items, n_items, u, w, pair);
     w.id = u;
     return true;
 }
@@ -229,11 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int pair = p.group_cnt ? 0 : p.pair_single;  // grouped launches: decided from the counts below
     int stages = p.stages;
     int stage_bytes = (pair ? 2 : 1) * kABytes + p.b_region;
-    int total_units = units_of_phase(p, 0, pair) + (p.nphase > 1 ? units_of_phase(p, 1, pair) : 0);
-    TR(const int trs = p.tr % kTrLaunches; if (threadIdx.x == 0) {
-        g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
-        if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, 0, 0); g_tr_meta[trs][3] = gridDim.x; }
-    })
+    int n_items = p.n_tiles;  // grouped launches: from the plan below
+    int total_units = units_of_phase(p, n_items, 0, pair) + (p.nphase > 1 ? units_of_phase(p, n_items, 1, pair) : 0);
+    TR(const int trs = p.tr % kTrLaunches;)
 
     // control block first (fixed size), then the 1024-aligned stage ring
     extern __shared__ uint8_t smem_raw[];
@@ -245,7 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* ring_empty = ring_full + kRing; // [kRing]
     int* ring = reinterpret_cast<int*>(ring_empty + kRing);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 1023) & ~uintptr_t(1023));
+    Plan* plan = reinterpret_cast<Plan*>(tmem_slot + 4);
+    int16_t* s_items = reinterpret_cast<int16_t*>(plan + 1);
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_items + kMaxItems) + 1023) & ~uintptr_t(1023));
+    const int16_t* items = p.group_cnt ? s_items : nullptr;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMaxStages; ++s) {
@@ -281,19 +319,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) pdl_trigger();  // let the next kernel's CTAs take SMs as ours retire
+    if (p.group_cnt) {
+        // grouped launches: the unit geometry (rows per expert) is written by the gate kernel that
+        // immediately precedes this one, so it may only be read after the dependency wait
+        dep_wait(p);
+        if (warp == 0) build_plan(p, s_items, plan);
+        __syncthreads();
+        n_items = plan->n_items;
+        pair = plan->pair;
+        stages = plan->stages;
+        stage_bytes = plan->stage_bytes;
+        total_units = units_of_phase(p, n_items, 0, pair) + (p.nphase > 1 ? units_of_phase(p, n_items, 1, pair) : 0);
+    }
+    TR(if (threadIdx.x == 0) {
+        g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
+        if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, n_items, 0, 0); g_tr_meta[trs][3] = gridDim.x; }
+    })
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- scheduler + TMA producer
             int it = 0;
-            bool kernel_dep = false;  // griddepcontrol.wait done: the previous kernel's outputs are visible
-            if (p.group_cnt) {
-                // grouped launches: the unit geometry (rows per expert) is written by the gate kernel
-                // that immediately precedes this one, so it may only be read after the dependency wait
-                dep_wait(p);
-                kernel_dep = true;
-                grouped_layout(p, stages, stage_bytes, pair);
-                total_units = units_of_phase(p, 0, pair) + (p.nphase > 1 ? units_of_phase(p, 1, pair) : 0);
-            }
+            // griddepcontrol.wait done: the previous kernel's outputs are visible (grouped: waited above)
+            bool kernel_dep = p.group_cnt != nullptr;
             for (int pub = 0;; ++pub) {
                 // dynamic work distribution: claim the next non-empty unit (single-group geometry is
                 // host-known; grouped geometry was waited for above)
@@ -301,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 Unit w;
                 do {
                     u = atomicAdd(&p.sched[0], 1);
-                } while (u < total_units && !decode_unit(p, u, w, pair));
+                } while (u < total_units && !decode_unit(p, items, n_items, u, w, pair));
                 TR(if (u < total_units && u < kTrUnits) { g_tr_unit[trs][u].cta = blockIdx.x | ((long long)p.tr << 32); g_tr_unit[trs][u].claim = gtimer(); })
                 const int r = pub % kRing;
                 mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
@@ -367,12 +414,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!kernel_dep) dep_wait(p);
         }
     } else if (warp == 1) {
-        dep_wait(p);
-        if (p.group_cnt) grouped_layout(p, stages, stage_bytes, pair);
+        if (!p.group_cnt) dep_wait(p);
         if (lane == 0) {  // ---------------- MMA issuer
             int it = 0, cnt = 0, cons = 0;
             Unit w;
-            while (next_unit(p, ring_full, ring_empty, ring, cons, false, w, pair)) {
+            while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, false, w, pair)) {
                 const int acc = cnt & 1;
                 mbar_wait(&acc_empty[acc], (uint32_t)(((cnt >> 1) & 1) ^ 1));
                 tc_fence_after();
@@ -411,12 +457,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
-        dep_wait(p);
+        if (!p.group_cnt) dep_wait(p);
         const int q = warp & 3;
         int cnt = 0, cons = 0;
         Unit w;
-        if (p.group_cnt) grouped_layout(p, stages, stage_bytes, pair);
-        while (next_unit(p, ring_full, ring_empty, ring, cons, true, w, pair)) {
+        while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, true, w, pair)) {
             const int acc = cnt & 1;
             mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
             tc_fence_after();
@@ -555,11 +600,9 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
 #define SMOE_TC_SMEM_KB 220
 #endif
     constexpr int kSmemBudget = SMOE_TC_SMEM_KB * 1024;  // stages + 1.5 KB control <= 227 KB
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_use_on_device(configured))
         SMOE_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI0, EPI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = true;
-    }
     TcParams p{};
     p.ph[0] = make_phase(a);
     p.nphase = b ? 2 : 1;
@@ -571,6 +614,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.single_rows = a.single_rows;
     p.single_slot = a.single_slot;
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
+    if (a.group_cnt && (long long)p.G * p.n_tiles > kMaxItems)
+        throw Error(kInvariant, "tcgen05 GEMM: more (group, token tile) items than the plan holds");
     constexpr int kCtrl = 1024;  // control block (barriers, unit ring, TMEM slot) + alignment slack below
     static const bool pair_env = [] {
         const char* v = getenv("SMOE_TC_PAIR");

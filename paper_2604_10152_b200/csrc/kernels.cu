@@ -668,11 +668,10 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
     a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0) +
                   (a.in_draft ? sizeof(int) * ((size_t)a.E * a.N + a.N) + a.E : 0);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_use_on_device(configured)) {
         SMOE_CUDA(cudaFuncSetAttribute(k_gate<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         SMOE_CUDA(cudaFuncSetAttribute(k_gate<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
     }
     const RowShape rs = row_shape(gate_threads(a.d, a.E));  // a row per cluster, a (virtual) warp per expert
     if (a.op == kF32) launch_kc(k_gate<float>, a.T * rs.C, rs.RT, smem, s, rs.C, a);

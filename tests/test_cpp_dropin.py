@@ -52,3 +52,31 @@ def test_sampling_caller_matches_reference():
     want = json.load(open(os.path.join(ROOT, "tests", "golden", "cpp_caller_sampling.json")))
     for k in want:
         assert got[k] == want[k], k
+
+
+@pytest.mark.gpu
+def test_caller_refilling_weights_in_place_sees_new_values():
+    """The device copy of a ModelWeights is keyed by its full contents, not its address: refilling the
+    tensors in place between calls reaches the GPU (head x2 -> logits x2 exactly; one expert value)."""
+    exe = os.path.join(ROOT, "build", "caller_mutate_b200")
+    build_caller("caller_mutate.cpp", exe)
+    got = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+    assert got == {"head_scaled_exact": 1, "expert_change_seen": 1}
+
+
+@pytest.mark.gpu
+def test_caller_on_tcgen05_path_is_lossless():
+    """The same reference-API client with SPECMOE_B200_DTYPE=bf16 (the drop-in's tcgen05 path): every
+    speculative policy decodes exactly the on-demand token stream, overlap/caching decode it too, the
+    error behaviour is the reference's, and the logits are within the bf16 tolerance of the reference's."""
+    build_caller()
+    env = dict(os.environ, SPECMOE_B200_DTYPE="bf16")
+    got = json.loads(subprocess.run([EXE], capture_output=True, text=True, check=True, env=env).stdout)
+    want = json.load(open(os.path.join(ROOT, "tests", "golden", "cpp_caller.json")))
+    od = got["ondemand"]["tokens"]
+    for k in ("specmoe_hot_temporal", "specmoe_random", "specmoe_hot_global", "overlap", "caching"):
+        assert got[k]["tokens"] == od, k
+    assert got["errors"] == want["errors"]
+    assert got["specmoe_hot_temporal"]["metrics"]["bytes_spec"] == 0
+    gl, wl = np.asarray(got["forward"]["logits"]), np.asarray(want["forward"]["logits"])
+    assert np.max(np.abs(gl - wl)) <= 3e-2 * np.max(np.abs(wl))

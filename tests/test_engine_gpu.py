@@ -26,7 +26,8 @@ def gold(name):
         return json.load(f)
 
 
-def run_dict(r, drop=("wall_s", "gpu_s", "h2d_expert_bytes", "h2d_s")):
+def run_dict(r, drop=("wall_s", "gpu_s", "h2d_expert_bytes", "h2d_s", "prefetch_bytes",
+                        "prefetch_wasted_bytes")):
     return {"tokens": r.tokens, "ledger": [list(x) for x in r.ledger],
             "outcomes": [list(o[:5]) + [list(o[5])] for o in r.outcomes],
             "trace": [[t[0], t[1], t[2], list(t[3])] for t in r.trace],

@@ -25,10 +25,16 @@ def run(B, gamma, out):
     from paper_2604_10152_b200 import engine as eng
     from paper_2604_10152_b200.engine import BF16, SWIGLU3, Engine, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
-    spec = ModelSpec(num_layers=32, experts=8, top_k=2, hidden=D, ffn=F, vocab=32000, expert_kind=SWIGLU3)
+    if os.environ.get("SHAPE") == "c4":  # fine-grained E64 K6 (C4), N=8
+        spec = ModelSpec(num_layers=28, experts=64, top_k=6, hidden=2048, ffn=1408, vocab=102400,
+                         moe_mask=[0] + [1] * 27, expert_kind=SWIGLU3)
+        nd = 8
+    else:
+        spec = ModelSpec(num_layers=32, experts=8, top_k=2, hidden=D, ffn=F, vocab=32000, expert_kind=SWIGLU3)
+        nd = 4
     e = Engine(spec, weight_type=BF16, max_batch=B, max_gamma=gamma).init_device(0)
     e.build_affinity_device()
-    e.spec_begin(RunCfg(gamma=gamma, n_draft=4, max_new_tokens=1 << 30), make_prompts(1000, B, 8, spec.vocab))
+    e.spec_begin(RunCfg(gamma=gamma, n_draft=nd, max_new_tokens=1 << 30), make_prompts(1000, B, 8, spec.vocab))
     for _ in range(4):
         e.spec_step()
     lib = eng.lib()
@@ -176,6 +182,36 @@ def analyze(path):
     return rows
 
 
+def dump_units(path, rows, dst, per_kind=3):
+    """Every unit of a few fused MoE launches per kind (draft / verify by unit count): [cta, claim,
+    tma_done, mma_first, mma_done, epi_done] in us from the launch's first CTA start, + unit id."""
+    raw = open(path, "rb").read()
+    nl, nu, nc = np.frombuffer(raw[:12], np.int32)
+    off = 12 + nl * 16
+    cta = np.frombuffer(raw[off:off + nl * nc * 2 * 8], np.int64).reshape(nl, nc, 2)
+    off += nl * nc * 16
+    un = np.frombuffer(raw[off:], np.int64).reshape(nl, nu, 6)
+    out, seen = [], {}
+    for r in rows:
+        if r["kind"] == "mix/head":
+            continue
+        k = r["n_up"] + r["n_down"]
+        if seen.get(k, 0) >= per_kind:
+            continue
+        seen[k] = seen.get(k, 0) + 1
+        s = r["slot"]
+        tag = un[s, :, 0] >> 32
+        m = (un[s, :, 1] > 0) & (tag == r["launch"])
+        t0 = r["t0"]
+        ids = np.nonzero(m)[0]
+        U = un[s, m]
+        units = [[int(U[i, 0] & 0xFFFFFFFF)] + [round((int(U[i, j]) - t0) / 1e3, 2) for j in range(1, 6)] + [int(ids[i])]
+                 for i in range(len(U))]
+        ends = [round((int(x) - t0) / 1e3, 2) for x in cta[s, :r["grid"], 1]]
+        out.append({"launch": r["launch"], "units_total": k, "dur_us": r["dur_us"], "units": units, "cta_end": ends})
+    json.dump(out, open(dst, "w"))
+
+
 if __name__ == "__main__":
     if sys.argv[1:2] == ["--analyze"]:
         analyze(sys.argv[2])
@@ -187,3 +223,4 @@ if __name__ == "__main__":
         run(B, g, out)
         rows = analyze(out)
         json.dump(rows, open("gpurun_out/" + os.path.basename(out).replace(".bin", ".json"), "w"), indent=0)
+        dump_units(out, rows, "gpurun_out/" + os.path.basename(out).replace(".bin", "_units.json"))
