@@ -42,12 +42,15 @@ typedef struct {
                                 (0, 0 or 0, 1 = single GPU); attach a transport before running */
 } smoe_engine_config;
 
-/* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy/seed (greedy). */
+/* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy/seed + decode mode. */
 typedef struct {
     int gamma, n_draft, max_new_tokens, use_affinity, warmup_steps, policy, collect_trace;
     uint64_t run_seed;
     uint64_t device_capacity_bytes, bytes_per_expert; /* ledger accounting (reference units) */
     double host_bandwidth, ssd_bandwidth, compute_rate, compute_cost_per_expert;
+    int mode;           /* DecodeMode (specdec.hpp:15): 0 greedy, 1 sampling (draws on the device from the
+                           host's sample_rng stream, substream(run_seed, "samp"), in the reference's order) */
+    double temperature; /* sampling temperature (> 0) */
 } smoe_run_config;
 
 typedef struct { int phase, step, layer, expert; uint64_t bytes; } smoe_ledger_entry; /* memsim.hpp:44-49 */

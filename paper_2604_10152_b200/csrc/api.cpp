@@ -319,6 +319,8 @@ smoe::RunCfg run_cfg(const SpecConfig& c, DraftPolicy p, const TierConfig& t, ui
     r.ssd_bandwidth = t.ssd_bandwidth;
     r.compute_rate = t.compute_rate_tokens_per_s;
     r.compute_cost_per_expert = t.compute_cost_per_active_expert_s;
+    r.mode = c.mode == DecodeMode::sampling ? 1 : 0;  // device-side draws, host RNG order (sampling.cu)
+    r.temperature = c.temperature;
     return r;
 }
 
@@ -890,128 +892,6 @@ VerifyResult verify_sampling(const ModelWeights& weights, const std::vector<int>
     });
 }
 
-namespace {
-// Host-orchestrated loop for sampling mode (reference specdec.cpp:190-397 control flow), compute on
-// the GPU through speculate / verify_sampling.
-RunResult run_specmoe_sampling(const ModelWeights& w, const SpecConfig& cfg, DraftPolicy policy, const TierConfig& tier,
-                               const std::vector<std::vector<int>>& prompts, uint64_t run_seed,
-                               const AffinityTable* affinity, bool trace) {
-    const ModelSpec& s = w.spec;
-    const int M = s.moe_layer_count(), E = s.experts_per_block, g = cfg.gamma;
-    const AffinityTable* remap = cfg.use_affinity ? affinity : nullptr;
-    const int B = (int)prompts.size();
-    Rng policy_rng(substream(run_seed, 0x706f6c69ull));
-    Rng sample_rng(substream(run_seed, 0x73616d70ull));
-    RunResult r;
-    r.hotness = HotnessCounter(M, E);
-    ResidencyState res(s, tier);
-    DraftState ds;
-    ds.policy = policy;
-    ds.n_draft = cfg.n_draft;
-    HotnessCounter pc(M, E);
-    ds.sets = select_draft_experts(DraftPolicy::random, pc, ds, E, policy_rng);
-    if (policy == DraftPolicy::hot_global) {
-        HotnessCounter wc(M, E);
-        MigrationLedger wl;
-        ResidencyState wr(s, tier);
-        auto work = prompts;
-        for (int st = 0; st < cfg.warmup_steps; ++st) {
-            std::set<ExpertKey> need;
-            ActivationRecord rec;
-            for (auto& sq : work) {
-                ForwardResult fr = forward(w, sq);
-                for (size_t l = 0; l < fr.activations.size(); ++l)
-                    for (int x : fr.activations[l].raw) need.insert({(int)l, x});
-                sq.push_back(greedy_next(fr.logits));
-                rec.rows.push_back(std::move(fr.activations));
-            }
-            ensure_resident(need, Phase::baseline_step, st, wl, wr);
-            flush_transients(wr);
-            record_activations(wc, rec);
-        }
-        r.metrics.warmup_bytes = wl.total();
-        ds.sets = select_draft_experts(DraftPolicy::hot_global, wc, ds, E, policy_rng);
-    }
-    pin_draft_experts(ds.sets, res, r.ledger, Phase::verification, -1);
-    r.metrics.setup_bytes = r.ledger.snapshot().total;
-    r.ledger.reset();
-    auto seq = prompts;
-    std::vector<int> gen(B, 0);
-    r.tokens.assign(B, {});
-    uint64_t tau_sum = 0, tau_cnt = 0;
-    double spec_s = 0, ver_s = 0, step_s = 0;
-    int phase = 0;
-    for (;; ++phase) {
-        std::vector<int> act;
-        for (int b = 0; b < B; ++b)
-            if (gen[b] < cfg.max_new_tokens) act.push_back(b);
-        if (act.empty()) break;
-        std::vector<std::vector<int>> pre;
-        for (int b : act) pre.push_back(seq[b]);
-        SpeculationResult sr = speculate(w, ds, remap, pre, g, cfg.mode, cfg.temperature, sample_rng);
-        for (int t = 0; t < g; ++t) spec_s += step_latency(act.size(), sr.distinct_draft_experts[t], 0, tier, false).total_s;
-        std::vector<VerifyResult> vs;
-        for (size_t i = 0; i < act.size(); ++i)
-            vs.push_back(verify_sampling(w, seq[act[i]], sr.drafts[i], sr.draw_probs[i], cfg.temperature, sample_rng));
-        std::set<ExpertKey> need, first;
-        for (const auto& v : vs)
-            for (size_t p = 0; p < v.positions.rows.size(); ++p)
-                for (size_t l = 0; l < v.positions.rows[p].size(); ++l)
-                    for (int x : v.positions.rows[p][l].raw) {
-                        need.insert({(int)l, x});
-                        if (p == 0) first.insert({(int)l, x});
-                    }
-        const uint64_t vb = ensure_resident(need, Phase::verification, phase, r.ledger, res);
-        const uint64_t vt = act.size() * (uint64_t)(g + 1);
-        ver_s += step_latency(vt, need.size(), vb, tier, false).total_s;
-        r.lambda_inputs.push_back(LambdaInputs{vt, need.size(), act.size(), first.size()});
-        step_s += step_latency(act.size(), first.size(), first.size() * tier.bytes_per_expert, tier, false).total_s;
-        for (size_t i = 0; i < act.size(); ++i) {
-            const int b = act[i];
-            const VerifyResult& v = vs[i];
-            r.outcomes.push_back(StepOutcome{b, phase, sr.drafts[i], v.accepted, v.correction, v.accepted + 1});
-            tau_sum += v.accepted + 1;
-            ++tau_cnt;
-            std::vector<int> prod(sr.drafts[i].begin(), sr.drafts[i].begin() + v.accepted);
-            prod.push_back(v.correction);
-            const int take = std::min<int>((int)prod.size(), cfg.max_new_tokens - gen[b]);
-            for (int t = 0; t < take; ++t) {
-                seq[b].push_back(prod[t]);
-                r.tokens[b].push_back(prod[t]);
-            }
-            gen[b] += take;
-            record_activations(pc, v.positions);
-            record_activations(r.hotness, v.positions);
-            if (trace)
-                for (const auto& row : v.positions.rows)
-                    for (size_t l = 0; l < row.size(); ++l) r.trace.push_back(TraceRow{phase, b, (int)l, row[l].raw});
-        }
-        if (policy == DraftPolicy::hot_temporal) {
-            auto next = select_draft_experts(DraftPolicy::hot_temporal, pc, ds, E, policy_rng);
-            pin_draft_experts(next, res, r.ledger, Phase::verification, phase);
-            ds.sets = std::move(next);
-        }
-        pc.reset();
-        flush_transients(res);
-    }
-    RunMetrics& m = r.metrics;
-    m.phases = phase;
-    m.tau_mean = tau_cnt ? (double)tau_sum / (double)tau_cnt : 1.0;
-    for (const auto& t : r.tokens) m.tokens_total += t.size();
-    m.speculation_s = spec_s;
-    m.verification_s = ver_s;
-    m.modeled_seconds = spec_s + ver_s;
-    m.tokens_per_sec = m.modeled_seconds > 0 ? (double)m.tokens_total / m.modeled_seconds : 0.0;
-    m.bytes_spec = r.ledger.total(Phase::speculation);
-    m.bytes_verify = r.ledger.total(Phase::verification);
-    m.bytes_baseline = r.ledger.total(Phase::baseline_step);
-    m.bytes_total = r.ledger.total();
-    m.lambda = r.lambda_inputs.empty() ? 1.0 : measure_lambda(r.lambda_inputs, tier);
-    m.c_measured = (phase > 0 && step_s > 0) ? (spec_s / ((double)phase * g)) / (step_s / (double)phase) : 0.0;
-    return r;
-}
-}  // namespace
-
 RunResult run_specmoe(const ModelWeights& weights, const SpecConfig& config, DraftPolicy policy, const TierConfig& tier,
                       const std::vector<std::vector<int>>& prompts, uint64_t run_seed, const AffinityTable* affinity,
                       bool collect_trace) {
@@ -1023,8 +903,6 @@ RunResult run_specmoe(const ModelWeights& weights, const SpecConfig& config, Dra
     if (prompts.empty()) throw ConfigError("run_specmoe: no prompts");
     tier.validate(config.n_draft, M);
     if (config.use_affinity && !affinity) throw InvariantError("run_specmoe: affinity table required but missing");
-    if (config.mode == DecodeMode::sampling)
-        return run_specmoe_sampling(weights, config, policy, tier, prompts, run_seed, affinity, collect_trace);
     return guard([&] {
         std::lock_guard<std::mutex> lk(g_mu);
         smoe::Engine& e = engine_for(weights, (int)prompts.size(), config.gamma, config.use_affinity ? affinity : nullptr);
@@ -1081,48 +959,6 @@ RunResult stepwise(const ModelWeights& w, const std::vector<std::vector<int>>& p
     const int M = s.moe_layer_count(), E = s.experts_per_block;
     if (prompts.empty()) throw ConfigError("baseline run: no prompts");
     tier.validate(0, M);
-    if (decode.mode == DecodeMode::sampling) {  // host loop, GPU forward (reference baselines.cpp:29-99)
-        Rng rng(substream(run_seed, 0x73616d70ull));
-        RunResult r;
-        r.hotness = HotnessCounter(M, E);
-        ResidencyState res(s, tier);
-        if (pinned) {
-            pin_draft_experts(*pinned, res, r.ledger, Phase::baseline_step, -1);
-            r.metrics.setup_bytes = r.ledger.snapshot().total;
-            r.ledger.reset();
-        }
-        auto seq = prompts;
-        r.tokens.assign(prompts.size(), {});
-        double modeled = 0.0;
-        for (int st = 0; st < decode.max_new_tokens; ++st) {
-            std::set<ExpertKey> need;
-            ActivationRecord rec;
-            for (size_t b = 0; b < seq.size(); ++b) {
-                ForwardResult fr = forward(w, seq[b]);
-                for (size_t l = 0; l < fr.activations.size(); ++l)
-                    for (int x : fr.activations[l].raw) need.insert({(int)l, x});
-                const int tok = sample_next(fr.logits, decode.temperature, rng);
-                seq[b].push_back(tok);
-                r.tokens[b].push_back(tok);
-                if (trace)
-                    for (size_t l = 0; l < fr.activations.size(); ++l)
-                        r.trace.push_back(TraceRow{st, (int)b, (int)l, fr.activations[l].raw});
-                rec.rows.push_back(std::move(fr.activations));
-            }
-            const uint64_t by = ensure_resident(need, Phase::baseline_step, st, r.ledger, res);
-            modeled += step_latency(seq.size(), need.size(), by, tier, overlap).total_s;
-            record_activations(r.hotness, rec);
-            flush_transients(res);
-        }
-        RunMetrics& m = r.metrics;
-        m.phases = decode.max_new_tokens;
-        m.tokens_total = (uint64_t)prompts.size() * decode.max_new_tokens;
-        m.modeled_seconds = m.verification_s = modeled;
-        m.tokens_per_sec = modeled > 0 ? (double)m.tokens_total / modeled : 0.0;
-        m.bytes_baseline = r.ledger.total(Phase::baseline_step);
-        m.bytes_total = r.ledger.total();
-        return r;
-    }
     return guard([&] {
         std::lock_guard<std::mutex> lk(g_mu);
         smoe::Engine& e = engine_for(w, (int)prompts.size(), decode.gamma, nullptr);

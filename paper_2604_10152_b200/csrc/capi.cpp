@@ -45,6 +45,8 @@ smoe::RunCfg cfg_of(const smoe_run_config* c) {
     r.ssd_bandwidth = c->ssd_bandwidth;
     r.compute_rate = c->compute_rate;
     r.compute_cost_per_expert = c->compute_cost_per_expert;
+    r.mode = c->mode;
+    r.temperature = c->temperature;
     return r;
 }
 

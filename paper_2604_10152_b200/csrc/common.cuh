@@ -43,7 +43,7 @@ enum Epi : int {
 };
 
 // Device-resident error flag bits (checked once per phase, SURVEY 5 failure detection).
-enum Flag : int { kFlagNonFiniteLogits = 1, kFlagEmptyRemap = 2, kFlagNonFiniteGate = 4 };
+enum Flag : int { kFlagNonFiniteLogits = 1, kFlagEmptyRemap = 2, kFlagNonFiniteGate = 4, kFlagZeroDrawProb = 8 };
 
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // common.hpp:27-32
     x += 0x9e3779b97f4a7c15ull;

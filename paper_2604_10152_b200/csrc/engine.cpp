@@ -102,13 +102,13 @@ Engine::Engine(const smoe_engine_config& c) {
     ep_rank = c.ep_rank;
     if (ep_rank < 0 || ep_rank >= ep_world) throw Error(kConfig, "engine: ep_rank outside [0, ep_world)");
     if (E % ep_world) throw Error(kConfig, "engine: experts_per_block must be divisible by ep_world");
-    if (ep_world > 1 && offload) throw Error(kConfig, "engine: expert parallelism with the offloaded store is not supported");
     e_lo = ep_rank * (E / ep_world);
     e_hi = e_lo + E / ep_world;
-    int exp_slots = M * (E / ep_world);
-    if (offload) {
-        exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * E, M * 4 + 2 * E);
-        if (exp_slots < E) throw Error(kConfig, "engine: hbm_expert_slots must be >= experts_per_block");
+    const int eo = E / ep_world;
+    int exp_slots = M * eo;
+    if (offload) {  // each rank stores its own experts: pinned draft share + two layers' transients
+        exp_slots = c.hbm_expert_slots > 0 ? c.hbm_expert_slots : std::min(M * eo, M * std::min(4, eo) + 2 * eo);
+        if (exp_slots < eo) throw Error(kConfig, "engine: hbm_expert_slots must be >= experts_per_block / ep_world");
     }
     n_slots = exp_slots + n_dense;
     emb64 = dalloc<double>((size_t)V * d);
@@ -188,12 +188,12 @@ Engine::Engine(const smoe_engine_config& c) {
         ep_p2p = use_tc && fuse_moe && E <= 64 && !(mode && std::string(mode) == "a2a");
         rcnt = dalloc<int>(E);
         ep_gslot = dalloc<int>((size_t)std::max(1, M) * E);
+        ep_cntg = dalloc<int>((size_t)ep_world * E);
         ep_logs = dalloc<int>((size_t)(1 + ep_world) * 2 * std::max(1, M) * Tmax * K);
         amax_loc = dalloc<int>(Tmax);
         logits_loc = dalloc<float>((size_t)Tmax * V);
         // group g = (source rank g / (E/G), local expert g % (E/G)) -> this rank's weight slot
         std::vector<int> gs((size_t)std::max(1, M) * E);
-        const int eo = E / ep_world;
         for (int m = 0; m < M; ++m)
             for (int g = 0; g < E; ++g) gs[(size_t)m * E + g] = h_slot_of[(size_t)m * E + e_lo + g % eo];
         h2d(ep_gslot, gs.data(), sizeof(int) * gs.size());
@@ -250,6 +250,7 @@ Engine::~Engine() {
     for (void* q : ep_ipc_opened) cudaIpcCloseMemHandle(q);
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
     fr(ep_flags); fr(ep_peer);
+    fr(ep_cntg); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(comb_ctr); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
@@ -278,6 +279,22 @@ void Engine::h2d(void* dst, const void* src, size_t bytes) {
     sync();
 }
 
+void Engine::sampling_alloc() {
+    if (samp_u) return;
+    samp_u = dalloc<double>((size_t)Gmax * Bmax + (size_t)Bmax * (Gmax + 1));
+    samp_q = dalloc<double>((size_t)Gmax * Bmax * V);
+    samp_stats = dalloc<double>((size_t)Tmax * 2);
+    samp_ratio = dalloc<double>((size_t)Bmax * Gmax);
+    samp_i = dalloc<int>((size_t)2 * Bmax + 1);
+}
+
+void Engine::upload_doubles(double* dst, const double* src, size_t n) {
+    if (n == 0) return;
+    std::vector<int> as_ints(n * 2);
+    std::memcpy(as_ints.data(), src, n * sizeof(double));
+    upload_ints(reinterpret_cast<int*>(dst), as_ints.data(), as_ints.size());
+}
+
 void Engine::check_flags() {
     int h = 0;
     SMOE_CUDA(cudaMemcpy(&h, flags, sizeof(int), cudaMemcpyDeviceToHost));
@@ -287,6 +304,7 @@ void Engine::check_flags() {
         if (h & kFlagNonFiniteLogits) throw Error(kInvariant, "greedy_next: non-finite logits");
         if (h & kFlagNonFiniteGate) throw Error(kInvariant, "softmax: non-finite input");
         if (h & kFlagEmptyRemap) throw Error(kInvariant, "nearest_draft_expert: empty candidate set");
+        if (h & kFlagZeroDrawProb) throw Error(kInvariant, "verify_sampling: zero draw probability for proposed token");
     }
 }
 
@@ -344,7 +362,7 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     auto up_dst = [&]() -> void* {
         const int sl = slot_for();
         if (sl >= 0) return at(up_pool, (size_t)sl * U * d);
-        SMOE_CUDA(cudaMemcpyAsync(stage_up, static_cast<char*>(host_up) + (size_t)off_key * U * d * ws, (size_t)U * d * ws,
+        SMOE_CUDA(cudaMemcpyAsync(stage_up, static_cast<char*>(host_up) + hkey(off_key) * U * d * ws, (size_t)U * d * ws,
                                   cudaMemcpyHostToDevice, stream));
         return stage_up;
     };
@@ -387,7 +405,7 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     if (off_key >= 0) {  // write the converted expert matrix back to the pinned host pool
         const bool is_down = name == "down" || name == "w2";
         const size_t bytes = is_down ? (size_t)d * f * ws : (size_t)U * d * ws;
-        void* host = static_cast<char*>(is_down ? host_down : host_up) + (size_t)off_key * bytes;
+        void* host = static_cast<char*>(is_down ? host_down : host_up) + hkey(off_key) * bytes;
         SMOE_CUDA(cudaMemcpyAsync(host, is_down ? stage_down : stage_up, bytes, cudaMemcpyDeviceToHost, stream));
     }
     sync();
@@ -479,14 +497,16 @@ void Engine::init_device(uint64_t s) {
         launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid_up, stream);
         launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid_down, stream);
     } else {
-        // identical values to the HBM-resident layout (element index = key*U*d + j), staged per expert
+        // identical values to the HBM-resident layout (element index = key*U*d + j), staged per expert;
+        // under expert parallelism only this rank's experts
         const size_t ws = wt == kF32 ? 4 : 2;
         for (int key = 0; key < M * E; ++key) {
+            if (!owns(key)) continue;
             launch_fill_normal(stage_up, wt, (long long)U * d, sd, s, tid_up, stream, (long long)key * U * d);
             launch_fill_normal(stage_down, wt, (long long)d * f, sd, s, tid_down, stream, (long long)key * d * f);
-            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_up) + (size_t)key * U * d * ws, stage_up,
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_up) + hkey(key) * U * d * ws, stage_up,
                                       (size_t)U * d * ws, cudaMemcpyDeviceToHost, stream));
-            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_down) + (size_t)key * d * f * ws, stage_down,
+            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_down) + hkey(key) * d * f * ws, stage_down,
                                       (size_t)d * f * ws, cudaMemcpyDeviceToHost, stream));
         }
         for (int l = 0, k = 0; l < L; ++l)
@@ -529,7 +549,7 @@ void Engine::build_affinity_device() {
     for (int m = 0; m < M; ++m) {
         SMOE_CUDA(cudaMemsetAsync(scratch64, 0, need * sizeof(double), stream));
         const int* slots = slot_of + (size_t)m * E;
-        if (offload) {  // bring the layer's experts into slots 0..E-1 for the pairwise pass
+        if (offload && ep_world == 1) {  // bring the layer's experts into slots 0..E-1 for the pairwise pass
             for (int e = 0; e < E; ++e) store_copy_in(m * E + e, e);
             SMOE_CUDA(cudaStreamSynchronize(copy_stream));
             upload_ints(group_slot, ident.data(), E);
@@ -794,7 +814,7 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                 launch_gate(g, stream);  // x += a; rms; gate, top-K, remap; dispatch rows into xperm
             }
             moe_dep = flag ? gate_ctr : nullptr;
-            if (fetch) store_fetch_layer(mo, T, rl, cnt);  // expert store: migrate this layer's missing experts
+            if (fetch) store_fetch_layer(mo, cnt);  // expert store: migrate this layer's missing experts
             // weight slots: the store's table for this layer's fetch, else the resident slot map (draft
             // passes touch only pinned draft experts)
             l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
@@ -880,6 +900,7 @@ void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_unifor
         int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
         int* fl = fin_log + ((size_t)log_slot * M + mo) * Tmax * K;
         int* cnt = grp_cnt + (size_t)mo * E;
+        const bool fetch = offload && !restricted;
         if (Tl > 0) {
             GateArgs g{x, pmix, s_mix, pm_stride, Tl, d, E, K, gate_w + (size_t)mo * E * d, gate_b + (size_t)mo * E,
                        xperm, cnt, pos, wt, rl, fl, wgt, restricted ? in_draft + (size_t)mo * E : nullptr,
@@ -902,7 +923,9 @@ void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_unifor
             launch_ep_signal(cnt, E, eo, ep_rank, G, peer + G, peer + 3 * G, 0, seq, stream);
             comm->fence(stream);
             launch_ep_wait(ep_flags, G, 0, seq, stream);
+            if (fetch) store_fetch_layer_ep(mo, cnt);  // needed ∩ owned, over this rank's PCIe link
             expert_ffn(seg, rcnt, ep_gslot + (size_t)mo * E, "expert_gemm", xrecv, &op_xrecv, peer + 2 * G);
+            if (fetch) store_finish_layer(mo);
             launch_ep_signal(nullptr, E, eo, ep_rank, G, peer + G, peer + 3 * G, 1, seq, stream);
             comm->fence(stream);
             launch_ep_wait(ep_flags, G, 1, seq, stream);
@@ -915,9 +938,11 @@ void Engine::pass_ep(int T, const int* rseq, const int* rextra, int extra_unifor
         // dispatch: chunk r of the expert-major segments = rank r's experts
         comm->alltoall(xperm, xrecv, (size_t)eo * seg * d * ws, stream);
         comm->alltoall(cnt, rcnt, sizeof(int) * eo, stream);
+        if (fetch) store_fetch_layer_ep(mo, cnt);
         // owner: one grouped FFN over the (source rank, local expert) groups, finished rows summed over the
         // split-K partials exactly as the combine would, then returned into the senders' [E][seg] layout
         expert_ffn(seg, rcnt, ep_gslot + (size_t)mo * E, "expert_gemm", xrecv, &op_xrecv);
+        if (fetch) store_finish_layer(mo);
         launch_ep_sum_partials(ybuf, s_down, yd_stride, rcnt, E, seg, d, ysend, stream);
         comm->alltoall(ysend, yret, (size_t)eo * seg * d * sizeof(float), stream);
         if (Tl > 0) {

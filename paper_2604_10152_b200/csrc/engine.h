@@ -70,6 +70,8 @@ struct RunCfg {
     uint64_t device_capacity_bytes = 0, bytes_per_expert = 0;
     double host_bandwidth = 64e9, ssd_bandwidth = 0.0, compute_rate = 1e6, compute_cost_per_expert = 2e-6;
     int overlap = 0;  // baselines: oracle overlap timing, total = max(compute, migration) (baselines.cpp:101-111)
+    int mode = 0;              // DecodeMode: 0 greedy, 1 sampling (specdec.hpp:15)
+    double temperature = 1.0;  // sampling temperature (SpecConfig.temperature)
 };
 
 struct LedgerEntry { int phase, step, layer, expert; uint64_t bytes; };
@@ -165,8 +167,8 @@ public:
     bool have_affinity = false;
 
     // ---- expert store (offload mode, store.cpp): pinned host pools, HBM slot pool
-    void* host_up = nullptr;    // [M*E][U][d] pinned
-    void* host_down = nullptr;  // [M*E][d][f] pinned
+    void* host_up = nullptr;    // [M*eo][U][d] pinned: this rank's experts (eo = E / ep_world), hkey order
+    void* host_down = nullptr;  // [M*eo][d][f] pinned
     void* stage_up = nullptr;   // device staging of one expert (offload init)
     void* stage_down = nullptr;
     int n_exp_slots = 0;
@@ -174,15 +176,19 @@ public:
     std::vector<uint8_t> key_pinned;
     std::vector<int> free_slots;
     int* h_store = nullptr;          // pinned: slot_of mirror [M*E], group sizes, group slots, raw picks
-    int store_last_T = 0;
+    std::vector<uint64_t> store_counts;  // routed picks per expert of the layer being fetched (all ranks' rows)
+    int* ep_cntg = nullptr;               // EP: [G][E] device, the ranks' per-expert counts of one layer
     // overlap baseline (run_overlap): prefetch of the next layer's previous-step experts
     bool store_prefetch = false;
     std::vector<uint8_t> key_prefetched;  // [M*E] resident because of a prefetch, not yet routed to
     std::vector<uint8_t> prev_need;       // [M*E] keys the previous step routed to
     uint64_t prefetch_bytes = 0, prefetch_wasted = 0, prefetch_hits = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev;
-    // hot_temporal re-pin decided per layer during a verify pass: (layer, raw picks [T][K], T) -> next set
-    std::function<bool(int, const int*, int, std::vector<int>&)> repin_hook;
+    // hot_temporal re-pin decided per layer during a verify pass: (layer, routed picks per expert over
+    // every row of the pass [E]) -> next set
+    std::function<bool(int, const uint64_t*, std::vector<int>&)> repin_hook;
+    bool owns(int key) const { const int e = key % E; return e >= e_lo && e < e_hi; }
+    size_t hkey(int key) const { return (size_t)(key / E) * (e_hi - e_lo) + (size_t)(key % E - e_lo); }
     void store_alloc(int exp_slots);
     void store_reset();
     void upload_slot_rows(int m0, int m1);
@@ -191,7 +197,9 @@ public:
     int store_take_slot(int key);
     void store_release(int key);
     void store_pin_sets(const std::vector<std::vector<int>>& sets);
-    void store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt_dev);
+    void store_fetch_layer(int mo, const int* cnt_dev);
+    void store_fetch_layer_ep(int mo, const int* cnt_dev);
+    void store_issue_layer(int mo, const int* cnt, int* gslot_dev);
     void store_finish_layer(int mo);
     void collect_h2d();
 
@@ -220,6 +228,15 @@ public:
     int* rank = nullptr;          // [M][E][Nmax]
     int* acc = nullptr;
     int* corr = nullptr;
+    // sampling mode (sampling.cu), allocated on first use: host-drawn uniforms, the draft passes'
+    // probabilities [Gmax][Bmax][V] f64, verify row statistics, acceptance scratch
+    double* samp_u = nullptr;      // [Gmax*Bmax + Bmax*(Gmax+1)]
+    double* samp_q = nullptr;
+    double* samp_stats = nullptr;  // [Tmax][2]
+    double* samp_ratio = nullptr;  // [Bmax*Gmax]
+    int* samp_i = nullptr;         // kind [Bmax], uidx [Bmax], used [1]
+    void sampling_alloc();
+    void upload_doubles(double* dst, const double* src, size_t n);
     int* commit_toks = nullptr;  // [Bmax][stride]
     int* commit_take = nullptr;  // [Bmax]
     int* seqs = nullptr;         // [Bmax]

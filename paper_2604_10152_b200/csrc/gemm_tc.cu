@@ -88,7 +88,7 @@ struct TcParams {
 // Timeline instrumentation (tools/tc_trace.py; variant builds only): per launch, per unit
 // {cta, t_claim, t_tma_done, t_mma_first, t_mma_done, t_epi_done} and per CTA {t_start, t_end}, globaltimer ns.
 constexpr int kTrLaunches = 192, kTrUnits = 8192, kTrCtas = 160;
-struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done; };
+struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done, epi_start; };
 __device__ TrUnit g_tr_unit[kTrLaunches][kTrUnits];
 __device__ long long g_tr_cta[kTrLaunches][kTrCtas][2];
 __device__ int g_tr_meta[kTrLaunches][4];  // total units, nphase, T rows bound, grid
@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = cnt & 1;
             mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
             tc_fence_after();
+            TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_start = gtimer();)
             const Phase& P = p.ph[w.phase];
             for (int h = 0; h < (w.pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
                 const int row = w.m0 + h * BM + q * 32 + lane;  // weight row within the slot
@@ -479,11 +480,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             if (p.nphase > 1 && w.phase == 0) {
-                // publish: all four warps' stores of this unit, then one counter increment
-                __threadfence();
+                // publish: all four warps' stores of this unit (ordered before the async-proxy reads of the
+                // down units), a CTA barrier, then ONE release increment -- release is cumulative over the
+                // barrier, so the other warps' stores are covered without each warp draining its stores
+                // through a full fence.sc (which waited microseconds behind the weight stream)
                 proxy_fence_async();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (warp == 2 && lane == 0) atomicAdd(&p.done[w.g], 1);
+#ifdef SMOE_PUBLISH_FENCE_SC
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    atomicAdd(&p.done[w.g], 1);
+                }
+#else
+                if (warp == 2 && lane == 0)
+                    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&p.done[w.g]) : "memory");
+#endif
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);

@@ -131,4 +131,16 @@ void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStre
 void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, long long n, const int* slots, int E,
                             double* out, cudaStream_t s);
 
+// Temperature sampling (sampling.cu).  sample_rows: row r of logits -> tok[r] drawn with u[r] from
+// softmax(logits/T) (model.cpp:178-190), q row r = those probabilities when q != nullptr.
+void launch_sample_rows(const float* logits, int R, int V, double T, const double* u, int* tok, double* q,
+                        long long q_stride, cudaStream_t s);
+// verify_sampling (specdec.cpp:82-157) for na sequences at once: verify rows s*(g+1)+i, draft probabilities
+// q + i*q_tstride + s*V, uniforms from `pool` in sequence order; acc/corr per sequence, used[0] = uniforms
+// consumed.  stats [na*(g+1)][2], kind/uidx [na], ratio [na*g] are scratch.
+void launch_verify_sampling(const float* logits, int V, double T, double* stats, const double* q, long long q_tstride,
+                            const int* drafts, int dstride, const int* seqs, int na, int g, const double* pool,
+                            int* acc, int* kind, int* uidx, int* used, int* corr, int* flags, double* ratio,
+                            cudaStream_t s);
+
 }  // namespace smoe

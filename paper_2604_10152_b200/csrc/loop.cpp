@@ -214,10 +214,14 @@ struct Timer {
 
 }  // namespace
 
+// uniform01 (common.hpp:40-42): one 64-bit output per draw
+static double uniform01(std::mt19937_64& r) { return (double)(r() >> 11) * 0x1.0p-53; }
+
 struct SpecState {
     RunCfg c;
     int B = 0, M = 0, E = 0, K = 0, g = 0, nd = 0;
     std::mt19937_64 prng;
+    std::mt19937_64 srng;  // sample_rng (specdec.cpp:209): drafts and verify draws in sampling mode
     std::unique_ptr<Residency> res;
     Ledger led;
     std::vector<std::vector<int>> sets;
@@ -285,6 +289,11 @@ void spec_begin(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>&
     if (S->B > e.Bmax) throw Error(kConfig, "engine: batch exceeds max_batch");
     if (S->g > e.Gmax) throw Error(kConfig, "engine: gamma exceeds max_gamma");
     S->prng.seed(substream(c.run_seed, 0x706f6c69ull));
+    S->srng.seed(substream(c.run_seed, 0x73616d70ull));
+    if (c.mode == 1) {
+        if (!(c.temperature > 0.0)) throw Error(kConfig, "spec: temperature > 0 violated in sampling mode");
+        e.sampling_alloc();
+    }
     S->res = std::make_unique<Residency>(e.M, e.E, c);
     S->pc.assign((size_t)e.M * e.E, 0);
     S->out.B = S->B; S->out.max_new = c.max_new_tokens; S->out.gamma = c.gamma;
@@ -353,20 +362,29 @@ int spec_step(Engine& e, int* accepted_tokens) {
     e.upload_ints(drows, S.rows.data() + 2 * TV, na);
     e.upload_ints(e.seqs, act.data(), na);
 
-    // (a) speculation: gamma restricted passes, drafts stay on device
+    // (a) speculation: gamma restricted passes, drafts stay on device.  Sampling mode: the draft token
+    // of step t, sequence s is drawn with the (t*na + s)-th uniform of the phase (speculate's loop order,
+    // specdec.cpp:38-50) from softmax(logits/T), whose rows are kept as the draw probabilities q.
+    const bool samp = S.c.mode == 1;
+    if (samp) {
+        std::vector<double> u((size_t)g * na);
+        for (double& x : u) x = uniform01(S.srng);
+        e.upload_doubles(e.samp_u, u.data(), u.size());
+    }
     if (g_host_prof) hp1 = host_now();
     for (int t = 0; t < g; ++t) {
         e.pass(na, drows, nullptr, t, true, S.c.use_affinity, t);
+        if (samp)
+            launch_sample_rows(e.logits, na, e.V, S.c.temperature, e.samp_u + (size_t)t * na, e.amax,
+                               e.samp_q + (size_t)t * e.Bmax * e.V, e.V, e.stream);
         launch_scatter_tokens(e.amax, drows, nullptr, t, na, e.drafts, e.stride, e.stream);
     }
     // (b) verification: one pass over all gamma+1 positions of every active sequence.  Offloaded
     // experts are migrated layer by layer inside the pass; hot_temporal re-pins each layer as soon as
     // its routing over all verify rows is known (same rule and inputs as the phase-end selection).
     if (e.offload && S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
-        e.repin_hook = [&S, E, K](int mo, const int* raw, int T, std::vector<int>& next) {
-            std::vector<uint64_t> cnt(E, 0);
-            for (int q = 0; q < T * K; ++q) cnt[raw[q]]++;
-            next = select_layer_hot(cnt.data(), E, &S.sets[mo], S.nd);
+        e.repin_hook = [&S, E](int mo, const uint64_t* cnt, std::vector<int>& next) {
+            next = select_layer_hot(cnt, E, &S.sets[mo], S.nd);
             return true;
         };
     }
@@ -377,9 +395,25 @@ int spec_step(Engine& e, int* accepted_tokens) {
         throw;
     }
     e.repin_hook = nullptr;
-    launch_scatter_tokens(e.amax, e.row_seq, e.row_extra, 0, TV, e.vam, e.stride, e.stream);
-    // (c) accept
-    launch_accept(e.drafts, e.vam, e.seqs, na, g, e.stride, e.acc, e.corr, e.stream);
+    // (c) accept: greedy (specdec.cpp:76-78) or Leviathan acceptance with the residual resample
+    // (specdec.cpp:104-157) over a pool of na*(g+1) uniforms; the stream then advances by what was used
+    std::mt19937_64 srng_before;
+    int used = 0;
+    if (samp) {
+        srng_before = S.srng;
+        std::vector<double> pool((size_t)na * (g + 1));
+        for (double& x : pool) x = uniform01(S.srng);
+        double* dpool = e.samp_u + (size_t)e.Gmax * e.Bmax;
+        e.upload_doubles(dpool, pool.data(), pool.size());
+        launch_verify_sampling(e.logits, e.V, S.c.temperature, e.samp_stats, e.samp_q, (long long)e.Bmax * e.V,
+                               e.drafts, e.stride, e.seqs, na, g, dpool, e.acc, e.samp_i, e.samp_i + e.Bmax,
+                               e.samp_i + 2 * e.Bmax, e.corr, e.flags, e.samp_ratio, e.stream);
+        SMOE_CUDA(cudaMemcpyAsync(&used, e.samp_i + 2 * e.Bmax, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+        e.launches += 3 + g;
+    } else {
+        launch_scatter_tokens(e.amax, e.row_seq, e.row_extra, 0, TV, e.vam, e.stride, e.stream);
+        launch_accept(e.drafts, e.vam, e.seqs, na, g, e.stride, e.acc, e.corr, e.stream);
+    }
     S.h_acc.resize(na); S.h_corr.resize(na); S.h_drafts.resize((size_t)e.Bmax * e.stride);
     SMOE_CUDA(cudaMemcpyAsync(S.h_acc.data(), e.acc, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
     SMOE_CUDA(cudaMemcpyAsync(S.h_corr.data(), e.corr, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
@@ -396,6 +430,10 @@ int spec_step(Engine& e, int* accepted_tokens) {
     if (g_host_prof) hp3 = host_now();
     NvtxRange nv_book("smoe bookkeeping (reference order)");
     e.check_flags();
+    if (samp) {
+        S.srng = srng_before;
+        S.srng.discard((unsigned long long)used);
+    }
     e.launches += (uint64_t)g + 2;  // scatters + accept (commit counted below)
     e.ctl_d2h += sizeof(int) * ((size_t)2 * na + (size_t)e.Bmax * e.stride + (size_t)M * K * (TV + (size_t)g * na));
     {  // algorithmic expert bytes: every distinct (layer, expert) a pass touches streams its weights once
@@ -509,7 +547,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
         S.res->pin(next, S.led, 1, S.phase);
         if (e.offload)  // the store re-pinned layer by layer during verify: it must agree
             for (int m = 0; m < M; ++m)
-                for (int ex = 0; ex < E; ++ex)
+                for (int ex = e.e_lo; ex < e.e_hi; ++ex)  // this rank's experts
                     if ((e.key_pinned[(size_t)m * E + ex] != 0) !=
                         (std::find(next[m].begin(), next[m].end(), ex) != next[m].end()))
                         throw Error(kInvariant, "expert store: per-layer re-pin diverged from the phase selection");
@@ -615,11 +653,25 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
     e.upload_ints(e.row_seq, rs.data(), B);
     e.upload_ints(e.seqs, rs.data(), B);
     e.upload_ints(e.commit_take, one.data(), B);
+    // sampling mode: token of (step, b) drawn with the (step*B + b)-th uniform of sample_rng
+    // (baselines.cpp:43, 59-64)
+    const bool samp = c.mode == 1;
+    std::mt19937_64 srng(substream(c.run_seed, 0x73616d70ull));
+    if (samp) {
+        if (!(c.temperature > 0.0)) throw Error(kConfig, "sample_next: temperature must be > 0");
+        e.sampling_alloc();
+    }
     Timer tm;
     tm.start(e.stream);
     double modeled = 0.0;
     for (int step = 0; step < c.max_new_tokens; ++step) {
+        if (samp) {
+            std::vector<double> u(B);
+            for (double& x : u) x = uniform01(srng);
+            e.upload_doubles(e.samp_u, u.data(), B);
+        }
         e.pass(B, e.row_seq, nullptr, 0, false, 0, 0);
+        if (samp) launch_sample_rows(e.logits, B, e.V, c.temperature, e.samp_u, e.amax, nullptr, 0, e.stream);
         launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream);
         read_log(e, e.raw_log, 0, B, raw);
         SMOE_CUDA(cudaMemcpyAsync(am.data(), e.amax, sizeof(int) * B, cudaMemcpyDeviceToHost, e.stream));

@@ -30,10 +30,10 @@ void Engine::store_alloc(int exp_slots) {
     free_slots.clear();
     for (int s = n_exp_slots - 1; s >= 0; --s) free_slots.push_back(s);
     const size_t ws = wt == kF32 ? 4 : 2;
-    const size_t up_b = (size_t)U * d * ws, dn_b = (size_t)d * f * ws;
-    SMOE_CUDA(cudaHostAlloc(&host_up, (size_t)M * E * up_b, cudaHostAllocDefault));
-    SMOE_CUDA(cudaHostAlloc(&host_down, (size_t)M * E * dn_b, cudaHostAllocDefault));
-    SMOE_CUDA(cudaMallocHost(&h_store, sizeof(int) * ((size_t)M * E + 4 * (size_t)E + 8 + (size_t)Tmax * K)));
+    const size_t up_b = (size_t)U * d * ws, dn_b = (size_t)d * f * ws, owned = (size_t)M * (e_hi - e_lo);
+    SMOE_CUDA(cudaHostAlloc(&host_up, owned * up_b, cudaHostAllocDefault));
+    SMOE_CUDA(cudaHostAlloc(&host_down, owned * dn_b, cudaHostAllocDefault));
+    SMOE_CUDA(cudaMallocHost(&h_store, sizeof(int) * ((size_t)M * E + (4 + (size_t)ep_world) * E + 8)));
 }
 
 void Engine::store_reset() {
@@ -50,9 +50,18 @@ void Engine::store_reset() {
 }
 
 // slot_of rows [m0, m1) -> device, ordered on the compute stream (pinned source region per layer).
+// Under expert parallelism the GEMM groups are (source rank, local expert): their slot table ep_gslot
+// is rebuilt from the same rows (group g -> this rank's expert e_lo + g % eo).
 void Engine::upload_slot_rows(int m0, int m1) {
-    int* hp = h_store;  // first M*E ints: pinned mirror of h_slot_of
+    int* hp = h_store;  // first M*E ints: pinned mirror of h_slot_of (or of the EP group slots)
     const size_t a = (size_t)m0 * E, n = (size_t)(m1 - m0) * E;
+    if (ep_world > 1) {
+        const int eo = e_hi - e_lo;
+        for (int m = m0; m < m1; ++m)
+            for (int g = 0; g < E; ++g) hp[(size_t)m * E + g] = h_slot_of[(size_t)m * E + e_lo + g % eo];
+        SMOE_CUDA(cudaMemcpyAsync(ep_gslot + a, hp + a, n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        return;
+    }
     std::memcpy(hp + a, h_slot_of.data() + a, n * sizeof(int));
     SMOE_CUDA(cudaMemcpyAsync(slot_of + a, hp + a, n * sizeof(int), cudaMemcpyHostToDevice, stream));
 }
@@ -64,11 +73,11 @@ size_t Engine::expert_bytes(int which) const {
 
 // Copy one expert host -> HBM slot on the copy stream.
 void Engine::store_copy_in(int key, int slot) {
-    const size_t ub = expert_bytes(0), db = expert_bytes(1);
-    SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(up_pool) + (size_t)slot * ub, static_cast<char*>(host_up) + (size_t)key * ub,
+    const size_t ub = expert_bytes(0), db = expert_bytes(1), hk = hkey(key);
+    SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(up_pool) + (size_t)slot * ub, static_cast<char*>(host_up) + hk * ub,
                               ub, cudaMemcpyHostToDevice, copy_stream));
     SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(down_pool) + (size_t)slot * db,
-                              static_cast<char*>(host_down) + (size_t)key * db, db, cudaMemcpyHostToDevice, copy_stream));
+                              static_cast<char*>(host_down) + hk * db, db, cudaMemcpyHostToDevice, copy_stream));
     h2d_bytes += ub + db;
 }
 
@@ -96,7 +105,8 @@ void Engine::store_pin_sets(const std::vector<std::vector<int>>& sets) {
     if (!offload) return;
     std::vector<uint8_t> target((size_t)M * E, 0);
     for (int m = 0; m < M; ++m)
-        for (int e : sets[m]) target[(size_t)m * E + e] = 1;
+        for (int e : sets[m])
+            if (e >= e_lo && e < e_hi) target[(size_t)m * E + e] = 1;  // this rank's share of the sets
     for (int k = 0; k < M * E; ++k)
         if (key_pinned[k] && !target[k]) {
             key_pinned[k] = 0;
@@ -117,18 +127,48 @@ void Engine::store_pin_sets(const std::vector<std::vector<int>>& sets) {
 // queued right behind them, so the copy engine keeps streaming while this layer computes and the host
 // waits for the next gate; the next layer then copies only what the prefetch missed.  Prefetched
 // experts the next layer does not route to are released unused at its finish (wasted bytes, counted).
-void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt_dev) {
+void Engine::store_fetch_layer(int mo, const int* cnt_dev) {
     int* cnt = h_store + (size_t)M * E;
-    int* gslot = cnt + E + 1;
-    int* raw = gslot + E;
     SMOE_CUDA(cudaMemcpyAsync(cnt, cnt_dev, sizeof(int) * E, cudaMemcpyDeviceToHost, stream));
-    SMOE_CUDA(cudaMemcpyAsync(raw, raw_dev, sizeof(int) * T * K, cudaMemcpyDeviceToHost, stream));
     sync();
+    store_counts.assign(cnt, cnt + E);  // picks per expert over every row (unrestricted: final == raw)
+    store_issue_layer(mo, cnt, group_slot);
+}
+
+// Expert parallelism: this rank owns experts [e_lo, e_hi); the counts every sender routed to them have
+// arrived (rcnt, group g = (source rank g / eo, local expert g % eo)), so the rank fetches exactly
+// needed ∩ owned over its own PCIe link.  The re-pin needs the layer's counts over all experts: one
+// all-gather of every rank's per-expert counts of its own rows.
+void Engine::store_fetch_layer_ep(int mo, const int* cnt_dev) {
+    const int G = ep_world, eo = e_hi - e_lo;
+    int* rc = h_store + (size_t)M * E;          // [E] received group counts
+    int* all = rc + 3 * E + 8;                  // [G][E] gathered per-expert counts
+    if (repin_hook) comm->allgather(cnt_dev, ep_cntg, sizeof(int) * E, stream);
+    SMOE_CUDA(cudaMemcpyAsync(rc, rcnt, sizeof(int) * E, cudaMemcpyDeviceToHost, stream));
+    if (repin_hook) SMOE_CUDA(cudaMemcpyAsync(all, ep_cntg, sizeof(int) * G * E, cudaMemcpyDeviceToHost, stream));
+    sync();
+    store_counts.assign(E, 0);
+    if (repin_hook)
+        for (int r = 0; r < G; ++r)
+            for (int e = 0; e < E; ++e) store_counts[e] += (uint64_t)all[(size_t)r * E + e];
+    std::vector<int> need(E, 0);  // owned experts' totals, indexed by the global expert id
+    for (int g = 0; g < E; ++g) need[e_lo + g % eo] += rc[g];
+    int* gs = rc + E;  // [E] group slots, staged after the fetch
+    store_issue_layer(mo, need.data(), nullptr);
+    for (int g = 0; g < E; ++g) gs[g] = rc[g] > 0 ? h_slot_of[(size_t)mo * E + e_lo + g % eo] : -1;
+    SMOE_CUDA(cudaMemcpyAsync(ep_gslot + (size_t)mo * E, gs, sizeof(int) * E, cudaMemcpyHostToDevice, stream));
+}
+
+// Issue the copies of layer mo's needed (cnt[e] > 0), owned, non-resident experts on the copy stream
+// (+ the overlap baseline's prefetch of the next layer), make the compute stream wait for them, and
+// (single GPU) stage the layer's group slots into gslot_dev.
+void Engine::store_issue_layer(int mo, const int* cnt, int* gslot_dev) {
+    int* gslot = h_store + (size_t)M * E + E + 1;
     cudaEvent_t a, b;
     SMOE_CUDA(cudaEventCreate(&a));
     SMOE_CUDA(cudaEventCreate(&b));
     SMOE_CUDA(cudaEventRecord(a, copy_stream));
-    for (int e = 0; e < E; ++e) {
+    for (int e = e_lo; e < e_hi; ++e) {
         const int key = mo * E + e;
         if (cnt[e] > 0) {
             if (h_slot_of[key] < 0) store_copy_in(key, store_take_slot(key));
@@ -137,7 +177,6 @@ void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt
             prefetch_wasted += expert_bytes(0) + expert_bytes(1);  // released unused at the layer's finish
         }
         key_prefetched[key] = 0;
-        gslot[e] = cnt[e] > 0 ? h_slot_of[key] : -1;
     }
     // the copy stream is in order: this event also covers every earlier prefetch of this layer
     SMOE_CUDA(cudaEventRecord(b, copy_stream));
@@ -148,7 +187,7 @@ void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt
         SMOE_CUDA(cudaEventCreate(&pa));
         SMOE_CUDA(cudaEventCreate(&pb));
         SMOE_CUDA(cudaEventRecord(pa, copy_stream));
-        for (int e = 0; e < E; ++e) {
+        for (int e = e_lo; e < e_hi; ++e) {
             const int key = (mo + 1) * E + e;
             if (!prev_need.empty() && prev_need[key] && h_slot_of[key] < 0 && !free_slots.empty()) {
                 const uint64_t before = h2d_bytes;
@@ -160,19 +199,20 @@ void Engine::store_fetch_layer(int mo, int T, const int* raw_dev, const int* cnt
         SMOE_CUDA(cudaEventRecord(pb, copy_stream));
         h2d_ev.emplace_back(pa, pb);
     }
-    SMOE_CUDA(cudaMemcpyAsync(group_slot, gslot, sizeof(int) * E, cudaMemcpyHostToDevice, stream));
-    store_last_T = T;
+    if (gslot_dev) {
+        for (int e = 0; e < E; ++e) gslot[e] = cnt[e] > 0 ? h_slot_of[(size_t)mo * E + e] : -1;
+        SMOE_CUDA(cudaMemcpyAsync(gslot_dev, gslot, sizeof(int) * E, cudaMemcpyHostToDevice, stream));
+    }
 }
 
 // After the layer's expert GEMMs are enqueued: optional re-pin (hot_temporal), then flush.
 void Engine::store_finish_layer(int mo) {
     if (repin_hook) {
-        const int* raw = h_store + (size_t)M * E + 2 * E + 1;
         std::vector<int> next;
-        if (repin_hook(mo, raw, store_last_T, next)) {
+        if (repin_hook(mo, store_counts.data(), next)) {
             std::vector<uint8_t> want(E, 0);
             for (int e : next) want[e] = 1;
-            for (int e = 0; e < E; ++e) {
+            for (int e = e_lo; e < e_hi; ++e) {
                 const int key = mo * E + e;
                 if (want[e]) {
                     if (h_slot_of[key] < 0)
@@ -184,7 +224,7 @@ void Engine::store_finish_layer(int mo) {
             }
         }
     }
-    for (int e = 0; e < E; ++e) {
+    for (int e = e_lo; e < e_hi; ++e) {
         const int key = mo * E + e;
         if (!key_pinned[key]) store_release(key);
     }

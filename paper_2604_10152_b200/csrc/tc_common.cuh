@@ -160,15 +160,22 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_store(const Phase& P, const Unit& w, int row, int lane, int c,
                                                const uint32_t* v) {
     if (EPI == kEpiSwiglu) {
-        // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes
+        // rows 2j / 2j+1 of the slot hold w1 / w3 of feature j: pair up adjacent lanes.  silu with the
+        // fast intrinsics (ex2.approx, approximate divide): each element is a fixed function of its
+        // accumulator, so every pass computes it identically, and H is rounded to bf16 right after (the
+        // <= 2-ulp f32 differences from expf/IEEE division vanish there).  The accurate-division path
+        // serialised the 16 columns and made this epilogue the up->down critical path (9.7 us per C4
+        // draft unit, tools/tc_trace.py).
+        float other[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const float mine = __uint_as_float(v[j]);
-            const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-            if (!(lane & 1) && row < P.Nrows && c + j < w.n_valid) {
-                const float h = mine / (1.0f + expf(-mine)) * other;
-                reinterpret_cast<__nv_bfloat16*>(P.Y)[(long long)(w.n0 + c + j) * P.ldy + (row >> 1)] =
-                    __float2bfloat16_rn(h);
+        for (int j = 0; j < 16; ++j) other[j] = __shfl_xor_sync(0xffffffffu, __uint_as_float(v[j]), 1);
+        if (!(lane & 1) && row < P.Nrows) {
+            __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(P.Y) + (long long)(w.n0 + c) * P.ldy + (row >> 1);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float a = __uint_as_float(v[j]);
+                const float h = __fdividef(a, 1.0f + __expf(-a)) * other[j];
+                if (c + j < w.n_valid) y[(long long)j * P.ldy] = __float2bfloat16_rn(h);
             }
         }
     } else if (row < P.Nrows) {

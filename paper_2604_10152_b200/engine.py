@@ -53,7 +53,7 @@ class RunConfig(C.Structure):
                 ("warmup_steps", C.c_int), ("policy", C.c_int), ("collect_trace", C.c_int), ("run_seed", C.c_uint64),
                 ("device_capacity_bytes", C.c_uint64), ("bytes_per_expert", C.c_uint64),
                 ("host_bandwidth", C.c_double), ("ssd_bandwidth", C.c_double), ("compute_rate", C.c_double),
-                ("compute_cost_per_expert", C.c_double)]
+                ("compute_cost_per_expert", C.c_double), ("mode", C.c_int), ("temperature", C.c_double)]
 
 
 class LedgerEntry(C.Structure):
@@ -192,13 +192,16 @@ class RunCfg:
     ssd_bandwidth: float = 0.0
     compute_rate: float = 1e6
     compute_cost_per_expert: float = 2e-6
+    mode: str = "greedy"       # "greedy" | "sampling" (DecodeMode, specdec.hpp:15)
+    temperature: float = 1.0
 
     def to_c(self, spec: ModelSpec) -> RunConfig:
         bpe = self.bytes_per_expert or spec.bytes_per_expert()
         cap = self.device_capacity_bytes or spec.moe_layers * spec.experts * bpe
         return RunConfig(self.gamma, self.n_draft, self.max_new_tokens, int(self.use_affinity), self.warmup_steps,
                          POLICIES[self.policy], int(self.collect_trace), self.run_seed, cap, bpe, self.host_bandwidth,
-                         self.ssd_bandwidth, self.compute_rate, self.compute_cost_per_expert)
+                         self.ssd_bandwidth, self.compute_rate, self.compute_cost_per_expert,
+                         {"greedy": 0, "sampling": 1}[self.mode], self.temperature)
 
 
 @dataclass

@@ -77,6 +77,7 @@ def test_caller_on_tcgen05_path_is_lossless():
     for k in ("specmoe_hot_temporal", "specmoe_random", "specmoe_hot_global", "overlap", "caching"):
         assert got[k]["tokens"] == od, k
     assert got["errors"] == want["errors"]
-    assert got["specmoe_hot_temporal"]["metrics"]["bytes_spec"] == 0
+    m = got["specmoe_hot_temporal"]["metrics"]
+    assert m["bytes_total"] == m["bytes_verify"]  # speculation migrates nothing
     gl, wl = np.asarray(got["forward"]["logits"]), np.asarray(want["forward"]["logits"])
     assert np.max(np.abs(gl - wl)) <= 3e-2 * np.max(np.abs(wl))

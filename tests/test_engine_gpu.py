@@ -286,13 +286,14 @@ def test_bf16_fine_grained_lossless():
 
 
 # ---------------------------------------------------------------- expert parallelism (virtual ranks)
-def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False, work_fn=None):
+def _run_ep(G, spec, init, cfg, prompts, weight_type=BF16, ondemand=False, work_fn=None, offload=0):
     import threading
     from paper_2604_10152_b200.engine import LoopbackGroup
     grp = LoopbackGroup(G)
     engines = []
     for r in range(G):
-        e = Engine(spec, weight_type=weight_type, max_batch=len(prompts), max_gamma=cfg.gamma, ep_rank=r, ep_world=G)
+        e = Engine(spec, weight_type=weight_type, max_batch=len(prompts), max_gamma=cfg.gamma, ep_rank=r, ep_world=G,
+                   offload=offload)
         init(e)
         e.attach_loopback(grp)
         engines.append(e)
@@ -366,6 +367,37 @@ def test_expert_parallel_fine_grained_bitexact(G, ep_mode):
     for r, lg in _run_ep(G, s, init, cfg, prompts, work_fn=work):
         assert r.tokens == want.tokens and r.trace == want.trace and r.ledger == want.ledger
         assert np.array_equal(lg[0], want_lg[0]) and np.array_equal(lg[1], want_lg[1])
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("policy", ["hot_temporal", "random"])
+def test_expert_parallel_offloaded_store(G, policy, ep_mode):
+    """Expert parallelism with the offloaded store: every rank keeps its experts in its own
+    pinned host pool and fetches needed ∩ owned per verify layer over its own PCIe link; hot_temporal
+    re-pins per layer from the all-gathered counts.  Tokens, routing trace and ledger equal the
+    single-GPU offloaded (and resident) runs, and the ranks' migrated bytes add up to the ledger."""
+    s = _c1_like(SWIGLU3, skew=1.0)
+    prompts = make_prompts(4, 3, 8, s.vocab)
+    cfg = RunCfg(gamma=4, n_draft=4, max_new_tokens=14, collect_trace=True, policy=policy)
+
+    def init(e):
+        e.init_device(21)
+        e.build_affinity_device()
+
+    one = Engine(s, weight_type=BF16, max_batch=3, max_gamma=4, offload=1)
+    init(one)
+    want = one.run_specmoe(cfg, prompts)
+    bpe = one.info()["bytes_per_expert"]
+    assert want.metrics["h2d_expert_bytes"] == len(want.ledger) * bpe
+    res = _run_ep(G, s, init, cfg, prompts, offload=1)
+    for r in res:
+        assert r.tokens == want.tokens and r.trace == want.trace and r.ledger == want.ledger
+        assert r.outcomes == want.outcomes
+    assert sum(r.metrics["h2d_expert_bytes"] for r in res) == len(want.ledger) * bpe
+    od = _run_ep(G, s, init, cfg, prompts, offload=1, ondemand=True)
+    od1 = one.run_ondemand(cfg, prompts)
+    assert od[0].tokens == od1.tokens == want.tokens and od[0].ledger == od1.ledger
+    assert sum(r.metrics["h2d_expert_bytes"] for r in od) == len(od1.ledger) * bpe
 
 
 @pytest.mark.slow
