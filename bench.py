@@ -353,7 +353,7 @@ def spec_measure(eng, stream, cfg, prompts, steps: int, warmup: int, profile: bo
                                                      "expert_flops:draft", "expert_flops:verify")}
         eng.counters(reset=True)
         out["prof"] = {c: eng.profile_read(c) for c in (
-            "expert_gemm", "expert_gemm:draft", "expert_gemm:verify", "dense_gemm", "head_gemm", "pass", "gate",
+            "expert_gemm", "expert_gemm:draft", "expert_gemm:verify", "dense_gemm", "head_gemm", "gate",
             "combine")}
     res = eng.spec_end()
     out["tau"] = res.metrics["tau_mean"]
@@ -533,29 +533,19 @@ def run_b200(a) -> None:
             dist.barrier()
             dist.destroy_process_group()
         return
-    pas = m["prof"]["pass"]
-    if pas["launches"] > 0:
-        # persistent pass kernel (every layer of a pass in one launch): its algorithmic bytes are the
-        # touched expert weights plus the Mix (and dense-FFN) weights of every pass; the head GEMM is a
-        # separate launch
-        head = m["prof"]["head_gemm"]
-        head_bytes = float(head["launches"]) * spec.vocab * spec.hidden * 2
-        alg_bytes = m["cnt_prof"]["alg_expert_bytes"] + m["cnt_prof"]["alg_dense_bytes"] - head_bytes
-        dom = pas
-        roof_kernel = "k_pass_tc (persistent pass kernel; tcgen05/TMEM/TMA)"
-        roof_alg = "per pass: distinct (layer, expert) touched x 3*d*f*2 B + L*d*d*2 B Mix weights (bf16)"
-        traffic, traffic_src = None, "no capture for the pass kernel in this round"
-    else:
-        dom = m["prof"]["expert_gemm"]
-        alg_bytes = m["cnt_prof"]["alg_expert_bytes"]
-        roof_kernel = "k_gemm_tc<SwiGLU, StoreF32> (fused MoE up+down: tcgen05 grouped expert GEMM)"
-        roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
-        traffic = ncu_traffic(a.gamma) if a.shape == "c2" and a.batch == 64 and a.gamma == 4 else None
-        traffic_src = ("ncu --set full, profiles/r02_ncu_fused_moe.json: dram read+write of one draft-pass and one "
+    # the fused MoE launch (k_gemm_tc<SwiGLU, StoreF32>) dominates the step
+    dom = m["prof"]["expert_gemm"]
+    alg_bytes = m["cnt_prof"]["alg_expert_bytes"]
+    roof_kernel = "k_gemm_tc<SwiGLU, StoreF32> (fused MoE up+down: tcgen05 grouped expert GEMM)"
+    roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
+    traffic, traffic_src = None, "no committed capture for this configuration"
+    if a.shape == "c2" and a.batch == 64 and a.gamma == 4:
+        traffic = ncu_traffic(a.gamma, "r03_ncu_fused_moe.json")
+        traffic_src = ("ncu --set full, profiles/r03_ncu_fused_moe.json: dram read+write of one draft-pass and one "
                        "verify-pass launch, weighted gamma:1 like the step (committed capture of this kernel)")
-        if a.shape == "c4":
-            traffic = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
-            traffic_src = "ncu --set full, profiles/r03_ncu_c4_moe.json (committed capture), weighted gamma:1"
+    elif a.shape == "c4" and a.batch == 32 and a.gamma == 4:
+        traffic = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
+        traffic_src = "ncu --set full, profiles/r03_ncu_c4_moe.json (committed capture), weighted gamma:1"
     achieved = alg_bytes / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
     ep_mode = os.environ.get("SMOE_EP_MODE", "p2p")
     exch = ("gate/down-projection epilogues store rows into peer memory over NVLink (fused dispatch/combine)"

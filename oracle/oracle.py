@@ -33,7 +33,8 @@ PHASES = {0: "speculation", 1: "verification", 2: "baseline-step"}
 class OmSpec(C.Structure):
     _fields_ = [("num_layers", C.c_int), ("experts", C.c_int), ("top_k", C.c_int), ("hidden", C.c_int),
                 ("ffn", C.c_int), ("vocab", C.c_int), ("gate_skew", C.c_double), ("seed", C.c_uint64),
-                ("moe_mask", C.POINTER(C.c_uint8)), ("expert_kind", C.c_int)]
+                ("moe_mask", C.POINTER(C.c_uint8)), ("expert_kind", C.c_int), ("attn_heads", C.c_int),
+                ("kv_heads", C.c_int), ("head_dim", C.c_int), ("rope_theta", C.c_double)]
 
 
 class OmRunCfg(C.Structure):
@@ -88,6 +89,10 @@ class ModelSpec:
     seed: int = 0
     moe_mask: list | None = None
     expert_kind: int = 0  # 0 tanh2, 1 swiglu3
+    attn_heads: int = 0   # > 0: real GQA attention with RoPE instead of the prefix-mean surrogate (port only)
+    kv_heads: int = 0
+    head_dim: int = 0
+    rope_theta: float = 10000.0
 
     @property
     def moe_layers(self) -> int:
@@ -185,7 +190,8 @@ class Oracle:
         if spec.moe_mask is not None:
             mask = (C.c_uint8 * spec.num_layers)(*[1 if m else 0 for m in spec.moe_mask])
         s = OmSpec(spec.num_layers, spec.experts, spec.top_k, spec.hidden, spec.ffn, spec.vocab, spec.gate_skew,
-                   spec.seed, C.cast(mask, C.POINTER(C.c_uint8)) if mask is not None else None, spec.expert_kind)
+                   spec.seed, C.cast(mask, C.POINTER(C.c_uint8)) if mask is not None else None, spec.expert_kind,
+                   spec.attn_heads, spec.kv_heads, spec.head_dim, spec.rope_theta)
         err = C.create_string_buffer(256)
         h = self.lib.om_build_model(C.byref(s), err, 256)
         if not h:

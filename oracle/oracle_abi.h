@@ -27,6 +27,11 @@ typedef struct {
     uint64_t seed;
     const uint8_t* moe_mask; /* num_layers entries, or NULL = every layer MoE */
     int expert_kind;         /* 0 = tanh2 (reference), 1 = swiglu3 (port only) */
+    /* Port-only extension: real GQA attention with RoPE replaces the reference's
+     * prefix-mean + mix surrogate when attn_heads > 0 (x0 = embedding of the token at each position;
+     * per layer x += Wo attn(RoPE(Wq rms x), RoPE(Wk rms x), Wv rms x)).  The reference rejects it. */
+    int attn_heads, kv_heads, head_dim;
+    double rope_theta;
 } om_spec;
 
 /* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy + seed. */

@@ -112,6 +112,7 @@ extern "C" {
 void* om_build_model(const om_spec* s, char* err, int errlen) {
     try {
         if (s->expert_kind != 0) throw ConfigError("reference supports only the tanh2 expert");
+        if (s->attn_heads > 0) throw ConfigError("reference has no attention (prefix-mean surrogate only)");
         ModelSpec spec;
         spec.num_layers = s->num_layers;
         if (s->moe_mask) spec.moe_layer_mask.assign(s->moe_mask, s->moe_mask + s->num_layers);

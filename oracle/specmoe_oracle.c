@@ -121,11 +121,14 @@ typedef struct {
 typedef struct {
     int is_moe;
     double *mix, *gate, *bias; /* mix d*d, gate d*E, bias E */
+    double *wq, *wk, *wv, *wo; /* attention: [Hq*hd][d], [Hkv*hd][d] x2, [d][Hq*hd] (y = W x) */
     oexpert* experts;          /* E */
     oexpert ffn;
 } olayer;
 typedef struct {
     int L, E, K, d, f, V, M, kind;
+    int Hq, Hkv, hd; /* attention extension (Hq = 0: the reference's surrogate) */
+    double theta;
     double skew;
     uint64_t seed;
     uint8_t* mask;
@@ -149,6 +152,7 @@ static void free_model(omodel* m) {
         for (int l = 0; l < m->L; ++l) {
             olayer* ly = &m->layers[l];
             free(ly->mix); free(ly->gate); free(ly->bias);
+            free(ly->wq); free(ly->wk); free(ly->wv); free(ly->wo);
             if (ly->experts)
                 for (int e = 0; e < m->E; ++e) { free(ly->experts[e].up); free(ly->experts[e].down); free(ly->experts[e].w3); }
             free(ly->experts);
@@ -178,6 +182,9 @@ void* om_build_model(const om_spec* sp, char* err, int errlen) { /* model.cpp:10
     else if (sp->ffn < 1) bad = "model: ffn_dim >= 1 violated";
     else if (sp->num_layers < 1) bad = "model: num_layers >= 1 violated";
     else if (sp->gate_skew < 0.0) bad = "model: gate_skew >= 0 violated";
+    else if (sp->attn_heads > 0 && (sp->kv_heads < 1 || sp->attn_heads % sp->kv_heads || sp->head_dim < 2 ||
+                                    sp->head_dim % 2 || sp->rope_theta <= 0.0))
+        bad = "model: attention needs kv_heads | attn_heads, an even head_dim and rope_theta > 0";
     int any = 0;
     if (!bad) {
         for (int l = 0; l < sp->num_layers; ++l) any |= sp->moe_mask ? sp->moe_mask[l] != 0 : 1;
@@ -190,6 +197,7 @@ void* om_build_model(const om_spec* sp, char* err, int errlen) { /* model.cpp:10
     omodel* m = (omodel*)calloc(1, sizeof(omodel));
     m->L = sp->num_layers; m->E = sp->experts; m->K = sp->top_k; m->d = sp->hidden; m->f = sp->ffn;
     m->V = sp->vocab; m->skew = sp->gate_skew; m->seed = sp->seed; m->kind = sp->expert_kind;
+    m->Hq = sp->attn_heads; m->Hkv = sp->kv_heads; m->hd = sp->head_dim; m->theta = sp->rope_theta;
     m->mask = (uint8_t*)malloc(m->L);
     m->moe_index = (int*)malloc(sizeof(int) * m->L);
     m->M = 0;
@@ -206,7 +214,15 @@ void* om_build_model(const om_spec* sp, char* err, int errlen) { /* model.cpp:10
     for (int l = 0; l < m->L; ++l) {
         olayer* ly = &m->layers[l];
         ly->is_moe = m->mask[l];
-        ly->mix = gfill((size_t)d * d, sd, r);
+        if (m->Hq > 0) { /* extension: the attention weights take the mix's place in the draw order */
+            const size_t qd = (size_t)m->Hq * m->hd, kd = (size_t)m->Hkv * m->hd;
+            ly->wq = gfill(qd * d, sd, r);
+            ly->wk = gfill(kd * d, sd, r);
+            ly->wv = gfill(kd * d, sd, r);
+            ly->wo = gfill((size_t)d * qd, sd, r);
+        } else {
+            ly->mix = gfill((size_t)d * d, sd, r);
+        }
         if (ly->is_moe) {
             ly->gate = gfill((size_t)d * E, sd, r);
             ly->bias = (double*)malloc(sizeof(double) * E);
@@ -234,7 +250,11 @@ long long om_get_tensor(void* model, const char* name, int layer, int expert, do
     else {
         if (layer < 0 || layer >= m->L) return -1;
         olayer* ly = &m->layers[layer];
-        if (!strcmp(name, "mix")) { src = ly->mix; n = d * d; }
+        if (!strcmp(name, "mix")) { src = ly->mix; n = ly->mix ? d * d : 0; }
+        else if (!strcmp(name, "wq")) { src = ly->wq; n = (long long)m->Hq * m->hd * d; }
+        else if (!strcmp(name, "wk")) { src = ly->wk; n = (long long)m->Hkv * m->hd * d; }
+        else if (!strcmp(name, "wv")) { src = ly->wv; n = (long long)m->Hkv * m->hd * d; }
+        else if (!strcmp(name, "wo")) { src = ly->wo; n = (long long)m->Hq * m->hd * d; }
         else if (!strcmp(name, "gate")) { src = ly->gate; n = ly->is_moe ? d * E : 0; }
         else if (!strcmp(name, "gate_bias")) { src = ly->bias; n = ly->is_moe ? E : 0; }
         else {
@@ -371,6 +391,93 @@ typedef struct { double* dist; int E, M; } oaff; /* drafting.hpp:14-19 */
 
 /* model.cpp:192-263.  restricted: [M*nd] or NULL. */
 static __thread double* g_gate_dump;  /* om_forward_gates: per-layer gate logits destination */
+static __thread int g_committed;      /* attention extension: committed prefix length of a draft forward */
+
+/* The MoE half of a layer (model.cpp:226-258): xf = rms(x); x += sum_k p[raw_k] expert_final_k(xf). */
+static void moe_half(const omodel* m, const olayer* ly, int mo, double* x, int plen, const int* restricted, int nd,
+                     const oaff* aff, int* raw_out, int* fin_out);
+
+/* Real-attention extension (no reference counterpart): positions 0..n-1 are run in order,
+ * each attending causally to every earlier position's K/V of the same layer.  Positions < nc-1 (the
+ * committed prefix except its last token) use the target model; with draft sets, positions >= nc-1 use
+ * the restricted model (their K/V are the draft model's) -- the engine's KV cache after a phase's draft
+ * passes.  Without draft sets every position is the target's.  RoPE: rotate-half, angle = p * theta^(-2j/hd).
+ * Routing outputs and logits are those of the last position. */
+static void fwd_attn(const omodel* m, const int* prefix, int n, const int* restricted, int nd, const oaff* aff,
+                     int nc, double* logits, int* raw_out, int* fin_out) {
+    const int d = m->d, Hq = m->Hq, Hkv = m->Hkv, hd = m->hd, G = Hq / Hkv;
+    const size_t qd = (size_t)Hq * hd, kd = (size_t)Hkv * hd;
+    blk* mark = g_arena;
+    double* kc = (double*)amalloc(sizeof(double) * (size_t)m->L * n * kd); /* [L][n][kd] */
+    double* vc = (double*)amalloc(sizeof(double) * (size_t)m->L * n * kd);
+    double* x = (double*)amalloc(sizeof(double) * d);
+    double* xn = (double*)amalloc(sizeof(double) * d);
+    double* q = (double*)amalloc(sizeof(double) * qd);
+    double* o = (double*)amalloc(sizeof(double) * qd);
+    double* a = (double*)amalloc(sizeof(double) * d);
+    double* sc = (double*)amalloc(sizeof(double) * n);
+    const double inv_sqrt = 1.0 / sqrt((double)hd);
+    for (int p = 0; p < n; ++p) {
+        const int last = p == n - 1;
+        const int draft = restricted && p >= nc - 1;
+        const double* e = m->emb + (size_t)prefix[p] * d;
+        for (int j = 0; j < d; ++j) x[j] = e[j];
+        int mo = 0;
+        for (int l = 0; l < m->L; ++l) {
+            const olayer* ly = &m->layers[l];
+            double* kp = kc + ((size_t)l * n + p) * kd;
+            double* vp = vc + ((size_t)l * n + p) * kd;
+            rms(x, d, xn);
+            mv(ly->wq, xn, (int)qd, d, q);
+            mv(ly->wk, xn, (int)kd, d, kp);
+            mv(ly->wv, xn, (int)kd, d, vp);
+            for (int h = 0; h < Hq + Hkv; ++h) { /* RoPE on every query and key head */
+                double* v = h < Hq ? q + (size_t)h * hd : kp + (size_t)(h - Hq) * hd;
+                for (int j = 0; j < hd / 2; ++j) {
+                    const double ang = (double)p * pow(m->theta, -2.0 * j / hd);
+                    const double c = cos(ang), s = sin(ang), x0 = v[j], x1 = v[j + hd / 2];
+                    v[j] = x0 * c - x1 * s;
+                    v[j + hd / 2] = x1 * c + x0 * s;
+                }
+            }
+            for (int h = 0; h < Hq; ++h) { /* softmax(q k^T / sqrt(hd)) v over positions 0..p */
+                const double* qh = q + (size_t)h * hd;
+                const int kh = h / G;
+                double mx = -INFINITY;
+                for (int t = 0; t <= p; ++t) {
+                    const double* kt = kc + ((size_t)l * n + t) * kd + (size_t)kh * hd;
+                    double s = 0.0;
+                    for (int j = 0; j < hd; ++j) s += qh[j] * kt[j];
+                    sc[t] = s * inv_sqrt;
+                    if (sc[t] > mx) mx = sc[t];
+                }
+                double sum = 0.0;
+                for (int t = 0; t <= p; ++t) { sc[t] = exp(sc[t] - mx); sum += sc[t]; }
+                double* oh = o + (size_t)h * hd;
+                for (int j = 0; j < hd; ++j) oh[j] = 0.0;
+                for (int t = 0; t <= p; ++t) {
+                    const double* vt = vc + ((size_t)l * n + t) * kd + (size_t)kh * hd;
+                    const double w = sc[t] / sum;
+                    for (int j = 0; j < hd; ++j) oh[j] += w * vt[j];
+                }
+            }
+            mv(ly->wo, o, d, (int)qd, a);
+            for (int j = 0; j < d; ++j) x[j] += a[j];
+            if (ly->is_moe) {
+                moe_half(m, ly, mo, x, p + 1, draft ? restricted : NULL, nd, aff, last ? raw_out : NULL,
+                         last ? fin_out : NULL);
+                ++mo;
+            } else {
+                moe_half(m, ly, -1, x, p + 1, NULL, 0, NULL, NULL, NULL);
+            }
+        }
+        if (last) {
+            rms(x, d, xn);
+            mtv(m->head, xn, d, m->V, logits);
+        }
+    }
+    arena_release(mark);
+}
 
 static void fwd(const omodel* m, const int* prefix, int n, const int* restricted, int nd, const oaff* aff,
                 double* logits, int* raw_out, int* fin_out) {
@@ -379,6 +486,10 @@ static void fwd(const omodel* m, const int* prefix, int n, const int* restricted
     for (int i = 0; i < n; ++i)
         if (prefix[i] < 0 || prefix[i] >= m->V) fail(2, "forward: token out of range");
     if (restricted && nd < K) fail(2, "forward: restricted set smaller than top_k");
+    if (m->Hq > 0) {
+        fwd_attn(m, prefix, n, restricted, nd, aff, g_committed > 0 ? g_committed : n, logits, raw_out, fin_out);
+        return;
+    }
     blk* mark = g_arena;
     double* x = (double*)amalloc(sizeof(double) * d);
     double* xn = (double*)amalloc(sizeof(double) * d);
@@ -432,9 +543,49 @@ static void fwd(const omodel* m, const int* prefix, int n, const int* restricted
     arena_release(mark);
 }
 
+static void moe_half(const omodel* m, const olayer* ly, int mo, double* x, int plen, const int* restricted, int nd,
+                     const oaff* aff, int* raw_out, int* fin_out) {
+    const int d = m->d, E = m->E, K = m->K;
+    blk* mark = g_arena;
+    double* xn = (double*)amalloc(sizeof(double) * d);
+    double* y = (double*)amalloc(sizeof(double) * d);
+    double* eo = (double*)amalloc(sizeof(double) * d);
+    double* gl = (double*)amalloc(sizeof(double) * E);
+    double* pr = (double*)amalloc(sizeof(double) * E);
+    int* raw = (int*)amalloc(sizeof(int) * K);
+    int* chosen = (int*)amalloc(sizeof(int) * K);
+    rms(x, d, xn);
+    for (int j = 0; j < d; ++j) y[j] = 0.0;
+    if (mo >= 0) {
+        mtv(ly->gate, xn, d, E, gl);
+        for (int e = 0; e < E; ++e) gl[e] += ly->bias[e];
+        if (g_gate_dump && raw_out) memcpy(g_gate_dump + (size_t)mo * E, gl, sizeof(double) * E);
+        softmax_(gl, E, pr);
+        topk_(gl, E, K, raw);
+        for (int k = 0; k < K; ++k) {
+            int pick = raw[k], ex = pick;
+            if (restricted) {
+                const int* ds = restricted + (size_t)mo * nd;
+                ex = aff ? nearest_(aff->dist + (size_t)mo * E * E, E, pick, ds, nd, chosen, k)
+                         : surrogate_(mo, pick, (size_t)plen, ds, nd, chosen, k);
+            }
+            chosen[k] = ex;
+            expert_fwd(m, &ly->experts[ex], xn, eo);
+            for (int j = 0; j < d; ++j) y[j] += pr[pick] * eo[j];
+        }
+        if (raw_out) memcpy(raw_out + (size_t)mo * K, raw, sizeof(int) * K);
+        if (fin_out) memcpy(fin_out + (size_t)mo * K, chosen, sizeof(int) * K);
+    } else {
+        expert_fwd(m, &ly->ffn, xn, y);
+    }
+    for (int j = 0; j < d; ++j) x[j] += y[j];
+    arena_release(mark);
+}
+
 int om_forward(void* model, const int* prefix, int n, const int* restricted, int nd, void* aff, double* logits,
                int* raw_out, int* final_out, char* err, int errlen) {
     ENTER(err, errlen, g_code);
+    g_committed = 0;
     fwd((omodel*)model, prefix, n, restricted, nd, (oaff*)aff, logits, raw_out, final_out);
     LEAVE();
     return 0;
@@ -795,7 +946,9 @@ static om_result* run_spec_(omodel* m, const om_run_cfg* cfg, const int* prompts
                 work.n = 0;
                 for (int i = 0; i < seq[b].n; ++i) spush(&work, seq[b].t[i]);
                 for (int i = 0; i < t; ++i) spush(&work, drafts[(size_t)s * g + i]);
+                g_committed = seq[b].n; /* attention extension: the committed part of work */
                 fwd(m, work.t, work.n, sets, nd, remap, lg, raw, fin);
+                g_committed = 0;
                 drafts[(size_t)s * g + t] = greedy_(lg, m->V);
                 for (int i = 0; i < M * K; ++i) {
                     int k = (i / K) * E + fin[i];

@@ -224,9 +224,6 @@ Engine::Engine(const smoe_engine_config& c) {
     if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
     if (const char* v = getenv("SMOE_GATE_FLAG")) gate_flag = atoi(v) != 0;
     if (const char* v = getenv("SMOE_COMBINE_FLAG")) combine_flag = atoi(v) != 0;
-    if (const char* v = getenv("SMOE_PASS_KERNEL")) pass_kernel = atoi(v) != 0;
-    if (const char* v = getenv("SMOE_PASS_MAX_ROWS")) pass_kernel_max_rows = atoi(v);
-    if (const char* v = getenv("SMOE_PASS_MIN_ROWS")) pass_kernel_min_rows = atoi(v);
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
@@ -772,20 +769,6 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     // K1+K2: x0 and the first rms
     launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
                   stream);
-    if (pass_kernel && fuse_moe && T >= pass_kernel_min_rows && T <= pass_kernel_max_rows && pass_kernel_supported(*this)) {
-        // every layer in one persistent launch (pass_tc.cu), then the head and the argmax
-        {
-            ProfScope ps(*this, "pass");
-            launch_pass_tc(*this, T, restricted, use_aff, log_slot);
-        }
-        gemm(head, 0, op_head, V, V, d, nullptr, nullptr, 1, 0, T, 0, T, xa, op_xa, logits, V, kEpiStoreF32,
-             "head_gemm", (double)V * d * ws);
-        launch_argmax(logits, T, V, amax, flags, stream);
-        SMOE_CUDA(cudaGetLastError());
-        launches += 5;
-        alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
-        return;
-    }
     const double wbytes_dd = (double)d * d * ws;
     const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;

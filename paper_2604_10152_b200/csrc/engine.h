@@ -253,11 +253,6 @@ public:
     unsigned* comb_ctr = nullptr;  // device: combine blocks finished (monotonic)
     unsigned comb_epoch = 0;
     const unsigned* gemm_dep = nullptr;  // hand-off counter of the next gemm() launch
-    // one persistent launch per pass (pass_tc.cu), opt-in with env SMOE_PASS_KERNEL=1: bit-identical to
-    // the per-layer launches but 2-4% slower end to end at B = 1..64 (profiles/r02_pass_kernel.md)
-    int pass_kernel = 0;
-    // row range of the passes that use it when enabled (env SMOE_PASS_MIN_ROWS / SMOE_PASS_MAX_ROWS)
-    int pass_kernel_min_rows = 1, pass_kernel_max_rows = 1 << 30;
     int* pass_ctr = nullptr;     // pass kernel dependency counters (self-resetting)
     unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
@@ -339,9 +334,6 @@ public:
     std::unique_ptr<SpecState, SpecStateDeleter> st;
 };
 
-// pass_tc.cu: the whole pass (all layers) as one persistent tcgen05 kernel (bf16, HBM-resident, 1 GPU)
-bool pass_kernel_supported(const Engine& e);
-void launch_pass_tc(Engine& e, int T, bool restricted, int use_aff, int log_slot);
 
 // loop.cpp
 RunOut run_specmoe(Engine& e, const RunCfg& c, const std::vector<std::vector<int>>& prompts);

@@ -91,6 +91,7 @@ constexpr int kTrLaunches = 192, kTrUnits = 8192, kTrCtas = 160;
 struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done, epi_start; };
 __device__ TrUnit g_tr_unit[kTrLaunches][kTrUnits];
 __device__ long long g_tr_cta[kTrLaunches][kTrCtas][2];
+__device__ long long g_tr_cta_dep[kTrLaunches][kTrCtas];  // after the grouped launch's dependency wait
 __device__ int g_tr_meta[kTrLaunches][4];  // total units, nphase, T rows bound, grid
 __device__ __forceinline__ long long gtimer() {
     long long t;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage_bytes = (pair ? 2 : 1) * kABytes + p.b_region;
     int n_items = p.n_tiles;  // grouped launches: from the plan below
     int total_units = units_of_phase(p, n_items, 0, pair) + (p.nphase > 1 ? units_of_phase(p, n_items, 1, pair) : 0);
-    TR(const int trs = p.tr % kTrLaunches;)
+    TR(const int trs = p.tr % kTrLaunches; const long long tr_entry = gtimer();)
 
     // control block first (fixed size), then the 1024-aligned stage ring
     extern __shared__ uint8_t smem_raw[];
@@ -332,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         total_units = units_of_phase(p, n_items, 0, pair) + (p.nphase > 1 ? units_of_phase(p, n_items, 1, pair) : 0);
     }
     TR(if (threadIdx.x == 0) {
-        g_tr_cta[trs][blockIdx.x % kTrCtas][0] = gtimer();
+        g_tr_cta[trs][blockIdx.x % kTrCtas][0] = tr_entry;
+        g_tr_cta_dep[trs][blockIdx.x % kTrCtas] = gtimer();
         if (blockIdx.x == 0) { g_tr_meta[trs][0] = total_units; g_tr_meta[trs][1] = p.nphase; g_tr_meta[trs][2] = units_of_phase(p, n_items, 0, 0); g_tr_meta[trs][3] = gridDim.x; }
     })
 
@@ -711,6 +713,8 @@ extern "C" int smoe_tc_trace_dump(const char* path) {
     cudaMemcpyFromSymbol(u.data(), g_tr_unit, u.size() * sizeof(TrUnit));
     cudaMemcpyFromSymbol(c.data(), g_tr_cta, c.size() * sizeof(long long));
     cudaMemcpyFromSymbol(m.data(), g_tr_meta, m.size() * sizeof(int));
+    std::vector<long long> dep((size_t)kTrLaunches * kTrCtas);
+    cudaMemcpyFromSymbol(dep.data(), g_tr_cta_dep, dep.size() * sizeof(long long));
     FILE* fp = fopen(path, "wb");
     if (!fp) return -3;
     int hdr[3] = {kTrLaunches, kTrUnits, kTrCtas};
@@ -718,6 +722,7 @@ extern "C" int smoe_tc_trace_dump(const char* path) {
     fwrite(m.data(), sizeof(int), m.size(), fp);
     fwrite(c.data(), sizeof(long long), c.size(), fp);
     fwrite(u.data(), sizeof(TrUnit), u.size(), fp);
+    fwrite(dep.data(), sizeof(long long), dep.size(), fp);
     fclose(fp);
     return 0;
 #else

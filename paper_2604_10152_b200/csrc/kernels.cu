@@ -298,19 +298,32 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     extern __shared__ float sm[];  // [gw[E*d] when staged], xf[d], gl[E], p[E], red[8*32 + 33]
     __shared__ uint64_t gw_bar;
     float* gw = sm;
-    float* xf = sm + (a.stage_gw ? (size_t)a.E * a.d : 0);
+    const int gw_rows = a.stage_gw == 2 ? (a.E / (gate_threads(a.d, a.E) >> 5)) * (int)(blockDim.x >> 5)
+                                        : (a.stage_gw ? a.E : 0);
+    float* xf = sm + (size_t)gw_rows * a.d;
     float* gl = xf + a.d;
     float* red = gl + 2 * a.E + 8 * 32;
+    // Gate weights staged per CTA: one CTA per row stages all E rows; a row cluster (SMOE_ROW_CLUSTER,
+    // one virtual thread per real thread) stages only its CTA's experts -- its virtual warps
+    // w0 = c*RT/32 .. +RT/32 own experts w0 + k*nvw, i.e. E/nvw chunks of RT/32 contiguous rows.
+    const int gw_wpc = (int)(blockDim.x >> 5), gw_nvw = gate_threads(a.d, a.E) >> 5;
+    const int gw_c = a.stage_gw == 2 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
     if (a.stage_gw && threadIdx.x == 0) {
         // the layer's gate weights do not depend on earlier kernels: copy them into shared memory while
         // this block waits for the Mix GEMM (the GEMV then reads shared memory, not four L2 round trips)
         tc::mbar_init(&gw_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t total = (uint32_t)a.E * a.d * 4;
-        tc::mbar_expect_tx(&gw_bar, total);
-        for (uint32_t off = 0; off < total; off += 32768)
-            tc::bulk_g2s(reinterpret_cast<char*>(gw) + off, reinterpret_cast<const char*>(a.gate_w) + off,
-                         min(32768u, total - off), &gw_bar);
+        const uint32_t row_b = (uint32_t)a.d * 4;
+        const int chunks = a.stage_gw == 2 ? a.E / gw_nvw : 1;
+        const uint32_t chunk_b = a.stage_gw == 2 ? (uint32_t)gw_wpc * row_b : (uint32_t)a.E * row_b;
+        tc::mbar_expect_tx(&gw_bar, chunk_b * chunks);
+        for (int k = 0; k < chunks; ++k) {
+            const char* src = reinterpret_cast<const char*>(a.gate_w) +
+                              (size_t)(a.stage_gw == 2 ? k * gw_nvw + gw_c * gw_wpc : 0) * row_b;
+            char* dst = reinterpret_cast<char*>(gw) + (size_t)k * chunk_b;
+            for (uint32_t off = 0; off < chunk_b; off += 32768)
+                tc::bulk_g2s(dst + off, src + off, min(32768u, chunk_b - off), &gw_bar);
+        }
     }
     pdl_wait();
     pdl_trigger();
@@ -362,7 +375,9 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j) {
         for (int e = rc.vt(j) >> 5; e < E; e += nvw) {
-            const float4* g = reinterpret_cast<const float4*>(gsrc + (long long)e * d);
+            // staged per cluster CTA: chunk e / nvw, row e % nvw - c*wpc within it
+            const long long gr = a.stage_gw == 2 ? (long long)(e / gw_nvw) * gw_wpc + (e % gw_nvw - gw_c * gw_wpc) : e;
+            const float4* g = reinterpret_cast<const float4*>(gsrc + gr * d);
             float acc = 0.f;
 #pragma unroll 8
             for (int i = lane; i < d4; i += 32) {
@@ -663,9 +678,14 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
         const char* v = std::getenv("SMOE_GATE_STAGE");
         return !(v && v[0] == '0');
     }();
-    // stage the gate weights (E x d f32) in shared memory when they fit beside one row (C2: 128 KB)
-    const size_t gw_bytes = sizeof(float) * (size_t)a.E * a.d;
-    a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0;
+    // stage the gate weights (E x d f32) in shared memory when they fit beside one row (C2: 128 KB); a row
+    // cluster with one virtual thread per real thread stages only each CTA's experts (C4: 128 KB of 512)
+    const RowShape rs0 = row_shape(gate_threads(a.d, a.E));
+    const int vb = gate_threads(a.d, a.E), nvw = vb >> 5;
+    const bool per_cta = rs0.C > 1 && rs0.C * rs0.RT == vb && a.E % nvw == 0;
+    const size_t gw_bytes = sizeof(float) * (size_t)(per_cta ? (rs0.RT >> 5) * (a.E / nvw) : a.E) * a.d;
+    a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0
+                     ? (per_cta ? 2 : 1) : 0;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0) +
                   (a.in_draft ? sizeof(int) * ((size_t)a.E * a.N + a.N) + a.E : 0);
     static std::atomic<uint64_t> configured{0};

@@ -485,7 +485,7 @@ def test_bf16_agreement_with_oracle_margin_aware(port):
     assert route_bad == 0 and tok_bad == 0
 
 
-# ---------------------------------------------------------------- persistent pass kernel (pass_tc.cu)
+# ---------------------------------------------------------------- launch-shape switches
 class _env:
     """Set engine environment switches for the engines constructed inside the block."""
 
@@ -502,71 +502,6 @@ class _env:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-
-
-def _pass_shapes():
-    return [_c1_like(TANH2, skew=1.0), _c1_like(SWIGLU3, skew=1.0),
-            ModelSpec(num_layers=3, experts=64, top_k=6, hidden=256, ffn=256, vocab=512, expert_kind=SWIGLU3,
-                      moe_mask=[0, 1, 1], gate_skew=0.5)]
-
-
-@pytest.mark.parametrize("which", [0, 1, 2])
-def test_pass_kernel_bitexact_vs_per_layer(which):
-    """The whole-pass kernel (every pass, SMOE_PASS_MIN_ROWS=1) against the per-layer launches on the
-    same weights: identical logits, routing and token streams (both evaluate the same GEMM units and
-    the same pinned reduction trees), and on the pass kernel itself speculative == on-demand and
-    per-sequence outputs independent of the batch."""
-    s = _pass_shapes()[which]
-    nd = 8 if s.experts == 64 else 4
-    with _env(SMOE_PASS_MIN_ROWS=1, SMOE_PASS_KERNEL=1):
-        a = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4).init_device(5)
-    with _env(SMOE_PASS_KERNEL=0):
-        b = Engine(s, weight_type=BF16, max_batch=4, max_gamma=4).init_device(5)
-    for prefix in ([1, 2, 3], list(range(40)), [100] * 9):
-        la, ra, fa = a.forward(prefix)
-        lb, rb, fb = b.forward(prefix)
-        assert np.array_equal(la, lb) and np.array_equal(ra, rb) and np.array_equal(fa, fb)
-    a.build_affinity_device()
-    b.build_affinity_device()
-    prompts = make_prompts(9, 4, 8, s.vocab)
-    rb_ = b.run_specmoe(RunCfg(gamma=4, n_draft=nd, max_new_tokens=16), prompts)
-    od = a.run_ondemand(RunCfg(gamma=4, max_new_tokens=16), prompts)
-    sp = a.run_specmoe(RunCfg(gamma=4, n_draft=nd, max_new_tokens=16), prompts)
-    assert sp.tokens == od.tokens == rb_.tokens and sp.ledger == rb_.ledger and sp.trace == rb_.trace
-    one = a.run_specmoe(RunCfg(gamma=4, n_draft=nd, max_new_tokens=16), prompts[1:2])
-    assert one.tokens[0] == sp.tokens[1]
-    a.close()
-    b.close()
-
-
-def test_pass_kernel_agreement_with_oracle_margin_aware(port):
-    """P3 on the pass kernel: same bar as the per-layer test above (C1 shape, reference weights)."""
-    from oracle.oracle import ModelSpec as OSpec
-    sp = dict(num_layers=4, experts=8, top_k=2, hidden=512, ffn=1024, vocab=1024, seed=0)
-    m = port.build(OSpec(**sp))
-    with _env(SMOE_PASS_MIN_ROWS=1, SMOE_PASS_KERNEL=1):
-        e = Engine(spec_of(sp), weight_type=BF16, max_batch=1, max_gamma=1).init_exact()
-    rng = np.random.RandomState(2)
-    route_bad = tok_bad = 0
-    worst = 0.0
-    e.counters(reset=True)
-    for trial in range(40):
-        prefix = rng.randint(0, sp["vocab"], size=rng.randint(1, 24)).tolist()
-        lg, raw, _ = e.forward(prefix)
-        assert e.counters(reset=True)["launches"] == 5  # x0 + pass kernel + head + argmax (+ memset)
-        rl, gates = m.forward_gates(prefix)
-        rr = m.forward(prefix)[1]
-        worst = max(worst, float(np.max(np.abs(lg - rl)) / np.max(np.abs(rl))))
-        for l in range(gates.shape[0]):
-            srt = np.sort(gates[l])[::-1]
-            if srt[sp["top_k"] - 1] - srt[sp["top_k"]] > 0.05:
-                route_bad += set(raw[l].tolist()) != set(rr[l].tolist())
-        s2 = np.sort(rl)[::-1]
-        if s2[0] - s2[1] > 0.1:
-            tok_bad += int(np.argmax(lg)) != int(np.argmax(rl))
-    assert worst <= 0.03
-    assert route_bad == 0 and tok_bad == 0
-    e.close()
 
 
 @pytest.mark.parametrize("env", ["SMOE_ROW_CLUSTER=1", "SMOE_ROW_THREADS=256", "SMOE_GATE_STAGE=0",

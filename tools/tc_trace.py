@@ -80,7 +80,7 @@ def analyze(path):
     off += nl * 16
     cta = np.frombuffer(raw[off:off + nl * nc * 2 * 8], np.int64).reshape(nl, nc, 2)
     off += nl * nc * 16
-    un = np.frombuffer(raw[off:], np.int64).reshape(nl, nu, 7)
+    un = np.frombuffer(raw[off:off + nl * nu * 7 * 8], np.int64).reshape(nl, nu, 7)
     rows = []
     for s in range(nl):
         total, nphase, u0, grid = (int(v) for v in meta[s])
@@ -190,7 +190,9 @@ def dump_units(path, rows, dst, per_kind=3):
     off = 12 + nl * 16
     cta = np.frombuffer(raw[off:off + nl * nc * 2 * 8], np.int64).reshape(nl, nc, 2)
     off += nl * nc * 16
-    un = np.frombuffer(raw[off:], np.int64).reshape(nl, nu, 7)
+    un = np.frombuffer(raw[off:off + nl * nu * 7 * 8], np.int64).reshape(nl, nu, 7)
+    off += nl * nu * 7 * 8
+    dep = np.frombuffer(raw[off:off + nl * nc * 8], np.int64).reshape(nl, nc)
     out, seen = [], {}
     for r in rows:
         if r["kind"] == "mix/head":
@@ -209,7 +211,9 @@ def dump_units(path, rows, dst, per_kind=3):
                  + [round((int(U[i, 6]) - t0) / 1e3, 2)]
                  for i in range(len(U))]
         ends = [round((int(x) - t0) / 1e3, 2) for x in cta[s, :r["grid"], 1]]
-        out.append({"launch": r["launch"], "units_total": k, "dur_us": r["dur_us"], "units": units, "cta_end": ends})
+        deps = [round((int(x) - t0) / 1e3, 2) for x in dep[s, :r["grid"]]]
+        out.append({"launch": r["launch"], "t0_ns": int(t0), "units_total": k, "dur_us": r["dur_us"], "units": units,
+                    "cta_end": ends, "cta_dep_released": deps})
     json.dump(out, open(dst, "w"))
 
 
