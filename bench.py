@@ -353,7 +353,7 @@ def spec_measure(eng, stream, cfg, prompts, steps: int, warmup: int, profile: bo
                                                      "expert_flops:draft", "expert_flops:verify")}
         eng.counters(reset=True)
         out["prof"] = {c: eng.profile_read(c) for c in (
-            "expert_gemm", "expert_gemm:draft", "expert_gemm:verify", "dense_gemm", "head_gemm", "gate",
+            "expert_gemm", "expert_gemm:draft", "expert_gemm:verify", "dense_gemm", "head_gemm", "gate", "attention",
             "combine")}
     res = eng.spec_end()
     out["tau"] = res.metrics["tau_mean"]
@@ -383,10 +383,10 @@ def expert_roofline(m: dict, pk: dict) -> dict:
     return out
 
 
-def c2_engine(a, spec, dev, max_batch, max_gamma, rank=0, world=1, ep=False):
+def c2_engine(a, spec, dev, max_batch, max_gamma, rank=0, world=1, ep=False, max_seq_len=0):
     from paper_2604_10152_b200.engine import BF16, Engine
     eng = Engine(spec, weight_type=BF16, max_batch=max_batch, max_gamma=max_gamma, device=dev,
-                 ep_rank=rank if ep else 0, ep_world=world if ep else 1)
+                 ep_rank=rank if ep else 0, ep_world=world if ep else 1, max_seq_len=max_seq_len)
     if ep:
         eng.attach_nccl(share_nccl_id(rank))
     eng.init_device(0)
@@ -442,20 +442,25 @@ def section_gamma(eng, stream, a, spec, pk, gamma: int, B: int) -> dict:
     return out
 
 
-def section_shape(a, dev, shape: str, B: int, n_draft: int, pk, skew: float = 0.0, steps: int = 4) -> dict:
-    """A separate engine for another config of BASELINE.json (C4 fine-grained, or C2 with gate_skew)."""
+def section_shape(a, dev, shape: str, B: int, n_draft: int, pk, skew: float = 0.0, steps: int = 4,
+                  attention: bool = False) -> dict:
+    """A separate engine for another config of BASELINE.json (C4 fine-grained, or C2 with gate_skew), or
+    C2 with real GQA attention (Mixtral's 32 query / 8 KV heads of 128, RoPE theta 1e6, paged KV cache)
+    in place of the reference's prefix-mean surrogate (SURVEY 8(f)#4)."""
     import torch
     from paper_2604_10152_b200.engine import SWIGLU3, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
-    spec = ModelSpec(**SHAPES[shape], seed=0, gate_skew=skew, expert_kind=SWIGLU3)
-    eng = c2_engine(a, spec, dev, B, a.gamma)
+    extra = dict(attn_heads=32, kv_heads=8, head_dim=128, rope_theta=1e6) if attention else {}
+    spec = ModelSpec(**SHAPES[shape], seed=0, gate_skew=skew, expert_kind=SWIGLU3, **extra)
+    eng = c2_engine(a, spec, dev, B, a.gamma, max_seq_len=256 if attention else 0)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", dev))
     m = spec_measure(eng, stream, RunCfg(gamma=a.gamma, n_draft=n_draft, max_new_tokens=1 << 30),
                      make_prompts(1000, B, 8, spec.vocab), steps=steps, warmup=3)
     r = expert_roofline(m, pk)
     eng.close()
     out = {"workload": f"{SHAPE_NAMES[shape]}, swiglu3 bf16 HBM-resident, B={B}, gamma={a.gamma}, N={n_draft}, "
-                       f"gate_skew={skew}", "tokens_per_s": m["tokens"] / (m["ms"] * 1e-3), "ms_per_step": m["ms"] / steps,
+                       f"gate_skew={skew}" + (", real GQA attention 32q/8kv x 128, RoPE 1e6, paged KV cache (16-token "
+                                              "pages), prompts prefilled" if attention else ""), "tokens_per_s": m["tokens"] / (m["ms"] * 1e-3), "ms_per_step": m["ms"] / steps,
            "tau": m["tau"], "hbm_expert_bytes_per_token": m["alg_expert_bytes"] / max(1, m["tokens"]),
            "expert_gemm": r, "gpu_launches_per_step": m["launches"] / steps,
            "breakdown_ms_per_step": {k: v["ms"] / steps for k, v in m["prof"].items() if v["launches"]}}
@@ -606,7 +611,8 @@ def run_b200(a) -> None:
         eng.close()
     if default_sections:
         for key, kw in (("hot_skew2_c2", dict(shape="c2", B=a.batch, n_draft=a.n_draft, skew=2.0)),
-                        ("c4", dict(shape="c4", B=32, n_draft=8))):
+                        ("c4", dict(shape="c4", B=32, n_draft=8)),
+                        ("attention_c2", dict(shape="c2", B=a.batch, n_draft=a.n_draft, attention=True))):
             try:
                 line[key] = section_shape(a, local, pk=pk, **kw)
             except Exception as ex:

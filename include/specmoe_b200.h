@@ -36,10 +36,17 @@ typedef struct {
     int max_batch, max_gamma;
     int gemm_backend;        /* SMOE_GEMM_* ; AUTO = tcgen05 for bf16, SIMT for f32 */
     int device;
-    int offload;             /* 0: all experts HBM-resident; 1: pinned host pool + HBM slots (C3) */
+    int offload;             /* 0: all experts HBM-resident; 1: pinned host pool + HBM slots (C3); 2: SSD tier,
+                                a file on local storage ($SMOE_SSD_DIR, default /tmp) read with O_DIRECT */
     int hbm_expert_slots;    /* offload: HBM slot count (0 = 4 pinned draft experts per layer + two layers' transients) */
     int ep_rank, ep_world;   /* expert parallelism: this rank holds experts [r*E/G, (r+1)*E/G) of every layer
                                 (0, 0 or 0, 1 = single GPU); attach a transport before running */
+    /* Extension (no reference counterpart): attn_heads > 0 replaces the reference's
+     * prefix-mean + mix surrogate with real GQA attention (RoPE, paged KV cache of max_seq_len tokens per
+     * sequence; 0 = 512).  Single GPU only. */
+    int attn_heads, kv_heads, head_dim;
+    double rope_theta;
+    int max_seq_len;
 } smoe_engine_config;
 
 /* SpecConfig (specdec.hpp:17-29) + TierConfig (memsim.hpp:28-39) + policy/seed + decode mode. */

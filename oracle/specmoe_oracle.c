@@ -395,7 +395,7 @@ static __thread int g_committed;      /* attention extension: committed prefix l
 
 /* The MoE half of a layer (model.cpp:226-258): xf = rms(x); x += sum_k p[raw_k] expert_final_k(xf). */
 static void moe_half(const omodel* m, const olayer* ly, int mo, double* x, int plen, const int* restricted, int nd,
-                     const oaff* aff, int* raw_out, int* fin_out);
+                     const oaff* aff, int last, int* raw_out, int* fin_out);
 
 /* Real-attention extension (no reference counterpart): positions 0..n-1 are run in order,
  * each attending causally to every earlier position's K/V of the same layer.  Positions < nc-1 (the
@@ -464,11 +464,11 @@ static void fwd_attn(const omodel* m, const int* prefix, int n, const int* restr
             mv(ly->wo, o, d, (int)qd, a);
             for (int j = 0; j < d; ++j) x[j] += a[j];
             if (ly->is_moe) {
-                moe_half(m, ly, mo, x, p + 1, draft ? restricted : NULL, nd, aff, last ? raw_out : NULL,
+                moe_half(m, ly, mo, x, p + 1, draft ? restricted : NULL, nd, aff, last, last ? raw_out : NULL,
                          last ? fin_out : NULL);
                 ++mo;
             } else {
-                moe_half(m, ly, -1, x, p + 1, NULL, 0, NULL, NULL, NULL);
+                moe_half(m, ly, -1, x, p + 1, NULL, 0, NULL, 0, NULL, NULL);
             }
         }
         if (last) {
@@ -544,7 +544,7 @@ static void fwd(const omodel* m, const int* prefix, int n, const int* restricted
 }
 
 static void moe_half(const omodel* m, const olayer* ly, int mo, double* x, int plen, const int* restricted, int nd,
-                     const oaff* aff, int* raw_out, int* fin_out) {
+                     const oaff* aff, int last, int* raw_out, int* fin_out) {
     const int d = m->d, E = m->E, K = m->K;
     blk* mark = g_arena;
     double* xn = (double*)amalloc(sizeof(double) * d);
@@ -559,7 +559,7 @@ static void moe_half(const omodel* m, const olayer* ly, int mo, double* x, int p
     if (mo >= 0) {
         mtv(ly->gate, xn, d, E, gl);
         for (int e = 0; e < E; ++e) gl[e] += ly->bias[e];
-        if (g_gate_dump && raw_out) memcpy(g_gate_dump + (size_t)mo * E, gl, sizeof(double) * E);
+        if (g_gate_dump && last) memcpy(g_gate_dump + (size_t)mo * E, gl, sizeof(double) * E);
         softmax_(gl, E, pr);
         topk_(gl, E, K, raw);
         for (int k = 0; k < K; ++k) {

@@ -68,6 +68,20 @@ Engine::Engine(const smoe_engine_config& c) {
     Gmax = std::max(1, c.max_gamma);
     stride = Gmax + 1;
     Tmax = Bmax * (Gmax + 1);
+    Hq = std::max(0, c.attn_heads);
+    if (Hq > 0) {
+        Hkv = c.kv_heads;
+        hd = c.head_dim;
+        theta = c.rope_theta;
+        if (Hkv < 1 || Hq % Hkv || Hq / Hkv > 32 || hd < 2 || hd % 2 || !(theta > 0.0))
+            throw Error(kConfig, "model: attention needs kv_heads | attn_heads (<= 32 per group), an even head_dim and rope_theta > 0");
+        if (c.ep_world > 1) throw Error(kConfig, "engine: attention with expert parallelism is not supported");
+        QD = Hq * hd;
+        KD = Hkv * hd;
+        QKVD = QD + 2 * KD;
+        max_seq = c.max_seq_len > 0 ? c.max_seq_len : 512;
+        maxp = (max_seq + Gmax + 1 + kKvPage - 1) / kKvPage;
+    }
     device = c.device;
     offload = c.offload;
     if (E < 1 || K < 1 || K > E) throw Error(kConfig, "model: 1 <= top_k <= experts_per_block violated");
@@ -112,7 +126,7 @@ Engine::Engine(const smoe_engine_config& c) {
     }
     n_slots = exp_slots + n_dense;
     emb64 = dalloc<double>((size_t)V * d);
-    mix = dalloc_bytes((size_t)L * d * d * ws);
+    if (!attn()) mix = dalloc_bytes((size_t)L * d * d * ws);
     gate_w = dalloc<float>((size_t)M * E * d);
     gate_b = dalloc<float>((size_t)M * E);
     up_pool = dalloc_bytes((size_t)n_slots * U * d * ws);
@@ -136,6 +150,26 @@ Engine::Engine(const smoe_engine_config& c) {
         for (int e = 0; e < E; ++e) bias[(size_t)m * E + e] = (float)(skew * (1.0 - (double)e / E));  // model.cpp:128-130
     h2d(gate_b, bias.data(), sizeof(float) * bias.size());
 
+    if (attn()) {
+        wqkv = dalloc_bytes((size_t)L * QKVD * d * ws);
+        wo = dalloc_bytes((size_t)L * d * QD * ws);
+        qbuf = dalloc<float>((size_t)Tmax * QD);
+        attn_o = dalloc_bytes((size_t)Tmax * QD * ws);
+        const size_t n_pages = (size_t)Bmax * maxp;
+        kv = dalloc_bytes(n_pages * L * 2 * KD * kKvPage * ws);
+        ptab = dalloc<int>((size_t)Bmax * maxp);
+        SMOE_CUDA(cudaMemset(ptab, 0, sizeof(int) * Bmax * maxp));
+        last_tok = dalloc<int>(Bmax);
+        row_pos = dalloc<int>(Tmax);
+        pre_tok = dalloc<int>(Tmax);
+        pre_pos = dalloc<int>(Tmax);
+        kv_pages.assign(Bmax, {});
+        for (int pg = (int)n_pages - 1; pg >= 0; --pg) kv_free.push_back(pg);
+        h_seq_len.assign(Bmax, 0);
+        op_wqkv = {wqkv, (long long)L * QKVD, d};
+        op_wo = {wo, (long long)L * d, QD};
+        op_ao = {attn_o, (long long)Tmax, QD};
+    }
     seq_sum = dalloc<double>((size_t)Bmax * d);
     seq_len = dalloc<int>(Bmax);
     drafts = dalloc<int>((size_t)Bmax * stride);
@@ -171,9 +205,11 @@ Engine::Engine(const smoe_engine_config& c) {
         // 54.1 ms/step at 4 splits vs 57.0 at 2, 54.0-54.3 at 6/8, 56.2 at 16 (tools/ab_env.sh, same
         // box).  C4 (f=1408): 2 splits, 16.8 vs 17.4 ms/step at 4.
         const long long pair_unit_bytes = 256ll * f * 2;  // 256 weight rows x f bf16
-        s_mix = pick(nkb_d, std::max(1, 148 / std::max(1, (d + 127) / 128)));
+        // (attention: the Wo GEMM, K = Hq*hd, produces the partials the gate kernel adds in the Mix's place)
+        s_mix = pick(attn() ? (QD + 63) / 64 : nkb_d, std::max(1, 148 / std::max(1, (d + 127) / 128)));
+        if (attn()) s_qkv = pick(nkb_d, std::max(1, 148 / std::max(1, (QKVD + 127) / 128)));
         s_down = pick(nkb_f, std::max(2, (int)((pair_unit_bytes + (2 << 20) - 1) / (2 << 20))));
-        if (const char* v = getenv("SMOE_S_MIX")) s_mix = pick(nkb_d, atoi(v));    // tuning overrides
+        if (const char* v = getenv("SMOE_S_MIX")) s_mix = pick(attn() ? (QD + 63) / 64 : nkb_d, atoi(v));  // tuning overrides
         if (const char* v = getenv("SMOE_S_DOWN")) s_down = pick(nkb_f, atoi(v));
     }
     ybuf = dalloc<float>((size_t)s_down * seg_rows * d);
@@ -199,6 +235,7 @@ Engine::Engine(const smoe_engine_config& c) {
         h2d(ep_gslot, gs.data(), sizeof(int) * gs.size());
     }
     pmix = dalloc<float>((size_t)s_mix * Tmax * d);
+    if (attn()) pqkv = dalloc<float>((size_t)s_qkv * Tmax * QKVD);
     // + ep_world rows: an EP all-gather writes G * ceil(T/G) >= T rows
     logits = dalloc<float>((size_t)(Tmax + ep_world) * V);
     amax = dalloc<int>(Tmax + ep_world);
@@ -247,7 +284,8 @@ Engine::~Engine() {
     for (void* q : ep_ipc_opened) cudaIpcCloseMemHandle(q);
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
     fr(ep_flags); fr(ep_peer);
-    fr(ep_cntg); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
+    fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos);
+    fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(comb_ctr); fr(scratch64); fr(pass_ctr);
     if (h_small) cudaFreeHost(h_small);
@@ -359,8 +397,7 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     auto up_dst = [&]() -> void* {
         const int sl = slot_for();
         if (sl >= 0) return at(up_pool, (size_t)sl * U * d);
-        SMOE_CUDA(cudaMemcpyAsync(stage_up, static_cast<char*>(host_up) + hkey(off_key) * U * d * ws, (size_t)U * d * ws,
-                                  cudaMemcpyHostToDevice, stream));
+        host_to_device(off_key, 0, stage_up, stream);  // read-modify-write of the w1/w3 rows
         return stage_up;
     };
     auto down_dst = [&]() -> void* {
@@ -376,7 +413,19 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
         launch_convert_transpose(stage(n), d, V, head, wt, stream);
     } else if (name == "mix") {
         need((long long)d * d);
+        if (attn()) throw Error(kConfig, "upload_tensor: an attention model has no mix (wq/wk/wv/wo)");
         launch_convert(stage(n), n, at(mix, (size_t)layer * d * d), wt, stream);
+    } else if (name == "wq" || name == "wk" || name == "wv" || name == "wo") {
+        if (!attn()) throw Error(kConfig, "upload_tensor: " + name + " needs an attention model");
+        if (layer < 0 || layer >= L) throw Error(kConfig, "upload_tensor: layer out of range");
+        if (name == "wo") {
+            need((long long)d * QD);
+            launch_convert(stage(n), n, at(wo, (size_t)layer * d * QD), wt, stream);
+        } else {
+            const int row0 = name == "wq" ? 0 : name == "wk" ? QD : QD + KD;
+            need((long long)(name == "wq" ? QD : KD) * d);
+            launch_convert(stage(n), n, at(wqkv, ((size_t)layer * QKVD + row0) * d), wt, stream);
+        }
     } else if (name == "gate") {
         need((long long)d * E);
         if (layer < 0 || layer >= L || !mask[layer]) throw Error(kConfig, "upload_tensor: gate on a dense layer");
@@ -401,9 +450,8 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     SMOE_CUDA(cudaGetLastError());
     if (off_key >= 0) {  // write the converted expert matrix back to the pinned host pool
         const bool is_down = name == "down" || name == "w2";
-        const size_t bytes = is_down ? (size_t)d * f * ws : (size_t)U * d * ws;
-        void* host = static_cast<char*>(is_down ? host_down : host_up) + hkey(off_key) * bytes;
-        SMOE_CUDA(cudaMemcpyAsync(host, is_down ? stage_down : stage_up, bytes, cudaMemcpyDeviceToHost, stream));
+        sync();
+        device_to_host(off_key, is_down ? 1 : 0, is_down ? stage_down : stage_up);
     }
     sync();
 }
@@ -419,8 +467,17 @@ void Engine::init_exact() {
     const int nmat = kind == kSwiglu3 ? 3 : 2;
     std::vector<std::vector<double>> ex((size_t)E * nmat);
     for (int l = 0; l < L; ++l) {
-        ps.fill(buf, (size_t)d * d, sd);
-        upload_tensor("mix", l, -1, buf.data(), (long long)buf.size());
+        if (attn()) {  // the attention weights take the mix's place in the draw order (oracle fwd_attn)
+            const char* names[4] = {"wq", "wk", "wv", "wo"};
+            const size_t cnt[4] = {(size_t)QD * d, (size_t)KD * d, (size_t)KD * d, (size_t)d * QD};
+            for (int q = 0; q < 4; ++q) {
+                ps.fill(buf, cnt[q], sd);
+                upload_tensor(names[q], l, -1, buf.data(), (long long)buf.size());
+            }
+        } else {
+            ps.fill(buf, (size_t)d * d, sd);
+            upload_tensor("mix", l, -1, buf.data(), (long long)buf.size());
+        }
         if (mask[l]) {
             ps.fill(buf, (size_t)d * E, sd);
             upload_tensor("gate", l, -1, buf.data(), (long long)buf.size());
@@ -466,7 +523,13 @@ void Engine::init_device(uint64_t s) {
     const double sd = 1.0 / std::sqrt((double)d);
     uint64_t tid = 1;
     launch_fill_normal_f64(emb64, (long long)V * d, sd, s, tid++, stream);
-    launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
+    if (attn()) {  // tensor ids 7, 8 (after the head's): the other tensors keep their streams
+        launch_fill_normal(wqkv, wt, (long long)L * QKVD * d, sd, s, 7, stream);
+        launch_fill_normal(wo, wt, (long long)L * d * QD, sd, s, 8, stream);
+        ++tid;
+    } else {
+        launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
+    }
     launch_fill_normal(gate_w, kF32, (long long)M * E * d, sd, s, tid++, stream);
     const uint64_t tid_up = tid++, tid_down = tid++;
     dev_rng = true;
@@ -501,10 +564,8 @@ void Engine::init_device(uint64_t s) {
             if (!owns(key)) continue;
             launch_fill_normal(stage_up, wt, (long long)U * d, sd, s, tid_up, stream, (long long)key * U * d);
             launch_fill_normal(stage_down, wt, (long long)d * f, sd, s, tid_down, stream, (long long)key * d * f);
-            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_up) + hkey(key) * U * d * ws, stage_up,
-                                      (size_t)U * d * ws, cudaMemcpyDeviceToHost, stream));
-            SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(host_down) + hkey(key) * d * f * ws, stage_down,
-                                      (size_t)d * f * ws, cudaMemcpyDeviceToHost, stream));
+            device_to_host(key, 0, stage_up);
+            device_to_host(key, 1, stage_down);
         }
         for (int l = 0, k = 0; l < L; ++l)
             if (!mask[l]) {
@@ -726,7 +787,7 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
                   sched + 4 * slot, moe_done + 64 * slot};
     if (l2_next && l2_prefetch) {
         up.l2_next = l2_next;
-        up.l2_next_bytes = (long long)d * d * (long long)ws;
+        up.l2_next_bytes = l2_next_bytes;
     }
     if (moe_dep) {
         up.dep_ctr = moe_dep;
@@ -766,16 +827,24 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
     const size_t ws = wt == kF32 ? 4 : 2;
     const long long pm_stride = (long long)Tmax * d, yd_stride = (long long)E * Tmax * d;
     if (M > 0) SMOE_CUDA(cudaMemsetAsync(grp_cnt, 0, sizeof(int) * (size_t)M * E, stream));  // dispatch counters
-    // K1+K2: x0 and the first rms
-    launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
-                  stream);
+    // K1+K2: x0 and the first rms (attention models: the row's own token embedding)
+    if (attn())
+        launch_x0_tok_rms(emb64, seq_len, last_tok, drafts, stride, rseq, rextra, extra_uniform,
+                          prefill_rows ? pre_tok : nullptr, prefill_rows ? pre_pos : nullptr, T, d, x, row_plen,
+                          row_pos, xa, wt, stream);
+    else
+        launch_x0_rms(emb64, seq_sum, seq_len, drafts, stride, rseq, rextra, extra_uniform, T, d, x, row_plen, xa, wt,
+                      stream);
     const double wbytes_dd = (double)d * d * ws;
     const double ebytes_up = (double)U * d * ws, ebytes_dn = (double)d * f * ws;
     const Epi up_epi = kind == kSwiglu3 ? kEpiSwiglu : kEpiTanh;
     for (int l = 0; l < L; ++l) {
-        // K3: a = Mix rms(x) as split-K partials; the residual add happens in the next kernel
-        gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, 0, T, l, T, xa, op_xa, pmix, d,
-             kEpiStoreF32, "dense_gemm", wbytes_dd, s_mix, pm_stride);
+        // K3: a = Mix rms(x) (or attention's Wo o) as split-K partials; the residual add happens in the next kernel
+        if (attn())
+            attn_layer(l, T, rseq);
+        else
+            gemm(mix, (long long)d * d, op_mix, d, d, d, nullptr, nullptr, 1, 0, T, l, T, xa, op_xa, pmix, d,
+                 kEpiStoreF32, "dense_gemm", wbytes_dd, s_mix, pm_stride);
         const int mo = moe_ord[l];
         if (mo >= 0) {
             int* rl = raw_log + ((size_t)log_slot * M + mo) * Tmax * K;
@@ -800,7 +869,13 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             if (fetch) store_fetch_layer(mo, cnt);  // expert store: migrate this layer's missing experts
             // weight slots: the store's table for this layer's fetch, else the resident slot map (draft
             // passes touch only pinned draft experts)
-            l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
+            if (attn()) {  // the next layer's QKV weights
+                l2_next = l + 1 < L ? static_cast<const char*>(wqkv) + (size_t)(l + 1) * QKVD * d * ws : nullptr;
+                l2_next_bytes = (long long)QKVD * d * (long long)ws;
+            } else {
+                l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
+                l2_next_bytes = (long long)d * d * (long long)ws;
+            }
             expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
             l2_next = nullptr;
             moe_dep = nullptr;
@@ -827,8 +902,94 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
          "head_gemm", (double)V * d * ws);
     launch_argmax(logits, T, V, amax, flags, stream);
     SMOE_CUDA(cudaGetLastError());
-    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 4 : 5) + (uint64_t)n_dense * 5;
-    alg_dense_bytes += (double)L * d * d * ws + (double)V * d * ws + (double)n_dense * (U + d) * (double)f * ws;
+    launches += 3 + (uint64_t)M * ((use_tc && fuse_moe && E <= 64) ? 4 : 5) + (uint64_t)n_dense * 5 +
+                (attn() ? 3ull * L : 0ull);
+    alg_dense_bytes += (double)L * (attn() ? (double)(QKVD + QD) * d : (double)d * d) * ws + (double)V * d * ws +
+                       (double)n_dense * (U + d) * (double)f * ws;
+}
+
+// ------------------------------------------------------------------ real attention (attn.cu)
+// One layer's attention for the T rows of a pass: QKV projection (split-K partials), RoPE + k/v into the
+// sequences' cache pages + attention (k_qkv_rope, k_attn), Wo projection into the Mix's partial buffer.
+void Engine::attn_layer(int l, int T, const int* rseq) {
+    const size_t ws = wt == kF32 ? 4 : 2;
+    gemm(wqkv, (long long)QKVD * d, op_wqkv, QKVD, QKVD, d, nullptr, nullptr, 1, 0, T, l, T, xa, op_xa, pqkv, QKVD,
+         kEpiStoreF32, "dense_gemm", (double)QKVD * d * ws, s_qkv, (long long)Tmax * QKVD);
+    {
+        ProfScope ps(*this, "attention");
+        AttnArgs a{pqkv, s_qkv, (long long)Tmax * QKVD, T, Hq, Hkv, hd, theta, rseq, row_pos, ptab, maxp, l, L,
+                   qbuf, kv, wt, maxp * kKvPage, attn_o};
+        launch_attention(a, stream);
+    }
+    gemm(wo, (long long)d * QD, op_wo, d, d, QD, nullptr, nullptr, 1, 0, T, l, T, attn_o, op_ao, pmix, d,
+         kEpiStoreF32, "dense_gemm", (double)d * QD * ws, s_mix, (long long)Tmax * d);
+}
+
+// Pages for positions [0, len + Gmax] of sequence b (the rows of the next draft / verify pass), the
+// rest returned to the pool -- the cache of a rolled-back sequence shrinks with its committed length.
+void Engine::kv_fit(int b) {
+    const int need = (h_seq_len[b] + Gmax + kKvPage) / kKvPage;
+    if (need > maxp) throw Error(kConfig, "attention: sequence longer than max_seq_len");
+    auto& pg = kv_pages[b];
+    if ((int)pg.size() == need) return;  // the table row is current (pages change every kKvPage tokens)
+    while ((int)pg.size() > need) {
+        kv_free.push_back(pg.back());
+        pg.pop_back();
+    }
+    while ((int)pg.size() < need) {
+        if (kv_free.empty()) throw Error(kInvariant, "attention: KV page pool exhausted");
+        pg.push_back(kv_free.back());
+        kv_free.pop_back();
+    }
+    std::vector<int> row(maxp, 0);
+    std::copy(pg.begin(), pg.end(), row.begin());
+    upload_ints(ptab + (size_t)b * maxp, row.data(), row.size());
+}
+
+void Engine::kv_advance(const std::vector<int>& seqs, const std::vector<int>& takes) {
+    if (!attn()) return;
+    for (size_t i = 0; i < seqs.size(); ++i) {
+        h_seq_len[seqs[i]] += takes[i];
+        kv_fit(seqs[i]);
+    }
+}
+
+// The prompts' k/v: positions 0..len-2 of every sequence (the last prompt token is the next pass's input),
+// as unrestricted passes of explicit (token, position) rows, position-major in chunks of Tmax rows so
+// every row's earlier positions are in the cache before its attention runs.
+void Engine::prefill(const std::vector<std::vector<int>>& prompts) {
+    std::vector<int> rs, tk, ps;
+    size_t longest = 0;
+    for (auto& p : prompts) longest = std::max(longest, p.size());
+    for (size_t p = 0; p + 1 < longest; ++p)
+        for (size_t b = 0; b < prompts.size(); ++b)
+            if (p + 1 < prompts[b].size()) {
+                rs.push_back((int)b);
+                tk.push_back(prompts[b][p]);
+                ps.push_back((int)p);
+            }
+    const uint64_t hb = h2d_bytes;  // expert fetches of the prefill are setup, not ledger traffic
+    const double hm = h2d_ms;
+    prefill_rows = true;
+    for (size_t r0 = 0; r0 < rs.size(); r0 += (size_t)Tmax) {
+        const int n = (int)std::min((size_t)Tmax, rs.size() - r0);
+        upload_ints(row_seq, rs.data() + r0, n);
+        upload_ints(pre_tok, tk.data() + r0, n);
+        upload_ints(pre_pos, ps.data() + r0, n);
+        try {
+            pass(n, row_seq, nullptr, 0, false, 0, 0);
+        } catch (...) {
+            prefill_rows = false;
+            throw;
+        }
+    }
+    prefill_rows = false;
+    sync();
+    if (offload) {
+        collect_h2d();
+        h2d_bytes = hb;
+        h2d_ms = hm;
+    }
 }
 
 // Peer tables for the fused exchange: every rank's xrecv, rcnt, yret and flag array, addressable from
@@ -1011,9 +1172,18 @@ void Engine::reset_sequences(const std::vector<std::vector<int>>& prompts) {
     upload_ints(dtoks, toks.data(), toks.size());
     upload_ints(commit_take, take.data(), B);
     upload_ints(seqs, sq.data(), B);
-    launch_commit(seq_sum, seq_len, emb64, seqs, dtoks, (int)plen, commit_take, B, d, stream);
+    launch_commit(seq_sum, seq_len, emb64, seqs, dtoks, (int)plen, commit_take, B, d, stream, last_tok);
     sync();
     SMOE_CUDA(cudaFree(dtoks));
+    if (attn()) {  // a fresh paged cache holding the prompts' k/v
+        for (int b = 0; b < Bmax; ++b) {
+            for (int pg : kv_pages[b]) kv_free.push_back(pg);
+            kv_pages[b].clear();
+            h_seq_len[b] = b < B ? (int)prompts[b].size() : 0;
+        }
+        for (int b = 0; b < B; ++b) kv_fit(b);
+        prefill(prompts);
+    }
 }
 
 void Engine::forward_one(const std::vector<int>& prefix, const int* restricted, int n_draft, int use_aff,

@@ -167,6 +167,14 @@ public:
     bool have_affinity = false;
 
     // ---- expert store (offload mode, store.cpp): pinned host pools, HBM slot pool
+    // offload 1: pinned host DRAM pools.  offload 2 (SSD tier): one file on local storage holding every
+    // expert of this rank (O_DIRECT when the filesystem allows), read through pinned staging chunks
+    struct SsdDeleter {
+        void operator()(struct SsdTier* t) const;
+    };
+    std::unique_ptr<struct SsdTier, SsdDeleter> ssd;
+    void host_to_device(int key, int which, void* dst, cudaStream_t s);   // which: 0 up/w1w3, 1 down
+    void device_to_host(int key, int which, const void* src);             // (synchronous)
     void* host_up = nullptr;    // [M*eo][U][d] pinned: this rank's experts (eo = E / ep_world), hkey order
     void* host_down = nullptr;  // [M*eo][d][f] pinned
     void* stage_up = nullptr;   // device staging of one expert (offload init)
@@ -289,6 +297,30 @@ public:
     // ---- draft tables
     void set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft);  // sorted per layer
     int cur_n_draft = 0;
+    // ---- real GQA attention (attn.cu; attn_heads > 0)
+    int Hq = 0, Hkv = 0, hd = 0, QD = 0, KD = 0, QKVD = 0, max_seq = 0, maxp = 0, s_qkv = 1;
+    double theta = 1e4;
+    void* wqkv = nullptr;    // [L][QKVD][d]: rows q (QD), k (KD), v (KD) -- K-major, like the Mix
+    void* wo = nullptr;      // [L][d][QD]
+    float* pqkv = nullptr;   // [s_qkv][Tmax][QKVD] split-K partials of the QKV projection
+    float* qbuf = nullptr;   // [Tmax][QD] rotated queries
+    void* attn_o = nullptr;  // [Tmax][QD] attention output (the Wo GEMM operand)
+    void* kv = nullptr;      // KV pages [n_pages][L][2][Hkv][kKvPage][hd]
+    int* ptab = nullptr;     // [Bmax][maxp] page table
+    int* last_tok = nullptr; // [Bmax] last committed token (the input of the next row)
+    int* row_pos = nullptr;  // [Tmax] position of each row of the pass
+    int* pre_tok = nullptr;  // [Tmax] prefill rows: explicit tokens and positions
+    int* pre_pos = nullptr;
+    bool prefill_rows = false;
+    TcOperand op_wqkv{}, op_wo{}, op_ao{};
+    std::vector<std::vector<int>> kv_pages;  // host: pages of each sequence
+    std::vector<int> kv_free, h_seq_len;
+    long long l2_next_bytes = 0;
+    bool attn() const { return Hq > 0; }
+    void kv_fit(int b);     // pages for positions [0, h_seq_len[b] + Gmax] (and the table row uploaded)
+    void kv_advance(const std::vector<int>& seqs, const std::vector<int>& takes);
+    void attn_layer(int l, int T, const int* rseq);
+    void prefill(const std::vector<std::vector<int>>& prompts);
 
     // ---- passes
     // rows r=0..T-1: sequence slot row_seq[r], pending-draft count row_extra[r] (or extra_uniform).

@@ -548,7 +548,7 @@ __global__ void k_accept(const int* drafts, const int* vam, const int* seqs, int
 }
 
 __global__ void k_commit(double* ssum, int* slen, const double* emb, const int* seqs, const int* toks, int tstride,
-                         const int* take, int d) {
+                         const int* take, int d, int* last_tok) {
     pdl_wait();
     pdl_trigger();
     const int j = blockIdx.x;
@@ -560,7 +560,10 @@ __global__ void k_commit(double* ssum, int* slen, const double* emb, const int* 
         for (int t = 0; t < n; ++t) s += emb[(long long)toks[(long long)j * tstride + t] * d + i];
         ssum[(long long)b * d + i] = s;
     }
-    if (threadIdx.x == 0) slen[b] += n;
+    if (threadIdx.x == 0) {
+        slen[b] += n;
+        if (last_tok && n > 0) last_tok[b] = toks[(long long)j * tstride + n - 1];  // attention models' next input
+    }
 }
 
 // ------------------------------------------------------------------ init / conversion
@@ -731,9 +734,9 @@ void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, i
 }
 
 void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
-                   int tok_stride, const int* take, int na, int d, cudaStream_t s) {
+                   int tok_stride, const int* take, int na, int d, cudaStream_t s, int* last_tok) {
     if (na <= 0) return;
-    launch_k(k_commit, na, 1024, 0, s, seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d);
+    launch_k(k_commit, na, 1024, 0, s, seq_sum, seq_len, emb64, seqs, toks, tok_stride, take, d, last_tok);
 }
 
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,

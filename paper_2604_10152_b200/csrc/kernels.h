@@ -90,7 +90,7 @@ void launch_accept(const int* drafts, const int* vam, const int* seqs, int na, i
 
 // State advance / rollback (F6): sum[b] += emb[tok] for the taken tokens, len[b] += take.
 void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int* seqs, const int* toks,
-                   int tok_stride, const int* take, int na, int d, cudaStream_t s);
+                   int tok_stride, const int* take, int na, int d, cudaStream_t s, int* last_tok = nullptr);
 
 // Grouped skinny GEMM on CUDA cores (f32 or bf16 weights, f32 accumulation):
 //   for group g with slot s = group_slot[g] >= 0 and rows [g*seg, g*seg + group_cnt[g]):
@@ -142,5 +142,28 @@ void launch_verify_sampling(const float* logits, int V, double T, double* stats,
                             const int* drafts, int dstride, const int* seqs, int na, int g, const double* pool,
                             int* acc, int* kind, int* uidx, int* used, int* corr, int* flags, double* ratio,
                             cudaStream_t s);
+
+// Real GQA attention (attn.cu).  KV cache pages of kKvPage tokens: [page][L][k|v][Hkv][kKvPage][hd].
+constexpr int kKvPage = 16;
+// x0 = emb[token of the row] and its rms (attention models): token/position from the sequence state
+// (position len-1+i, token = last committed or pending draft i-1) or explicit (rtok/rpos, the prefill)
+void launch_x0_tok_rms(const double* emb64, const int* seq_len, const int* last_tok, const int* pend, int pend_stride,
+                       const int* row_seq, const int* row_extra, int extra_uniform, const int* rtok, const int* rpos,
+                       int T, int d, float* x, int* row_plen, int* row_pos, void* xa, WType op, cudaStream_t s);
+struct AttnArgs {
+    const float* P;  // QKV projection split-K partials [S][Tmax][Hq*hd + 2*Hkv*hd]
+    int S;
+    long long pstride;
+    int T, Hq, Hkv, hd;
+    double theta;
+    const int *row_seq, *row_pos, *ptab;
+    int maxp, layer, L;
+    float* qbuf;   // [Tmax][Hq*hd]
+    void* kv;      // cache pages
+    WType kvt;     // cache / output element type
+    int max_pos;   // longest sequence the scores scratch holds
+    void* out;     // [Tmax][Hq*hd] -> the Wo GEMM operand
+};
+void launch_attention(const AttnArgs& a, cudaStream_t s);
 
 }  // namespace smoe

@@ -267,7 +267,8 @@ static void hot_global_warmup(Engine& e, SpecState& S, const std::vector<std::ve
                     need[key] = 1;
                     wc[key]++;
                 }
-        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream);
+        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream, e.last_tok);
+        e.kv_advance(rs, one);
         wr.ensure(need, 2, step, wl);
         wr.flush();
     }
@@ -539,7 +540,9 @@ int spec_step(Engine& e, int* accepted_tokens) {
     // rollback / advance of the device prefix state: only the taken tokens enter the running sums
     e.upload_ints(e.commit_toks, ctoks.data(), ctoks.size());
     e.upload_ints(e.commit_take, ctake.data(), na);
-    launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.commit_toks, e.stride, e.commit_take, na, e.d, e.stream);
+    launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.commit_toks, e.stride, e.commit_take, na, e.d, e.stream,
+                  e.last_tok);
+    e.kv_advance(act, ctake);
     e.launches += 1;
 
     if (S.c.policy == SMOE_POLICY_HOT_TEMPORAL) {
@@ -672,7 +675,8 @@ RunOut run_ondemand(Engine& e, const RunCfg& c, const std::vector<std::vector<in
         }
         e.pass(B, e.row_seq, nullptr, 0, false, 0, 0);
         if (samp) launch_sample_rows(e.logits, B, e.V, c.temperature, e.samp_u, e.amax, nullptr, 0, e.stream);
-        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream);
+        launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.amax, 1, e.commit_take, B, e.d, e.stream, e.last_tok);
+        e.kv_advance(rs, one);
         read_log(e, e.raw_log, 0, B, raw);
         SMOE_CUDA(cudaMemcpyAsync(am.data(), e.amax, sizeof(int) * B, cudaMemcpyDeviceToHost, e.stream));
         e.sync();

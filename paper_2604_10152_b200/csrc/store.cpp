@@ -14,12 +14,178 @@
 // HBM therefore needs only M*N pinned slots + (E - N) transient slots, not the whole model.
 // The reference-semantics ledger is kept separately by loop.cpp; the bytes this store moves are
 // exactly (ledger entries) x (real bytes per expert).
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
 
 #include "engine.h"
 
 namespace smoe {
+
+// ------------------------------------------------------------------ SSD tier (offload = 2)
+// The reference's third tier is a bandwidth scalar (TierConfig.ssd_bandwidth, memsim.hpp:31-37).  Here
+// it is a file on local storage: every expert of this rank at a 4 KB-aligned record, read with O_DIRECT
+// (page cache bypassed, so each migration really streams from the device; buffered reads + DONTNEED when
+// the filesystem refuses O_DIRECT) by a small reader pool into pinned staging chunks, each chunk copied
+// to its HBM slot on the copy stream as soon as it lands.  GPUDirect Storage (cuFile) would skip the
+// staging copy; without the nvidia-fs module it degrades to this same bounce-buffer path.
+struct SsdTier {
+    static constexpr size_t kChunk = 8u << 20, kAlign = 4096;
+    static constexpr int kSlots = 8, kReaders = 4;
+    int fd = -1;
+    bool direct = false;
+    size_t rec_up = 0, rec = 0;
+    char* stage[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+    int next = 0;
+    std::vector<std::thread> pool;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::function<void()>> q;
+    bool stop = false;
+    uint64_t read_bytes = 0;
+
+    static size_t ru(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+    SsdTier(size_t up_b, size_t dn_b, size_t keys) {
+        rec_up = ru(up_b);
+        rec = rec_up + ru(dn_b);
+        const char* dir = std::getenv("SMOE_SSD_DIR");
+        std::string path = std::string(dir && *dir ? dir : "/tmp") + "/specmoe_ssd_" + std::to_string(getpid()) + "_" +
+                           std::to_string(reinterpret_cast<uintptr_t>(this)) + ".bin";
+        fd = open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC | O_DIRECT, 0600);
+        direct = fd >= 0;
+        if (fd < 0) fd = open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+        if (fd < 0) throw Error(kConfig, "expert store: cannot create the SSD-tier file " + path);
+        unlink(path.c_str());  // removed when the engine closes it
+        if (ftruncate(fd, (off_t)(rec * keys)) != 0) throw Error(kConfig, "expert store: SSD-tier file too large");
+        for (int i = 0; i < kSlots; ++i) {
+            SMOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage[i]), kChunk, cudaHostAllocDefault));
+            SMOE_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+        for (int i = 0; i < kReaders; ++i)
+            pool.emplace_back([this] {
+                for (;;) {
+                    std::function<void()> job;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return stop || !q.empty(); });
+                        if (stop && q.empty()) return;
+                        job = std::move(q.front());
+                        q.pop_front();
+                    }
+                    job();
+                }
+            });
+    }
+    ~SsdTier() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : pool) t.join();
+        for (int i = 0; i < kSlots; ++i) {
+            if (ev[i]) cudaEventDestroy(ev[i]);
+            if (stage[i]) cudaFreeHost(stage[i]);
+        }
+        if (fd >= 0) close(fd);
+    }
+    void submit(std::function<void()> job) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            q.push_back(std::move(job));
+        }
+        cv.notify_one();
+    }
+    static void pread_all(int fd, char* buf, size_t n, off_t off, bool direct) {
+        size_t done = 0;
+        while (done < n) {
+            const ssize_t r = pread(fd, buf + done, n - done, off + (off_t)done);
+            if (r <= 0) throw Error(kCuda, "expert store: SSD-tier read failed");
+            done += (size_t)r;
+        }
+        if (!direct) posix_fadvise(fd, off, (off_t)n, POSIX_FADV_DONTNEED);  // the next migration reads the device
+    }
+    // file region [off, off + n) -> device dst on stream s, chunk by chunk, kSlots - 1 reads ahead
+    void read_to_device(size_t off, size_t n, char* dst, cudaStream_t s) {
+        const size_t nch = (n + kChunk - 1) / kChunk;
+        std::vector<std::atomic<int>> done(nch);
+        std::vector<int> slot_of(nch);
+        auto issue = [&](size_t i) {
+            const int sl = next++ % kSlots;
+            SMOE_CUDA(cudaEventSynchronize(ev[sl]));  // its previous chunk has left for the GPU
+            slot_of[i] = sl;
+            done[i] = 0;
+            const size_t o = i * kChunk, len = ru(std::min(kChunk, n - o));
+            char* buf = stage[sl];
+            std::atomic<int>* flag = &done[i];
+            const int f = fd;
+            const bool dio = direct;
+            submit([=] {
+                try {
+                    pread_all(f, buf, len, (off_t)(off + o), dio);
+                    flag->store(1);
+                } catch (...) {
+                    flag->store(-1);
+                }
+            });
+        };
+        size_t issued = 0;
+        for (; issued < nch && issued < (size_t)kSlots - 1; ++issued) issue(issued);
+        for (size_t i = 0; i < nch; ++i) {
+            while (done[i].load() == 0) std::this_thread::yield();
+            if (done[i].load() < 0) throw Error(kCuda, "expert store: SSD-tier read failed");
+            const size_t o = i * kChunk, len = std::min(kChunk, n - o);
+            SMOE_CUDA(cudaMemcpyAsync(dst + o, stage[slot_of[i]], len, cudaMemcpyHostToDevice, s));
+            SMOE_CUDA(cudaEventRecord(ev[slot_of[i]], s));
+            read_bytes += len;
+            if (issued < nch) issue(issued++);
+        }
+    }
+    void write_from_device(size_t off, size_t n, const char* src, cudaStream_t s) {
+        for (size_t o = 0; o < n; o += kChunk) {
+            const size_t len = std::min(kChunk, n - o);
+            SMOE_CUDA(cudaMemcpyAsync(stage[0], src + o, len, cudaMemcpyDeviceToHost, s));
+            SMOE_CUDA(cudaStreamSynchronize(s));
+            const size_t wl = ru(len);
+            if (pwrite(fd, stage[0], wl, (off_t)(off + o)) != (ssize_t)wl)
+                throw Error(kCuda, "expert store: SSD-tier write failed");
+        }
+    }
+};
+
+void Engine::SsdDeleter::operator()(SsdTier* t) const { delete t; }
+
+void Engine::host_to_device(int key, int which, void* dst, cudaStream_t s) {
+    const size_t bytes = expert_bytes(which), hk = hkey(key);
+    if (ssd) {
+        ssd->read_to_device(hk * ssd->rec + (which ? ssd->rec_up : 0), bytes, static_cast<char*>(dst), s);
+        return;
+    }
+    const char* src = static_cast<const char*>(which ? host_down : host_up) + hk * bytes;
+    SMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+}
+
+void Engine::device_to_host(int key, int which, const void* src) {
+    const size_t bytes = expert_bytes(which), hk = hkey(key);
+    if (ssd) {
+        ssd->write_from_device(hk * ssd->rec + (which ? ssd->rec_up : 0), bytes, static_cast<const char*>(src), stream);
+        return;
+    }
+    char* dst = static_cast<char*>(which ? host_down : host_up) + hk * bytes;
+    SMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+    sync();
+}
 
 void Engine::store_alloc(int exp_slots) {
     n_exp_slots = exp_slots;
@@ -31,8 +197,12 @@ void Engine::store_alloc(int exp_slots) {
     for (int s = n_exp_slots - 1; s >= 0; --s) free_slots.push_back(s);
     const size_t ws = wt == kF32 ? 4 : 2;
     const size_t up_b = (size_t)U * d * ws, dn_b = (size_t)d * f * ws, owned = (size_t)M * (e_hi - e_lo);
-    SMOE_CUDA(cudaHostAlloc(&host_up, owned * up_b, cudaHostAllocDefault));
-    SMOE_CUDA(cudaHostAlloc(&host_down, owned * dn_b, cudaHostAllocDefault));
+    if (offload == 2) {
+        ssd.reset(new SsdTier(up_b, dn_b, owned));
+    } else {
+        SMOE_CUDA(cudaHostAlloc(&host_up, owned * up_b, cudaHostAllocDefault));
+        SMOE_CUDA(cudaHostAlloc(&host_down, owned * dn_b, cudaHostAllocDefault));
+    }
     SMOE_CUDA(cudaMallocHost(&h_store, sizeof(int) * ((size_t)M * E + (4 + (size_t)ep_world) * E + 8)));
 }
 
@@ -73,11 +243,9 @@ size_t Engine::expert_bytes(int which) const {
 
 // Copy one expert host -> HBM slot on the copy stream.
 void Engine::store_copy_in(int key, int slot) {
-    const size_t ub = expert_bytes(0), db = expert_bytes(1), hk = hkey(key);
-    SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(up_pool) + (size_t)slot * ub, static_cast<char*>(host_up) + hk * ub,
-                              ub, cudaMemcpyHostToDevice, copy_stream));
-    SMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(down_pool) + (size_t)slot * db,
-                              static_cast<char*>(host_down) + hk * db, db, cudaMemcpyHostToDevice, copy_stream));
+    const size_t ub = expert_bytes(0), db = expert_bytes(1);
+    host_to_device(key, 0, static_cast<char*>(up_pool) + (size_t)slot * ub, copy_stream);
+    host_to_device(key, 1, static_cast<char*>(down_pool) + (size_t)slot * db, copy_stream);
     h2d_bytes += ub + db;
 }
 

@@ -45,7 +45,9 @@ class EngineConfig(C.Structure):
                 ("ffn", C.c_int), ("vocab", C.c_int), ("gate_skew", C.c_double), ("seed", C.c_uint64),
                 ("moe_mask", C.POINTER(C.c_uint8)), ("expert_kind", C.c_int), ("weight_type", C.c_int),
                 ("max_batch", C.c_int), ("max_gamma", C.c_int), ("gemm_backend", C.c_int), ("device", C.c_int),
-                ("offload", C.c_int), ("hbm_expert_slots", C.c_int), ("ep_rank", C.c_int), ("ep_world", C.c_int)]
+                ("offload", C.c_int), ("hbm_expert_slots", C.c_int), ("ep_rank", C.c_int), ("ep_world", C.c_int),
+                ("attn_heads", C.c_int), ("kv_heads", C.c_int), ("head_dim", C.c_int), ("rope_theta", C.c_double),
+                ("max_seq_len", C.c_int)]
 
 
 class RunConfig(C.Structure):
@@ -167,6 +169,12 @@ class ModelSpec:
     seed: int = 0
     moe_mask: list | None = None
     expert_kind: int = TANH2
+    # extension: attn_heads > 0 = real GQA attention with RoPE and a paged KV cache in
+    # place of the reference's prefix-mean + mix surrogate (restated in oracle/specmoe_oracle.c fwd_attn)
+    attn_heads: int = 0
+    kv_heads: int = 0
+    head_dim: int = 0
+    rope_theta: float = 10000.0
 
     @property
     def moe_layers(self) -> int:
@@ -311,7 +319,7 @@ class Engine:
 
     def __init__(self, spec: ModelSpec, weight_type: int = F32, max_batch: int = 8, max_gamma: int = 10,
                  gemm: int = GEMM_AUTO, device: int = 0, offload: int = 0, hbm_expert_slots: int = 0,
-                 ep_rank: int = 0, ep_world: int = 1):
+                 ep_rank: int = 0, ep_world: int = 1, max_seq_len: int = 0):
         self.spec = spec
         L = lib()
         self._mask = None
@@ -320,7 +328,8 @@ class Engine:
         cfg = EngineConfig(spec.num_layers, spec.experts, spec.top_k, spec.hidden, spec.ffn, spec.vocab, spec.gate_skew,
                            spec.seed, C.cast(self._mask, C.POINTER(C.c_uint8)) if self._mask is not None else None,
                            spec.expert_kind, weight_type, max_batch, max_gamma, gemm, device, offload,
-                           hbm_expert_slots, ep_rank, ep_world)
+                           hbm_expert_slots, ep_rank, ep_world, spec.attn_heads, spec.kv_heads, spec.head_dim,
+                           spec.rope_theta, max_seq_len)
         h = C.c_void_p()
         _check(L.smoe_engine_create(C.byref(cfg), C.byref(h)))
         self.h = h
