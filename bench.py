@@ -155,7 +155,7 @@ def forward_macs(s: dict, n_layers: int, mats: int) -> float:
 
 
 def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: int, steps: int = 1,
-                  warmup: int = 0) -> dict:
+                  warmup: int = 0, tau: float | None = None) -> dict:
     """Time the reference's own CPU path on a bounded sample of the workload.
 
     Sample: a one-MoE-layer slice of the shape (full d, f, E, K, V), built by the reference's
@@ -163,7 +163,10 @@ def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: in
     from one reference run_specmoe phase on the slice.  forward() is a per-layer loop, so its time is
     extrapolated to the full depth (and from the reference's 2-matrix expert to SwiGLU's 3) by its
     multiply-add count.  tokens/s = forwards/s * tau / (2*gamma + 1).  With steps > 1 the slice is built
-    once and the concurrent forward is timed `warmup` + `steps` times (median of the timed ones)."""
+    once and the concurrent forward is timed `warmup` + `steps` times (median of the timed ones).
+    `tau`: the acceptance of the full-depth model measured by the B200 arm on the same configuration (the
+    one-layer slice accepts far more drafts than 32 layers of expert substitution do); the slice's own tau
+    is used only when none is given (the reference arm)."""
     from oracle.oracle import LIBS, ModelSpec as OSpec, Oracle, RunCfg as ORun
     from paper_2604_10152_b200.prompts import make_prompts
     kind = "ref" if os.path.exists(LIBS["ref"]) else "port"
@@ -182,19 +185,23 @@ def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: in
     tp = statistics.median(samples)
     sp = m.run_specmoe(ORun(gamma=gamma, n_draft=min(n_draft, full["experts"]), max_new_tokens=gamma + 1,
                             run_seed=0), prompt)
-    tau = sp.metrics["tau_mean"]
+    tau_slice = sp.metrics["tau_mean"]
+    tau_used = tau if tau else tau_slice
     mats = 3 if expert == "swiglu3" else 2
     n_moe = SHAPES[shape]["num_layers"] if "moe_mask" not in SHAPES[shape] else sum(SHAPES[shape]["moe_mask"])
     scale = forward_macs(full, SHAPES[shape]["num_layers"], mats) / forward_macs(full, 1, 2)
     fwd_s_full = tp * scale  # wall of one forward per thread, full depth
-    value = threads * tau / ((2 * gamma + 1) * fwd_s_full)
+    value = threads * tau_used / ((2 * gamma + 1) * fwd_s_full)
+    tau_src = ("the B200 arm's measured tau at full depth" if tau else
+               f"one reference run_specmoe phase on the slice (gamma {gamma})")
     return {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference" if kind == "ref" else "port",
             "sample": (f"{kind} build of a 1-MoE-layer slice of {SHAPE_NAMES[shape]} (tanh2, fp64); "
-                       f"{threads} threads x 1 forward() = {tp:.3f}s (1 thread {t1:.3f}s); tau {tau:.3f} from one "
-                       f"reference run_specmoe phase (gamma {gamma}); extrapolated x{scale:.1f} by forward MACs "
-                       f"to L={n_moe} {expert}; slice build {build_s:.0f}s untimed"),
-            "tau": tau, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale,
-            "step_values": [threads * tau / ((2 * gamma + 1) * t * scale) for t in samples]}
+                       f"{threads} threads x 1 forward() = {tp:.3f}s (1 thread {t1:.3f}s); tau {tau_used:.3f} from "
+                       f"{tau_src}; extrapolated x{scale:.1f} by forward MACs to L={n_moe} {expert}; slice build "
+                       f"{build_s:.0f}s untimed"),
+            "tau": tau_used, "tau_slice": tau_slice, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale,
+            "ondemand_value": threads / fwd_s_full,
+            "step_values": [threads * tau_used / ((2 * gamma + 1) * t * scale) for t in samples]}
 
 
 # ---------------------------------------------------------------- the B200 arm
@@ -467,6 +474,85 @@ def section_shape(a, dev, shape: str, B: int, n_draft: int, pk, skew: float = 0.
     return out
 
 
+def measure_disk_read(dirpath: str, gib: int = 4) -> dict:
+    """Sequential O_DIRECT read bandwidth of the SSD tier's directory: a fresh file, 8 MB reads from 4
+    threads (the store's own reader shape), page cache bypassed (buffered + DONTNEED where O_DIRECT is
+    refused) -- the SSD tier's roofline."""
+    import mmap
+    import threading
+    path = os.path.join(dirpath, f"smoe_diskbench_{os.getpid()}.bin")
+    chunk, n = 8 << 20, (gib << 30) // (8 << 20)
+    buf = mmap.mmap(-1, chunk)
+    buf.write(os.urandom(1 << 20) * 8)
+    flags = os.O_RDWR | os.O_CREAT | os.O_TRUNC
+    try:
+        fd = os.open(path, flags | os.O_DIRECT, 0o600)
+        direct = True
+    except OSError:
+        fd = os.open(path, flags, 0o600)
+        direct = False
+    try:
+        for i in range(n):
+            os.pwritev(fd, [buf], i * chunk)
+        os.fsync(fd)
+        if not direct:
+            os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+        nxt = [0]
+        lock = threading.Lock()
+
+        def reader():
+            b = mmap.mmap(-1, chunk)
+            while True:
+                with lock:
+                    i = nxt[0]
+                    nxt[0] += 1
+                if i >= n:
+                    return
+                os.preadv(fd, [b], i * chunk)
+        t0 = time.perf_counter()
+        th = [threading.Thread(target=reader) for _ in range(4)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        dt = time.perf_counter() - t0
+    finally:
+        os.close(fd)
+        os.unlink(path)
+    return {"read_gbs": n * chunk / dt / 1e9, "o_direct": direct, "bytes": n * chunk, "dir": dirpath}
+
+
+def section_ssd(a, dev: int, B: int = 64, steps: int = 2) -> dict:
+    """The SSD tier (offload = 2): Mixtral-8x7B-shape experts, 4 MoE layers (11.3 GB of experts in one
+    file on local storage, read with O_DIRECT through pinned staging), speculative vs on-demand."""
+    import torch
+    from paper_2604_10152_b200.engine import BF16, SWIGLU3, Engine, ModelSpec, RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    d = os.environ.get("SMOE_SSD_DIR", "/tmp")
+    disk = measure_disk_read(d)
+    spec = ModelSpec(**dict(SHAPES["c2"], num_layers=4), seed=0, expert_kind=SWIGLU3)
+    eng = Engine(spec, weight_type=BF16, max_batch=B, max_gamma=a.gamma, device=dev, offload=2)
+    eng.init_device(0)
+    eng.build_affinity_device()
+    prompts = make_prompts(2000, B, 8, spec.vocab)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", dev))
+    m = spec_measure(eng, stream, RunCfg(gamma=a.gamma, n_draft=a.n_draft, max_new_tokens=1 << 30), prompts,
+                     steps=steps, warmup=1, profile=False)
+    r = m["res"]
+    od = eng.run_ondemand(RunCfg(gamma=a.gamma, max_new_tokens=steps), prompts)
+    direct = eng.counter("ssd_direct")
+    eng.close()
+    hb, hs = r.metrics["h2d_expert_bytes"], r.metrics["h2d_s"]
+    out = {"workload": f"Mixtral-8x7B-shape experts, 4 MoE layers (11.3 GB), SSD tier in {d}, B={B}, gamma={a.gamma}, "
+                       f"N={a.n_draft}", "disk": disk, "engine_o_direct": bool(direct == 1),
+           "tokens_per_s": m["tokens"] / (m["ms"] * 1e-3), "tau": m["tau"],
+           "ssd_to_hbm_gbs": hb / hs / 1e9 if hs else None,
+           "ssd_frac_of_disk_read": (hb / hs / 1e9) / disk["read_gbs"] if hs and disk["read_gbs"] else None,
+           "ondemand_tokens_per_s": od.metrics["tokens_total"] / od.metrics["gpu_s"],
+           "pcie_bytes_per_token": hb / max(1, m["tokens"]),
+           "ondemand_bytes_per_token": od.metrics["h2d_expert_bytes"] / max(1, od.metrics["tokens_total"])}
+    out["speedup_vs_ondemand"] = out["tokens_per_s"] / out["ondemand_tokens_per_s"]
+    return out
+
+
 def run_b200(a) -> None:
     import torch
     rank, world, local = dist_env()
@@ -624,10 +710,15 @@ def run_b200(a) -> None:
             line["offload_c3"] = offload_section(a, local, a.offload_batch, a.offload_steps, 1, gammas=(2, 4, 8))
         except Exception as ex:
             line["offload_c3"] = {"error": str(ex)[:300]}
+    if not a.no_offload_section and world == 1 and default_sections:
+        try:
+            line["offload_ssd"] = section_ssd(a, local)
+        except Exception as ex:
+            line["offload_ssd"] = {"error": str(ex)[:300]}
     if not a.no_cpu_baseline and world == 1:
         thr = a.cpu_threads or os.cpu_count()
         try:
-            line["cpu_baseline"] = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr)
+            line["cpu_baseline"] = cpu_reference(a.shape, a.expert, a.gamma, a.n_draft, thr, tau=line["tau"])
         except Exception as ex:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     print(json.dumps(line), flush=True)

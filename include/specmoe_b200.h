@@ -167,7 +167,8 @@ int smoe_counters(smoe_engine* e, uint64_t* launches, double* alg_expert_bytes, 
 
 /* Named counters since the last smoe_counters(reset): "alg_expert_bytes:draft" / ":verify" (the split of
  * alg_expert_bytes by pass kind) and "expert_flops:draft" / ":verify" (2 * (U*d + d*f) per routed
- * (row, pick) on this rank's experts).  Unknown names read 0. */
+ * (row, pick) on this rank's experts).  "ssd_direct": 1 when the SSD tier reads with O_DIRECT, 0 buffered,
+ * -1 no SSD tier.  Unknown names read 0. */
 int smoe_counter(smoe_engine* e, const char* name, double* value);
 
 /* Expert GEMMs timed alone (bench.py roofline): T tokens routed round-robin over every expert of

@@ -88,13 +88,23 @@ __device__ __forceinline__ long long kv_off(const int* ptab, int maxp, int b, in
     return ((((page * L + l) * 2 + kv) * Hkv + h) * kPage + p % kPage) * (long long)hd;
 }
 
-// qkv = sum_s P[s][r] (s in order); RoPE (rotate-half, angle p * theta^(-2j/hd), float64 angle) on the
-// Hq query and Hkv key heads; q -> qbuf, k/v -> the cache page of (b, p).
+// RoPE table: rope[p][j] = (cos, sin) of p * theta^(-2j/hd), evaluated in float64 and rounded once.
+__global__ void k_rope_table(int npos, int half, int hd, double theta, float2* __restrict__ rope) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npos * half; i += gridDim.x * blockDim.x) {
+        const int p = i / half, j = i % half;
+        double sn, cs;
+        sincos((double)p * pow(theta, -2.0 * j / hd), &sn, &cs);
+        rope[i] = make_float2((float)cs, (float)sn);
+    }
+}
+
+// qkv = sum_s P[s][r] (s in order); RoPE (rotate-half with the table) on the Hq query and Hkv key heads;
+// q -> qbuf, k/v -> the cache page of (b, p).
 template <typename KT>
-__global__ void k_qkv_rope(const float* __restrict__ P, int S, long long pstride, int Hq, int Hkv, int hd, double theta,
-                           const int* __restrict__ row_seq, const int* __restrict__ row_pos,
-                           const int* __restrict__ ptab, int maxp, int l, int L, float* __restrict__ qbuf,
-                           KT* __restrict__ kv) {
+__global__ void k_qkv_rope(const float* __restrict__ P, int S, long long pstride, int Hq, int Hkv, int hd,
+                           const float2* __restrict__ rope, const int* __restrict__ row_seq,
+                           const int* __restrict__ row_pos, const int* __restrict__ ptab, int maxp, int l, int L,
+                           float* __restrict__ qbuf, KT* __restrict__ kv) {
     pdl_wait();
     pdl_trigger();
     const int r = blockIdx.x, b = row_seq[r], p = row_pos[r];
@@ -110,9 +120,8 @@ __global__ void k_qkv_rope(const float* __restrict__ P, int S, long long pstride
         const int h = i / half, j = i % half;
         const int c0 = h * hd + j;  // heads are contiguous: q heads, then k heads
         const float x0 = sum(c0), x1 = sum(c0 + half);
-        double sn, cs;
-        sincos((double)p * pow(theta, -2.0 * j / hd), &sn, &cs);
-        const float c = (float)cs, s = (float)sn;
+        const float2 cs = rope[(long long)p * half + j];
+        const float c = cs.x, s = cs.y;
         const float y0 = x0 * c - x1 * s, y1 = x1 * c + x0 * s;
         if (h < Hq) {
             qbuf[(long long)r * QD + c0] = y0;
@@ -131,7 +140,11 @@ __global__ void k_qkv_rope(const float* __restrict__ P, int S, long long pstride
 
 // One CTA per (row, kv head), one warp per query head of the group: scores q.k_t / sqrt(hd) over
 // t = 0..p (lane-strided, each dot product in dimension order), max-subtracted exp, a butterfly sum,
-// then o = sum_t (e_t / sum) v_t in position order (lanes over dimensions).  o -> the Wo GEMM operand.
+// then o = sum_t (e_t / sum) v_t in position order (lanes over dimensions).  The K and V rows of the
+// sequence are staged in shared memory kAttnChunk positions at a time with coalesced 16-byte loads (the
+// CTA's warps share them); every per-lane loop keeps its order, so the result does not depend on the
+// staging.  o -> the Wo GEMM operand.
+constexpr int kAttnChunk = 64;
 template <typename KT, typename OT>
 __global__ void k_attn(const float* __restrict__ qbuf, int Hq, int Hkv, int hd, const int* __restrict__ row_seq,
                        const int* __restrict__ row_pos, const int* __restrict__ ptab, int maxp, int l, int L,
@@ -141,20 +154,36 @@ __global__ void k_attn(const float* __restrict__ qbuf, int Hq, int Hkv, int hd, 
     extern __shared__ float sm[];
     const int r = blockIdx.x, kh = blockIdx.y, b = row_seq[r], p = row_pos[r];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, G = Hq / Hkv, h = kh * G + w;
-    float* sq = sm + (size_t)w * hd;                       // this warp's query [hd]
-    float* sc = sm + (size_t)G * hd + (size_t)w * max_pos;  // its scores / weights [p + 1]
+    float* sq = sm + (size_t)w * hd;                        // this warp's query [hd]
+    float* sc = sm + (size_t)G * hd + (size_t)w * max_pos;   // its scores / weights [p + 1]
+    KT* stg = reinterpret_cast<KT*>(sm + (size_t)G * hd + (size_t)G * max_pos);  // [kAttnChunk][hd] K or V rows
     const int QD = Hq * hd;
     for (int j = lane; j < hd; j += 32) sq[j] = qbuf[(long long)r * QD + (long long)h * hd + j];
-    __syncwarp();
+    // cooperative staging of positions [t0, t0 + n) of the k (kv = 0) or v (kv = 1) rows of this kv head:
+    // a page holds kKvPage consecutive positions of one (layer, k|v, head) contiguously
+    const int vec = 16 / (int)sizeof(KT), hv = hd / vec;  // 16-byte vectors per row
+    auto stage = [&](int kvsel, int t0, int n) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < n * hv; i += blockDim.x) {
+            const int t = t0 + i / hv, c = i % hv;
+            const KT* src = kv + kv_off<KT>(ptab, maxp, b, t, l, L, kvsel, kh, Hkv, hd);
+            reinterpret_cast<uint4*>(stg + (size_t)(t - t0) * hd)[c] = reinterpret_cast<const uint4*>(src)[c];
+        }
+        __syncthreads();
+    };
     const float inv = 1.0f / sqrtf((float)hd);
     float mx = -INFINITY;
-    for (int t = lane; t <= p; t += 32) {
-        const KT* kt = kv + kv_off<KT>(ptab, maxp, b, t, l, L, 0, kh, Hkv, hd);
-        float s = 0.f;
-        for (int j = 0; j < hd; ++j) s = fmaf(sq[j], to_f(kt[j]), s);
-        s *= inv;
-        sc[t] = s;
-        mx = fmaxf(mx, s);
+    for (int t0 = 0; t0 <= p; t0 += kAttnChunk) {
+        const int n = min(kAttnChunk, p + 1 - t0);
+        stage(0, t0, n);
+        for (int t = t0 + lane; t < t0 + n; t += 32) {
+            const KT* kt = stg + (size_t)(t - t0) * hd;
+            float s = 0.f;
+            for (int j = 0; j < hd; ++j) s = fmaf(sq[j], to_f(kt[j]), s);
+            s *= inv;
+            sc[t] = s;
+            mx = fmaxf(mx, s);
+        }
     }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float part = 0.f;
@@ -164,12 +193,24 @@ __global__ void k_attn(const float* __restrict__ qbuf, int Hq, int Hkv, int hd, 
         part += e;
     }
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    __syncwarp();
-    for (int j = lane; j < hd; j += 32) {
-        float acc = 0.f;
-        for (int t = 0; t <= p; ++t) acc = fmaf(sc[t] / part, to_f(kv[kv_off<KT>(ptab, maxp, b, t, l, L, 1, kh, Hkv, hd) + j]), acc);
-        store_op<OT>(out, (long long)r * QD + (long long)h * hd + j, acc);
+    constexpr int kMaxDims = 8;  // hd <= 256: dimensions j = lane + 32 i of this lane
+    float acc[kMaxDims];
+#pragma unroll
+    for (int i = 0; i < kMaxDims; ++i) acc[i] = 0.f;
+    for (int t0 = 0; t0 <= p; t0 += kAttnChunk) {
+        const int n = min(kAttnChunk, p + 1 - t0);
+        stage(1, t0, n);
+        for (int t = t0; t < t0 + n; ++t) {
+            const float wgt = sc[t] / part;
+            const KT* vt = stg + (size_t)(t - t0) * hd;
+#pragma unroll
+            for (int i = 0; i < kMaxDims; ++i)
+                if (lane + 32 * i < hd) acc[i] = fmaf(wgt, to_f(vt[lane + 32 * i]), acc[i]);
+        }
     }
+#pragma unroll
+    for (int i = 0; i < kMaxDims; ++i)
+        if (lane + 32 * i < hd) store_op<OT>(out, (long long)r * QD + (long long)h * hd + lane + 32 * i, acc[i]);
 }
 
 }  // namespace
@@ -187,16 +228,22 @@ void launch_x0_tok_rms(const double* emb64, const int* seq_len, const int* last_
                  row_seq, row_extra, extra_uniform, rtok, rpos, d, x, row_plen, row_pos, xa);
 }
 
+void launch_rope_table(int npos, int hd, double theta, float2* rope, cudaStream_t s) {
+    launch_k(k_rope_table, 128, 256, 0, s, npos, hd / 2, hd, theta, rope);
+}
+
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
     if (a.T <= 0) return;
+    if (a.hd > 256 || a.hd % 8) throw Error(kConfig, "attention: head_dim must be a multiple of 8, at most 256");
     if (a.kvt == kF32)
-        launch_k(k_qkv_rope<float>, a.T, 256, 0, s, a.P, a.S, a.pstride, a.Hq, a.Hkv, a.hd, a.theta, a.row_seq,
+        launch_k(k_qkv_rope<float>, a.T, 256, 0, s, a.P, a.S, a.pstride, a.Hq, a.Hkv, a.hd, a.rope, a.row_seq,
                  a.row_pos, a.ptab, a.maxp, a.layer, a.L, a.qbuf, reinterpret_cast<float*>(a.kv));
     else
-        launch_k(k_qkv_rope<__nv_bfloat16>, a.T, 256, 0, s, a.P, a.S, a.pstride, a.Hq, a.Hkv, a.hd, a.theta, a.row_seq,
-                 a.row_pos, a.ptab, a.maxp, a.layer, a.L, a.qbuf, reinterpret_cast<__nv_bfloat16*>(a.kv));
+        launch_k(k_qkv_rope<__nv_bfloat16>, a.T, 256, 0, s, a.P, a.S, a.pstride, a.Hq, a.Hkv, a.hd, a.rope,
+                 a.row_seq, a.row_pos, a.ptab, a.maxp, a.layer, a.L, a.qbuf, reinterpret_cast<__nv_bfloat16*>(a.kv));
     const int G = a.Hq / a.Hkv;
-    const size_t sm = sizeof(float) * ((size_t)G * a.hd + (size_t)G * a.max_pos);
+    const size_t kvb = a.kvt == kF32 ? 4 : 2;
+    const size_t sm = sizeof(float) * ((size_t)G * a.hd + (size_t)G * a.max_pos) + (size_t)kAttnChunk * a.hd * kvb;
     const dim3 grid(a.T, a.Hkv);
     if (a.kvt == kF32)
         launch_k(k_attn<float, float>, grid, 32 * G, sm, s, (const float*)a.qbuf, a.Hq, a.Hkv, a.hd, a.row_seq,

@@ -315,6 +315,10 @@ int smoe_profile_reset(smoe_engine* h) {
 }
 int smoe_counter(smoe_engine* h, const char* name, double* value) {
     return guarded([&] {
+        if (std::strcmp(name, "ssd_direct") == 0) {  // the SSD tier reads with O_DIRECT (1) or buffered (0)
+            *value = h->e->ssd_direct();
+            return;
+        }
         auto it = h->e->named.find(name);
         *value = it == h->e->named.end() ? 0.0 : it->second;
     });

@@ -161,6 +161,8 @@ Engine::Engine(const smoe_engine_config& c) {
         SMOE_CUDA(cudaMemset(ptab, 0, sizeof(int) * Bmax * maxp));
         last_tok = dalloc<int>(Bmax);
         row_pos = dalloc<int>(Tmax);
+        rope = dalloc<float2>((size_t)maxp * kKvPage * (hd / 2));
+        launch_rope_table(maxp * kKvPage, hd, theta, rope, stream);
         pre_tok = dalloc<int>(Tmax);
         pre_pos = dalloc<int>(Tmax);
         kv_pages.assign(Bmax, {});
@@ -284,7 +286,7 @@ Engine::~Engine() {
     for (void* q : ep_ipc_opened) cudaIpcCloseMemHandle(q);
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
     fr(ep_flags); fr(ep_peer);
-    fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos);
+    fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos); fr(rope);
     fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(comb_ctr); fr(scratch64); fr(pass_ctr);
@@ -917,7 +919,7 @@ void Engine::attn_layer(int l, int T, const int* rseq) {
          kEpiStoreF32, "dense_gemm", (double)QKVD * d * ws, s_qkv, (long long)Tmax * QKVD);
     {
         ProfScope ps(*this, "attention");
-        AttnArgs a{pqkv, s_qkv, (long long)Tmax * QKVD, T, Hq, Hkv, hd, theta, rseq, row_pos, ptab, maxp, l, L,
+        AttnArgs a{pqkv, s_qkv, (long long)Tmax * QKVD, T, Hq, Hkv, hd, rope, rseq, row_pos, ptab, maxp, l, L,
                    qbuf, kv, wt, maxp * kKvPage, attn_o};
         launch_attention(a, stream);
     }

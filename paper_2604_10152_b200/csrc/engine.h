@@ -174,6 +174,7 @@ public:
     };
     std::unique_ptr<struct SsdTier, SsdDeleter> ssd;
     void host_to_device(int key, int which, void* dst, cudaStream_t s);   // which: 0 up/w1w3, 1 down
+    double ssd_direct() const;  // -1: no SSD tier; 1: O_DIRECT; 0: buffered reads
     void device_to_host(int key, int which, const void* src);             // (synchronous)
     void* host_up = nullptr;    // [M*eo][U][d] pinned: this rank's experts (eo = E / ep_world), hkey order
     void* host_down = nullptr;  // [M*eo][d][f] pinned
@@ -309,6 +310,7 @@ public:
     int* ptab = nullptr;     // [Bmax][maxp] page table
     int* last_tok = nullptr; // [Bmax] last committed token (the input of the next row)
     int* row_pos = nullptr;  // [Tmax] position of each row of the pass
+    float2* rope = nullptr;  // [maxp * kKvPage][hd/2] RoPE (cos, sin)
     int* pre_tok = nullptr;  // [Tmax] prefill rows: explicit tokens and positions
     int* pre_pos = nullptr;
     bool prefill_rows = false;

@@ -155,7 +155,7 @@ struct AttnArgs {
     int S;
     long long pstride;
     int T, Hq, Hkv, hd;
-    double theta;
+    const float2* rope;  // [positions][hd/2] (cos, sin), launch_rope_table
     const int *row_seq, *row_pos, *ptab;
     int maxp, layer, L;
     float* qbuf;   // [Tmax][Hq*hd]
@@ -165,5 +165,6 @@ struct AttnArgs {
     void* out;     // [Tmax][Hq*hd] -> the Wo GEMM operand
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+void launch_rope_table(int npos, int hd, double theta, float2* rope, cudaStream_t s);
 
 }  // namespace smoe

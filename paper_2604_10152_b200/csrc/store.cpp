@@ -165,6 +165,7 @@ struct SsdTier {
 };
 
 void Engine::SsdDeleter::operator()(SsdTier* t) const { delete t; }
+double Engine::ssd_direct() const { return ssd ? (ssd->direct ? 1.0 : 0.0) : -1.0; }
 
 void Engine::host_to_device(int key, int which, void* dst, cudaStream_t s) {
     const size_t bytes = expert_bytes(which), hk = hkey(key);
