@@ -58,6 +58,7 @@ def args_parse():
     p.add_argument("--gamma", type=int, default=4)
     p.add_argument("--n-draft", type=int, default=0, help="0: the shape's default (4; 8 for C4, SURVEY 8)")
     p.add_argument("--e2e-tokens", type=int, default=128, help="new tokens per sequence of the e2e run (SURVEY 8d: 128)")
+    p.add_argument("--skew", type=float, default=0.0, help="gate_skew of the headline model (SPEC: 0 uniform)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--offload", action="store_true", help="headline = C3 (experts in pinned host DRAM)")
@@ -582,7 +583,7 @@ def run_b200(a) -> None:
             print(json.dumps(line), flush=True)
         return
     shp = dict(SHAPES[a.shape])
-    spec = ModelSpec(**shp, seed=0, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
+    spec = ModelSpec(**shp, seed=0, gate_skew=a.skew, expert_kind=SWIGLU3 if a.expert == "swiglu3" else TANH2)
     ep = world > 1 and not a.replicas  # N > 1: experts sharded over the GPUs, rows split
     default_sections = world == 1 and a.shape == "c2" and not a.no_sections
     eng = c2_engine(a, spec, local, a.batch, max(a.gamma, 8 if default_sections else a.gamma), rank, world, ep)

@@ -74,6 +74,8 @@ struct TcParams {
     int stages, b_region;  // host layout (single-group launches): stage count, token bytes per stage
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
     int pair_ok;           // grouped launches: phases (bit 0 up, bit 1 down) that may use pair units
+    int pair_big;          // grouped launches: pair units also for groups of 129..256 tokens (both TMEM buffers)
+    int pair_min_units;    // grouped launches: the first phase pairs only if that leaves >= this many units
     int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
     int* sched;            // [3]: next-unit counter, finished-CTA counter, L2 prefetch chunk counter (self-resetting)
     const uint8_t* pf;     // prefetched into L2 by the producers that run out of units (the launch's tail)
@@ -88,7 +90,7 @@ struct TcParams {
 // Timeline instrumentation (tools/tc_trace.py; variant builds only): per launch, per unit
 // {cta, t_claim, t_tma_done, t_mma_first, t_mma_done, t_epi_done} and per CTA {t_start, t_end}, globaltimer ns.
 constexpr int kTrLaunches = 192, kTrUnits = 8192, kTrCtas = 160;
-struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done, epi_start; };
+struct TrUnit { long long cta, claim, tma_done, mma_first, mma_done, epi_done, epi_start, epi_stored, epi_fenced, epi_barred; };
 __device__ TrUnit g_tr_unit[kTrLaunches][kTrUnits];
 __device__ long long g_tr_cta[kTrLaunches][kTrCtas][2];
 __device__ long long g_tr_cta_dep[kTrLaunches][kTrCtas];  // after the grouped launch's dependency wait
@@ -147,7 +149,10 @@ __device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Pl
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) {
-        const int pair = p.pair_ok && mx <= BN_MAX / 2 ? p.pair_ok : 0;
+        int pair = p.pair_ok && (mx <= BN_MAX / 2 || p.pair_big) ? p.pair_ok : 0;
+        // few groups (a draft pass: N experts): paired first-phase units may not cover the SMs, and every
+        // such unit is on the first -> second phase critical path; unpaired units halve it
+        if ((pair & 1) && n * row_tiles(p.ph[0], 1) * p.ph[0].splits < p.pair_min_units) pair &= ~1;
         const int stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
         plan->n_items = n;
         plan->pair = pair;
@@ -201,6 +206,7 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, const int16_t* it
     w.n_valid = min(BN_MAX, r1 - w.n0);
     w.m0 = mt * (pair ? 2 * BM : BM);
     w.pair = pair;
+    w.big = pair && w.n_valid > BN_MAX / 2;
     w.ks = ks;
     w.kb0 = ks * P.kb_per_split;
     w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
@@ -418,13 +424,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (!p.group_cnt) dep_wait(p);
         if (lane == 0) {  // ---------------- MMA issuer
-            int it = 0, cnt = 0, cons = 0;
+            // TMEM = two 256-column accumulator buffers used alternately (epilogue of one unit overlaps the
+            // MMAs of the next); a big pair unit (two tiles x up to 256 tokens) takes both
+            // (bit a of `par`: phase parity of buffer a, kept in a register)
+            int it = 0, nb = 0, cons = 0;
+            uint32_t par = 0;
             Unit w;
             while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, false, w, pair)) {
-                const int acc = cnt & 1;
-                mbar_wait(&acc_empty[acc], (uint32_t)(((cnt >> 1) & 1) ^ 1));
+                const int acc = w.big ? 0 : nb;
+                mbar_wait(&acc_empty[acc], ((par >> acc) & 1) ^ 1);
+                if (w.big) mbar_wait(&acc_empty[1], ((par >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_MAX);
+                const uint32_t d_tile1 = d_tmem + (uint32_t)(w.big ? BN_MAX : BM);  // pair units' second tile
                 const int nmma = (w.n_valid + 15) & ~15;
                 const uint32_t idesc = idesc_bf16(BM, nmma);
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
@@ -441,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int kk = 0; kk < BK / 16; ++kk) {
                             const uint32_t accum = (kb > w.kb0 || kk) ? 1u : 0u;
                             mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc, accum);
-                            mma_bf16(d_tmem + BM, smem_desc(a_base + kABytes + kk * 32), smem_desc(b_base + kk * 32),
+                            mma_bf16(d_tile1, smem_desc(a_base + kABytes + kk * 32), smem_desc(b_base + kk * 32),
                                      idesc, accum);
                         }
                     } else {
@@ -453,25 +465,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&acc_full[acc]);
+                if (w.big) {
+                    mma_commit(&acc_full[1]);
+                    par ^= 3u;
+                } else {
+                    par ^= 1u << acc;
+                    nb ^= 1;
+                }
                 TR(g_tr_unit[trs][w.id % kTrUnits].mma_done = gtimer();)
-                ++cnt;
             }
         }
         __syncwarp();
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
         if (!p.group_cnt) dep_wait(p);
         const int q = warp & 3;
-        int cnt = 0, cons = 0;
+        int nb = 0, cons = 0;
+        uint32_t par = 0;
         Unit w;
         while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, true, w, pair)) {
-            const int acc = cnt & 1;
-            mbar_wait(&acc_full[acc], (uint32_t)((cnt >> 1) & 1));
+            const int acc = w.big ? 0 : nb;  // the MMA issuer's buffer sequence
+            mbar_wait(&acc_full[acc], (par >> acc) & 1);
+            if (w.big) mbar_wait(&acc_full[1], (par >> 1) & 1);
             tc_fence_after();
             TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_start = gtimer();)
             const Phase& P = p.ph[w.phase];
             for (int h = 0; h < (w.pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
                 const int row = w.m0 + h * BM + q * 32 + lane;  // weight row within the slot
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * BM);
+                const uint32_t taddr =
+                    tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * (w.big ? BN_MAX : BM));
+#ifndef SMOE_EPI32_MIN
+#define SMOE_EPI32_MIN 16
+#endif
+                if (EPI0 == kEpiSwiglu && w.phase == 0 && w.n_valid > SMOE_EPI32_MIN) {
+                    for (int c = 0; c < w.n_valid; c += 32) {  // 32 columns per step (tmem buffer is 256 wide)
+                        uint32_t v[32];
+                        tmem_ld16(taddr + c, v);
+                        tmem_ld16(taddr + c + 16, v + 16);
+                        tmem_wait_ld();
+                        epilogue_swiglu32(P, w, row, lane, c, v);
+                    }
+                    continue;
+                }
                 for (int c = 0; c < w.n_valid; c += 16) {
                     uint32_t v[16];
                     tmem_ld16(taddr + c, v);
@@ -480,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else epilogue_store<EPI1>(P, w, row, lane, c, v);
                 }
             }
+            TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_stored = gtimer();)
             tc_fence_before();
             if (p.nphase > 1 && w.phase == 0) {
                 // publish: all four warps' stores of this unit (ordered before the async-proxy reads of the
@@ -487,7 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // barrier, so the other warps' stores are covered without each warp draining its stores
                 // through a full fence.sc (which waited microseconds behind the weight stream)
                 proxy_fence_async();
+                TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_fenced = gtimer();)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_barred = gtimer();)
 #ifdef SMOE_PUBLISH_FENCE_SC
                 if (warp == 2 && lane == 0) {
                     __threadfence();
@@ -499,9 +536,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (lane == 0) {
+                mbar_arrive(&acc_empty[acc]);
+                if (w.big) mbar_arrive(&acc_empty[1]);
+            }
+            if (w.big) {
+                par ^= 3u;
+            } else {
+                par ^= 1u << acc;
+                nb ^= 1;
+            }
             TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_done = gtimer();)
-            ++cnt;
         }
     }
     if (p.nphase > 1 && p.ph[1].peer_y) __threadfence_system();  // peer stores performed before the grid ends
@@ -629,6 +674,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
     if (a.group_cnt && (long long)p.G * p.n_tiles > kMaxItems)
         throw Error(kInvariant, "tcgen05 GEMM: more (group, token tile) items than the plan holds");
+
     constexpr int kCtrl = 1024;  // control block (barriers, unit ring, TMEM slot) + alignment slack below
     static const bool pair_env = [] {
         const char* v = getenv("SMOE_TC_PAIR");
@@ -644,6 +690,16 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     }();
     // grouped launches: bit 0 pairs the first phase, bit 1 the second (applied when the counts allow)
     p.pair_ok = a.group_cnt && pair_env ? (1 | (b && pair_down_env ? 2 : 0)) : 0;
+    static const int pair_big_env = [] {
+        const char* v = getenv("SMOE_TC_PAIR_BIG");
+        return v ? atoi(v) : 1;
+    }();
+    static const int pair_min_env = [] {  // 0: always pair (measured: unpaired units are slower even when
+        const char* v = getenv("SMOE_TC_PAIR_MIN");  // the paired ones leave SMs idle, C4 draft 0.44 -> 0.40)
+        return v ? atoi(v) : 0;
+    }();
+    p.pair_big = pair_big_env;
+    p.pair_min_units = pair_min_env;
     // single-group launches pair only when that does not load the busiest SM with more weight bytes
     // (the C2 Mix launch at T=64 would run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us; the head
     // at T=64, 250 units = 2 waves of 1 MB, becomes 1 wave of 2 MB paired units)

@@ -153,7 +153,36 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 struct Unit {
     int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks, id;
     int pair;  // two 128-row tiles (gemm_tc.cu pair units)
+    int big;   // pair unit of more than 128 tokens: its two accumulators take both TMEM buffers
 };
+
+// SwiGLU over a 32-column TMEM chunk (two x16 loads in flight).  Rows 2i / 2i+1 of the slot hold w1 / w3 of
+// feature i: lanes 2i and 2i+1 split the chunk's tokens (even lane: tokens 0-15, odd lane: 16-31), trading the
+// half they do not finish through one shuffle per token, so every lane computes 16 independent silu products
+// (the 16-column form left the odd lanes idle and ran one dependent MUFU chain per token on the even lanes).
+// Same fast-intrinsic formula per element as epilogue_store<kEpiSwiglu> (bit-identical H).
+__device__ __forceinline__ void epilogue_swiglu32(const Phase& P, const Unit& w, int row, int lane, int c,
+                                                  const uint32_t* v) {
+    const bool odd = lane & 1;
+    float a[16], b[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float mine_keep = __uint_as_float(odd ? v[16 + j] : v[j]);
+        const float mine_send = __uint_as_float(odd ? v[j] : v[16 + j]);
+        const float other = __shfl_xor_sync(0xffffffffu, mine_send, 1);
+        a[j] = odd ? other : mine_keep;  // w1 (even row)
+        b[j] = odd ? mine_keep : other;  // w3 (odd row)
+    }
+    if (row >= P.Nrows) return;
+    const int t0 = c + (odd ? 16 : 0);
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(P.Y) + (long long)(w.n0 + t0) * P.ldy + (row >> 1);
+    float h[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) h[j] = __fdividef(a[j], 1.0f + __expf(-a[j])) * b[j];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        if (t0 + j < w.n_valid) y[(long long)j * P.ldy] = __float2bfloat16_rn(h[j]);
+}
 
 // One 16-column TMEM chunk of a finished accumulator -> the phase's output.
 template <int EPI>

@@ -20,22 +20,25 @@ SHAPES = {
     # E=64 at d=1024: 1024-thread gate tree (4-CTA clusters), gate weights too large to stage
     "e64_d1024": (ModelSpec(num_layers=3, experts=64, top_k=6, hidden=1024, ffn=512, vocab=512,
                             expert_kind=SWIGLU3, moe_mask=[0, 1, 1], gate_skew=0.5), 8),
+    # B=64 verify passes of 320 rows over 4 experts: groups of > 128 tokens (big pair units)
+    "e4_b64": (ModelSpec(num_layers=2, experts=4, top_k=2, hidden=1024, ffn=512, vocab=512,
+                         expert_kind=SWIGLU3, gate_skew=1.0), 2, 64),
 }
 
 
-def digest(spec, nd):
+def digest(spec, nd, batch=8):
     h = hashlib.sha256()
-    e = Engine(spec, weight_type=BF16, max_batch=8, max_gamma=4).init_device(3)
+    e = Engine(spec, weight_type=BF16, max_batch=batch, max_gamma=4).init_device(3)
     for prefix in ([1, 2, 3], list(range(40)), [100] * 9):
         lg, raw, fin = e.forward(prefix)
         for a in (lg, raw, fin):
             h.update(np.ascontiguousarray(a).tobytes())
     e.build_affinity_device()
-    r = e.run_specmoe(RunCfg(gamma=4, n_draft=nd, max_new_tokens=24), make_prompts(11, 8, 8, spec.vocab))
+    r = e.run_specmoe(RunCfg(gamma=4, n_draft=nd, max_new_tokens=24), make_prompts(11, batch, 8, spec.vocab))
     h.update(json.dumps([r.tokens, [list(x) for x in r.ledger]]).encode())
     e.close()
     return h.hexdigest()
 
 
 if __name__ == "__main__":
-    print(json.dumps({k: digest(s, nd) for k, (s, nd) in SHAPES.items()}))
+    print(json.dumps({k: digest(*v) for k, v in SHAPES.items()}))

@@ -18,6 +18,8 @@ import numpy as np
 sys.path.insert(0, ".")
 
 D, F = 4096, 14336
+NF = 10  # TrUnit fields: cta, claim, tma_done, mma_first, mma_done, epi_done, epi_start, epi_stored, epi_fenced,
+# epi_barred
 UP_UNIT = 128 * D * 2  # 128 weight rows x K=d bf16
 
 
@@ -80,7 +82,7 @@ def analyze(path):
     off += nl * 16
     cta = np.frombuffer(raw[off:off + nl * nc * 2 * 8], np.int64).reshape(nl, nc, 2)
     off += nl * nc * 16
-    un = np.frombuffer(raw[off:off + nl * nu * 7 * 8], np.int64).reshape(nl, nu, 7)
+    un = np.frombuffer(raw[off:off + nl * nu * NF * 8], np.int64).reshape(nl, nu, NF)
     rows = []
     for s in range(nl):
         total, nphase, u0, grid = (int(v) for v in meta[s])
@@ -190,8 +192,8 @@ def dump_units(path, rows, dst, per_kind=3):
     off = 12 + nl * 16
     cta = np.frombuffer(raw[off:off + nl * nc * 2 * 8], np.int64).reshape(nl, nc, 2)
     off += nl * nc * 16
-    un = np.frombuffer(raw[off:off + nl * nu * 7 * 8], np.int64).reshape(nl, nu, 7)
-    off += nl * nu * 7 * 8
+    un = np.frombuffer(raw[off:off + nl * nu * NF * 8], np.int64).reshape(nl, nu, NF)
+    off += nl * nu * NF * 8
     dep = np.frombuffer(raw[off:off + nl * nc * 8], np.int64).reshape(nl, nc)
     out, seen = [], {}
     for r in rows:
@@ -208,7 +210,7 @@ def dump_units(path, rows, dst, per_kind=3):
         ids = np.nonzero(m)[0]
         U = un[s, m]
         units = [[int(U[i, 0] & 0xFFFFFFFF)] + [round((int(U[i, j]) - t0) / 1e3, 2) for j in range(1, 6)] + [int(ids[i])]
-                 + [round((int(U[i, 6]) - t0) / 1e3, 2)]
+                 + [round((int(U[i, j]) - t0) / 1e3, 2) if U[i, j] else None for j in range(6, NF)]
                  for i in range(len(U))]
         ends = [round((int(x) - t0) / 1e3, 2) for x in cta[s, :r["grid"], 1]]
         deps = [round((int(x) - t0) / 1e3, 2) for x in dep[s, :r["grid"]]]
