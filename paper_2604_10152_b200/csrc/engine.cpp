@@ -795,6 +795,8 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
         up.dep_ctr = moe_dep;
         up.dep_target = gate_epoch;
     }
+    up.pred_groups = pred_groups;
+    up.n_pred = n_pred;
     if (peer_y) {
         dn.peer_y = peer_y;
         dn.peer_eo = E / ep_world;
@@ -878,7 +880,17 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                 l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
                 l2_next_bytes = (long long)d * d * (long long)ws;
             }
+            static const bool pf_pred = [] {
+                const char* v = getenv("SMOE_PF_PRED");
+                return !(v && v[0] == '0');
+            }();
+            if (restricted && !fetch && pf_pred) {
+                pred_groups = draft_sorted + (size_t)mo * E;
+                n_pred = cur_n_draft;
+            }
             expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
+            pred_groups = nullptr;
+            n_pred = 0;
             l2_next = nullptr;
             moe_dep = nullptr;
             if (fetch) store_finish_layer(mo);

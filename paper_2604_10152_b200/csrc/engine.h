@@ -57,6 +57,10 @@ struct TcGemmArgs {
     // instead of the previous grid's completion (nullptr: griddepcontrol.wait)
     const unsigned* dep_ctr = nullptr;
     unsigned dep_target = 0;
+    // grouped launches of draft passes: the groups expected to have rows (device, ascending), whose first
+    // weight boxes are prefetched into L2 before the dependency wait
+    const int* pred_groups = nullptr;
+    int n_pred = 0;
 };
 void launch_gemm_tc(const TcGemmArgs& a, cudaStream_t s);
 // One launch for a MoE layer's grouped up- (tanh / SwiGLU) and down-projection (f32 split partials):
@@ -228,6 +232,8 @@ public:
     void* hbuf = nullptr;   // [E*Tmax][f]
     float* ybuf = nullptr;  // [s_down][E*Tmax][d] split-K partials of the down projection
     const void* l2_next = nullptr;  // next layer's Mix weights, prefetched into L2 in the MoE launch's tail
+    const int* pred_groups = nullptr;  // draft passes: this layer's draft experts (fused MoE launch prefetch)
+    int n_pred = 0;
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
     int s_mix = 1, s_down = 1;
     float* logits = nullptr;  // [Tmax][V]

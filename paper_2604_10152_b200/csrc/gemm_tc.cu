@@ -84,6 +84,10 @@ struct TcParams {
     unsigned dep_target;
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
+    // draft passes: the groups the launch will most likely have (the layer's draft experts, ascending);
+    // before the dependency wait each CTA pulls the first pf_kb weight boxes of "its" predicted unit into L2
+    const int* pred;
+    int n_pred, pf_kb;
 };
 
 #ifdef SMOE_TC_TRACE
@@ -263,6 +267,36 @@ __device__ __forceinline__ void dep_wait(const TcParams& p) {
     proxy_fence_async();  // the producer kernel's generic stores before this launch's TMA reads
 }
 
+// Draft passes: while the CTAs wait for the gate (HBM is idle then), prefetch into L2 the first weight
+// boxes of the first wave of units as they will be enumerated if every predicted group has rows (the
+// claims are dynamic, so CTA b warms unit b for whichever CTA takes it).  A wrong guess costs only
+// bandwidth that was idle.
+__device__ __forceinline__ void prefetch_predicted(const TcParams& p, const WeightMaps& mapA0, const WeightMaps& mapA1) {
+    int u = blockIdx.x;
+    int ph = 0;
+    const int pr0 = p.pair_ok & 1, pr1 = (p.pair_ok >> 1) & 1;
+    const int up_units = p.n_pred * row_tiles(p.ph[0], pr0) * p.ph[0].splits;
+    if (u >= up_units) {
+        if (p.nphase < 2) return;
+        u -= up_units;
+        ph = 1;
+    }
+    const Phase& P = p.ph[ph];
+    const int pair = ph ? pr1 : pr0;
+    const int mtu = row_tiles(P, pair);
+    const int ks = u % P.splits;
+    u /= P.splits;
+    const int mt = u % mtu, item = u / mtu;
+    if (item >= p.n_pred) return;
+    const int g = p.pred[item];
+    const int slot = g >= 0 && g < p.G ? p.group_slot[g] : -1;
+    if (slot < 0) return;
+    const CUtensorMap* map = ph ? &mapA1.m[pair] : &mapA0.m[pair];
+    const int arow = (int)((long long)slot * P.a_rows_per_slot + mt * (pair ? 2 * BM : BM));
+    const int kb0 = ks * P.kb_per_split, kb1 = min(P.num_kb, min(kb0 + P.kb_per_split, kb0 + p.pf_kb));
+    for (int kb = kb0; kb < kb1; ++kb) tma_prefetch_2d(map, kb * BK, arow);
+}
+
 template <int EPI0, int EPI1>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ WeightMaps mapA0, const __grid_constant__ TokenMaps mapB0,
@@ -329,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.group_cnt) {
         // grouped launches: the unit geometry (rows per expert) is written by the gate kernel that
         // immediately precedes this one, so it may only be read after the dependency wait
+        if (p.pred && threadIdx.x == 0) prefetch_predicted(p, mapA0, mapA1);
         dep_wait(p);
         if (warp == 0) build_plan(p, s_items, plan);
         __syncthreads();
@@ -345,137 +380,173 @@ __global__ void __launch_bounds__(kThreads, 1)
     })
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- scheduler + TMA producer
-            int it = 0;
-            // griddepcontrol.wait done: the previous kernel's outputs are visible (grouped: waited above)
-            bool kernel_dep = p.group_cnt != nullptr;
-            for (int pub = 0;; ++pub) {
-                // dynamic work distribution: claim the next non-empty unit (single-group geometry is
-                // host-known; grouped geometry was waited for above)
-                int u;
-                Unit w;
+        // ---------------- scheduler + TMA producer: like the MMA issuer, the whole warp runs the loop and one
+        // elected lane issues, with the unit's coordinates made warp-uniform (uniform-register TMA operands)
+        int it = 0, ps = 0;
+        uint32_t pph = 0;
+        const int stg = __shfl_sync(0xffffffffu, stages, 0);
+        const uint32_t sbytes = (uint32_t)__shfl_sync(0xffffffffu, stage_bytes, 0);
+        const int a_space = __shfl_sync(0xffffffffu, (pair ? 2 : 1) * kABytes, 0);  // weight bytes of a stage
+        // griddepcontrol.wait done: the previous kernel's outputs are visible (grouped: waited above)
+        bool kernel_dep = p.group_cnt != nullptr;
+        for (int pub = 0;; ++pub) {
+            // dynamic work distribution: claim the next non-empty unit (single-group geometry is
+            // host-known; grouped geometry was waited for above)
+            int u = 0;
+            Unit w;
+            if (lane == 0) {
                 do {
                     u = atomicAdd(&p.sched[0], 1);
                 } while (u < total_units && !decode_unit(p, items, n_items, u, w, pair));
-                TR(if (u < total_units && u < kTrUnits) { g_tr_unit[trs][u].cta = blockIdx.x | ((long long)p.tr << 32); g_tr_unit[trs][u].claim = gtimer(); })
-                const int r = pub % kRing;
-                mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
+            }
+            u = __shfl_sync(0xffffffffu, u, 0);
+            TR(if (lane == 0 && u < total_units && u < kTrUnits) { g_tr_unit[trs][u].cta = blockIdx.x | ((long long)p.tr << 32); g_tr_unit[trs][u].claim = gtimer(); })
+            const int r = pub % kRing;
+            mbar_wait(&ring_empty[r], (uint32_t)(((pub / kRing) & 1) ^ 1));
+            if (lane == 0) {
                 ring[r] = u < total_units ? u : -1;
                 mbar_arrive(&ring_full[r]);
-                if (u >= total_units) {
-                    // out of units: the launch's tail has begun and HBM has spare bandwidth; pull the next
-                    // launch's weights (the next layer's Mix, 32 MB at C2) into L2 in 256 KB chunks
+            }
+            __syncwarp();
+            if (u >= total_units) {
+                // out of units: the launch's tail has begun and HBM has spare bandwidth; pull the next
+                // launch's weights (the next layer's Mix, 32 MB at C2) into L2 in 256 KB chunks
+                if (lane == 0)
                     for (;;) {
                         const long long off = (long long)atomicAdd(&p.sched[2], 1) * kPfChunk;
                         if (off >= p.pf_bytes) break;
                         const uint32_t n = (uint32_t)min((long long)kPfChunk, p.pf_bytes - off);
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf + off), "r"(n) : "memory");
                     }
-                    break;
+                __syncwarp();
+                break;
+            }
+            // lane 0's decode, broadcast (the other lanes' w is unset)
+            const int phase = __shfl_sync(0xffffffffu, w.phase, 0), wp = __shfl_sync(0xffffffffu, w.pair, 0);
+            const int kb0 = __shfl_sync(0xffffffffu, w.kb0, 0), kb1 = __shfl_sync(0xffffffffu, w.kb1, 0);
+            const int n0 = __shfl_sync(0xffffffffu, w.n0, 0), g = __shfl_sync(0xffffffffu, w.g, 0);
+            const int nval = __shfl_sync(0xffffffffu, w.n_valid, 0);
+            const int arow = __shfl_sync(0xffffffffu, (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0), 0);
+            const CUtensorMap* mA = phase ? &mapA1.m[wp] : &mapA0.m[wp];
+            // the unit's tokens as ONE box per stage: the smallest of 32/64/128/256 rows covering them
+            // (one TMA issue per stage; rows past the group are fetched but never multiplied in)
+            const int bi = tok_box_index(nval);
+            const CUtensorMap* mB = phase ? &mapB1.m[bi] : &mapB0.m[bi];
+            const uint32_t bytes = (uint32_t)((wp ? 2 : 1) * kABytes + tok_box_bytes(bi));
+            // Activations may be read once (a) the previous kernel is complete (PDL) and (b) for a
+            // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
+            // boxes are issued; at most `stages` of them are held back.
+            const int need = phase ? phase0_units_of_group(p, g, pair) : 0;
+            bool ready = kernel_dep && (phase == 0 || __shfl_sync(0xffffffffu, ld_relaxed(&p.done[g]), 0) >= need);
+            if (ready && phase) {
+                fence_acquire();
+                proxy_fence_async();
+            }
+            const int pend_it = it;
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                // ring position kept incrementally: the producer's per-stage instruction count is on the
+                // stream's critical path (a runtime it % stages is an emulated division)
+                const int s = ps;
+                const uint32_t sph = pph;
+                if (++ps == stg) {
+                    ps = 0;
+                    pph ^= 1u;
                 }
-                const CUtensorMap* mA = w.phase ? &mapA1.m[w.pair] : &mapA0.m[w.pair];
-                const int a_space = (pair ? 2 : 1) * kABytes;  // weight space of a stage (tokens after it)
-                const int a_bytes = (w.pair ? 2 : 1) * kABytes;  // one 128- or 256-row weight box
-                // the unit's tokens as ONE box per stage: the smallest of 32/64/128/256 rows covering them
-                // (one TMA issue per stage; rows past the group are fetched but never multiplied in)
-                const int bi = tok_box_index(w.n_valid);
-                const CUtensorMap* mB = w.phase ? &mapB1.m[bi] : &mapB0.m[bi];
-                const int arow = (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0);
-                const uint32_t bytes = a_bytes + (uint32_t)tok_box_bytes(bi);
-                // Activations may be read once (a) the previous kernel is complete (PDL) and (b) for a
-                // phase-1 unit, every phase-0 unit of its group has published.  Until then only weight
-                // boxes are issued; at most `stages` of them are held back.
-                const int need = w.phase ? phase0_units_of_group(p, w.g, pair) : 0;
-                bool ready = kernel_dep && (w.phase == 0 || ld_relaxed(&p.done[w.g]) >= need);
-                if (ready && w.phase) {
-                    fence_acquire();
-                    proxy_fence_async();
-                }
-                const int pend_it = it;
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                    const int s = it % stages;
-                    mbar_wait(&empty[s], (uint32_t)(((it / stages) & 1) ^ 1));
-                    uint8_t* st = smem + s * stage_bytes;
+                mbar_wait(&empty[s], sph ^ 1u);
+                uint8_t* st = smem + s * sbytes;
+                if (elect_one()) {
                     mbar_expect_tx(&full[s], bytes);
                     tma_load_2d(mA, &full[s], st, kb * BK, arow);
-                    if (ready) {
-                        tma_load_2d(mB, &full[s], st + a_space, kb * BK, w.n0);
-                        continue;
-                    }
-                    if (it + 1 - pend_it < stages && kb + 1 < w.kb1) continue;  // keep streaming weights
-                    if (!kernel_dep) {
-                        dep_wait(p);
-                        kernel_dep = true;
-                    }
-                    if (w.phase) {
-                        spin_until(&p.done[w.g], need);
-                        proxy_fence_async();  // generic-proxy stores of H before async-proxy (TMA) reads
-                    }
-                    ready = true;
-                    for (int j2 = pend_it; j2 <= it; ++j2) {  // activations of the held-back stages
-                        uint8_t* sp = smem + (j2 % stages) * stage_bytes + a_space;
-                        tma_load_2d(mB, &full[j2 % stages], sp, (w.kb0 + (j2 - pend_it)) * BK, w.n0);
-                    }
+                    if (ready) tma_load_2d(mB, &full[s], st + a_space, kb * BK, n0);
                 }
-                TR(if (u < kTrUnits) g_tr_unit[trs][u].tma_done = gtimer();)
+                __syncwarp();
+                if (ready) continue;
+                if (it + 1 - pend_it < stg && kb + 1 < kb1) continue;  // keep streaming weights
+                if (!kernel_dep) {
+                    dep_wait(p);
+                    kernel_dep = true;
+                }
+                if (phase) {
+                    spin_until(&p.done[g], need);
+                    proxy_fence_async();  // generic-proxy stores of H before async-proxy (TMA) reads
+                }
+                ready = true;
+                if (elect_one())
+                    for (int j2 = pend_it; j2 <= it; ++j2) {  // activations of the held-back stages
+                        uint8_t* sp = smem + (j2 % stg) * sbytes + a_space;
+                        tma_load_2d(mB, &full[j2 % stg], sp, (kb0 + (j2 - pend_it)) * BK, n0);
+                    }
+                __syncwarp();
             }
-            if (!kernel_dep) dep_wait(p);
+            TR(if (lane == 0 && u < kTrUnits) g_tr_unit[trs][u].tma_done = gtimer();)
         }
+        if (!kernel_dep) dep_wait(p);
     } else if (warp == 1) {
         if (!p.group_cnt) dep_wait(p);
-        if (lane == 0) {  // ---------------- MMA issuer
-            // TMEM = two 256-column accumulator buffers used alternately (epilogue of one unit overlaps the
-            // MMAs of the next); a big pair unit (two tiles x up to 256 tokens) takes both
-            // (bit a of `par`: phase parity of buffer a, kept in a register)
-            int it = 0, nb = 0, cons = 0;
-            uint32_t par = 0;
-            Unit w;
-            while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, false, w, pair)) {
-                const int acc = w.big ? 0 : nb;
-                mbar_wait(&acc_empty[acc], ((par >> acc) & 1) ^ 1);
-                if (w.big) mbar_wait(&acc_empty[1], ((par >> 1) & 1) ^ 1);
+        // ---------------- MMA issuer: the whole warp runs the loop convergently and one elected lane issues.
+        // Every operand is made warp-uniform (__shfl_sync from lane 0), so ptxas builds the descriptors in
+        // uniform registers once per stage instead of wrapping each tcgen05.mma in its own elect / R2UR
+        // loop -- this thread's per-stage latency (full barrier -> stage released) is on the stream's
+        // critical path.
+        // TMEM = two 256-column accumulator buffers used alternately (epilogue of one unit overlaps the
+        // MMAs of the next); a big pair unit (two tiles x up to 256 tokens) takes both
+        // (bit a of `par`: phase parity of buffer a)
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        const int stg = __shfl_sync(0xffffffffu, stages, 0);
+        const uint32_t sbytes = (uint32_t)__shfl_sync(0xffffffffu, stage_bytes, 0);
+        const uint32_t bofs = (uint32_t)__shfl_sync(0xffffffffu, (pair ? 2 : 1) * kABytes, 0);
+        const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+        int nb = 0, cons = 0, ms = 0;
+        uint32_t par = 0, mph = 0;
+        Unit w;
+        while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, true, w, pair)) {
+            const int kb0 = __shfl_sync(0xffffffffu, w.kb0, 0), kb1 = __shfl_sync(0xffffffffu, w.kb1, 0);
+            const int wpair = __shfl_sync(0xffffffffu, w.pair, 0), big = __shfl_sync(0xffffffffu, w.big, 0);
+            const int nval = __shfl_sync(0xffffffffu, w.n_valid, 0);
+            const int acc = big ? 0 : nb;
+            mbar_wait(&acc_empty[acc], ((par >> acc) & 1) ^ 1);
+            if (big) mbar_wait(&acc_empty[1], ((par >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tm + (uint32_t)(acc * BN_MAX);
+            const uint32_t d_tile1 = d_tmem + (uint32_t)(big ? BN_MAX : BM);  // pair units' second tile
+            const uint32_t idesc = idesc_bf16(BM, (nval + 15) & ~15);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                const int s = ms;
+                const uint32_t sph = mph;
+                if (++ms == stg) {
+                    ms = 0;
+                    mph ^= 1u;
+                }
+                mbar_wait(&full[s], sph);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_MAX);
-                const uint32_t d_tile1 = d_tmem + (uint32_t)(w.big ? BN_MAX : BM);  // pair units' second tile
-                const int nmma = (w.n_valid + 15) & ~15;
-                const uint32_t idesc = idesc_bf16(BM, nmma);
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-                    const int s = it % stages;
-                    mbar_wait(&full[s], (uint32_t)((it / stages) & 1));
-                    tc_fence_after();
-                    TR(if (kb == w.kb0) g_tr_unit[trs][w.id % kTrUnits].mma_first = gtimer();)
-                    const uint32_t a_base = smem_u32(smem + s * stage_bytes);
-                    const uint32_t b_base = a_base + (pair ? 2 : 1) * kABytes;
-                    // Two straight-line loops, branching once per stage: the single issuing thread's per-MMA
-                    // overhead bounds the stream (a predicated-off second MMA inside one loop cost 30%).
-                    if (w.pair) {  // second 128-row tile of the box -> second accumulator, same tokens
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint32_t accum = (kb > w.kb0 || kk) ? 1u : 0u;
-                            mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc, accum);
-                            mma_bf16(d_tile1, smem_desc(a_base + kABytes + kk * 32), smem_desc(b_base + kk * 32),
-                                     idesc, accum);
-                        }
-                    } else {
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            mma_bf16(d_tmem, smem_desc(a_base + kk * 32), smem_desc(b_base + kk * 32), idesc,
-                                     (kb > w.kb0 || kk) ? 1u : 0u);
-                    }
+                TR(if (kb == kb0 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].mma_first = gtimer();)
+                const uint32_t a_base = sbase + (uint32_t)s * sbytes;
+                // descriptors of the stage's K=16 slices: +32 B of address = +2 in the 14-bit start field
+                // (shared addresses < 256 KB never carry out of it)
+                const uint64_t da = smem_desc(a_base), db = smem_desc(a_base + bofs);
+                static_assert(BK == 64, "mma_stage_*: four K=16 slices per stage");
+                if (elect_one()) {
+                    if (wpair)  // second 128-row tile of the box -> second accumulator, same tokens
+                        mma_stage_pair(d_tmem, d_tile1, da, smem_desc(a_base + kABytes), db, idesc, kb > kb0);
+                    else
+                        mma_stage_single(d_tmem, da, db, idesc, kb > kb0);
                     mma_commit(&empty[s]);
                 }
-                mma_commit(&acc_full[acc]);
-                if (w.big) {
-                    mma_commit(&acc_full[1]);
-                    par ^= 3u;
-                } else {
-                    par ^= 1u << acc;
-                    nb ^= 1;
-                }
-                TR(g_tr_unit[trs][w.id % kTrUnits].mma_done = gtimer();)
+                __syncwarp();
             }
+            if (elect_one()) {
+                mma_commit(&acc_full[acc]);
+                if (big) mma_commit(&acc_full[1]);
+            }
+            __syncwarp();
+            if (big) {
+                par ^= 3u;
+            } else {
+                par ^= 1u << acc;
+                nb ^= 1;
+            }
+            TR(if (lane == 0) g_tr_unit[trs][w.id % kTrUnits].mma_done = gtimer();)
         }
-        __syncwarp();
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
         if (!p.group_cnt) dep_wait(p);
         const int q = warp & 3;
@@ -719,6 +790,15 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
     p.dep_ctr = a.dep_ctr;
     p.dep_target = a.dep_target;
+    static const int pf_kb_env = [] {
+        const char* v = getenv("SMOE_PF_KB");
+        return v ? atoi(v) : 8;
+    }();
+    if (a.group_cnt && a.pred_groups && a.n_pred > 0 && pf_kb_env > 0) {
+        p.pred = a.pred_groups;
+        p.n_pred = a.n_pred;
+        p.pf_kb = pf_kb_env;
+    }
     p.tr = g_launch_no++;
     const size_t smem = a.group_cnt ? (size_t)kSmemBudget : (size_t)p.stages * stage_bytes + kCtrl + 1024;
     const WeightMaps ma0{{tensor_map(a.A, BM), tensor_map(a.A, 2 * BM)}};

@@ -54,8 +54,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Bounded wait: a pipeline bug traps (context error) instead of hanging the GPU.
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
+    if (mbar_try(addr, parity)) return;  // fast path: no clock reads
     uint32_t done = 0;
     const long long t0 = clock64();
     while (true) {
@@ -136,6 +148,52 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(accum)
         : "memory");
+}
+// One 64-K stage of a pair unit in a single asm block: 2 tiles x 4 K=16 slices sharing the token operand
+// (descriptors advance by 2 per slice).  One block lets ptxas move each operand into the uniform
+// registers once instead of wrapping every tcgen05.mma in its own elect / R2UR sequence.
+__device__ __forceinline__ void mma_stage_pair(uint32_t d0, uint32_t d1, uint64_t da, uint64_t da1, uint64_t db,
+                                               uint32_t idesc, uint32_t accum_first) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, c1, c2, c3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 a1, %2, 2;\n\tadd.s64 a2, %2, 4;\n\tadd.s64 a3, %2, 6;\n\t"
+        "add.s64 c1, %3, 2;\n\tadd.s64 c2, %3, 4;\n\tadd.s64 c3, %3, 6;\n\t"
+        "add.s64 b1, %4, 2;\n\tadd.s64 b2, %4, 4;\n\tadd.s64 b3, %4, 6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %5, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c2, b2, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c3, b3, %5, 1;\n\t}"
+        ::"r"(d0), "r"(d1), "l"(da), "l"(da1), "l"(db), "r"(idesc), "r"(accum_first)
+        : "memory");
+}
+__device__ __forceinline__ void mma_stage_single(uint32_t d0, uint64_t da, uint64_t db, uint32_t idesc,
+                                                 uint32_t accum_first) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}"
+        ::"r"(d0), "l"(da), "l"(db), "r"(idesc), "r"(accum_first)
+        : "memory");
+}
+// One lane of a converged warp (the lowest active lane: lane 0 of a full warp, every time).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred)
+        :
+        : "memory");
+    return pred != 0;
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
