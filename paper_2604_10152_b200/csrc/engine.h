@@ -259,7 +259,8 @@ public:
     int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][4]
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
-    int l2_prefetch = 1;         // MoE launch tail prefetches the next Mix weights into L2 (env SMOE_L2_PREFETCH=0: off)
+    int l2_prefetch = 0;         // MoE launch tail prefetches the next Mix weights into L2 (env SMOE_L2_PREFETCH=1; measured
+                                 // slower once the fused MoE stream reached 0.95: it delays the MoE tail more than it saves)
     int gate_flag = 0;           // MoE launch waits on the gate blocks' counter, not the gate grid (env SMOE_GATE_FLAG)
     unsigned* gate_ctr = nullptr;  // device: gate blocks finished (monotonic)
     unsigned gate_epoch = 0;       // host: gate blocks launched so far
