@@ -791,6 +791,14 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
         up.l2_next = l2_next;
         up.l2_next_bytes = l2_next_bytes;
     }
+    static const bool mix_early = [] {  // opt-in: measured neutral (C2 50.6 ms/step either way)
+        const char* v = getenv("SMOE_MIX_EARLY");
+        return v && v[0] == '1';
+    }();
+    if (l2_next && mix_early) {  // next layer's Mix (QKV) weights, during this layer's gate
+        up.l2_early = l2_next;
+        up.l2_early_bytes = l2_next_bytes;
+    }
     if (moe_dep) {
         up.dep_ctr = moe_dep;
         up.dep_target = gate_epoch;

@@ -53,6 +53,9 @@ struct TcGemmArgs {
     // bytes to prefetch into L2 once the launch runs out of units (its tail): the next layer's Mix weights
     const void* l2_next = nullptr;
     long long l2_next_bytes = 0;
+    // grouped launches: bytes prefetched into L2 by the CTAs while they wait for the dependency (HBM idle)
+    const void* l2_early = nullptr;
+    long long l2_early_bytes = 0;
     // grouped launches: wait for *dep_ctr to reach dep_target (the gate blocks' completion count)
     // instead of the previous grid's completion (nullptr: griddepcontrol.wait)
     const unsigned* dep_ctr = nullptr;

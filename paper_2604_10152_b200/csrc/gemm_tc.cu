@@ -88,6 +88,9 @@ struct TcParams {
     // before the dependency wait each CTA pulls the first pf_kb weight boxes of "its" predicted unit into L2
     const int* pred;
     int n_pred, pf_kb;
+    int w_evict_first;         // weight boxes loaded with an L2 evict_first policy
+    const uint8_t* pf_early;   // prefetched into L2 before the dependency wait (the next layer's Mix weights)
+    long long pf_early_bytes;
 };
 
 #ifdef SMOE_TC_TRACE
@@ -364,6 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // grouped launches: the unit geometry (rows per expert) is written by the gate kernel that
         // immediately precedes this one, so it may only be read after the dependency wait
         if (p.pred && threadIdx.x == 0) prefetch_predicted(p, mapA0, mapA1);
+        if (p.pf_early && threadIdx.x == 32) {  // this CTA's slice of the next launch's weights, while HBM idles
+            const long long per = ((p.pf_early_bytes + gridDim.x - 1) / gridDim.x + 255) & ~255ll;
+            for (long long off = (long long)blockIdx.x * per, end = min(p.pf_early_bytes, off + per); off < end;
+                 off += kPfChunk) {
+                const uint32_t n = (uint32_t)min((long long)kPfChunk, end - off);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_early + off), "r"(n) : "memory");
+            }
+        }
         dep_wait(p);
         if (warp == 0) build_plan(p, s_items, plan);
         __syncthreads();
@@ -384,6 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // elected lane issues, with the unit's coordinates made warp-uniform (uniform-register TMA operands)
         int it = 0, ps = 0;
         uint32_t pph = 0;
+        const uint64_t wpol = policy_evict_first();
+        const bool wef = p.w_evict_first != 0;
         const int stg = __shfl_sync(0xffffffffu, stages, 0);
         const uint32_t sbytes = (uint32_t)__shfl_sync(0xffffffffu, stage_bytes, 0);
         const int a_space = __shfl_sync(0xffffffffu, (pair ? 2 : 1) * kABytes, 0);  // weight bytes of a stage
@@ -456,7 +469,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* st = smem + s * sbytes;
                 if (elect_one()) {
                     mbar_expect_tx(&full[s], bytes);
-                    tma_load_2d(mA, &full[s], st, kb * BK, arow);
+                    if (wef) tma_load_2d_hint(mA, &full[s], st, kb * BK, arow, wpol);
+                    else tma_load_2d(mA, &full[s], st, kb * BK, arow);
                     if (ready) tma_load_2d(mB, &full[s], st + a_space, kb * BK, n0);
                 }
                 __syncwarp();
@@ -790,6 +804,13 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
     p.dep_ctr = a.dep_ctr;
     p.dep_target = a.dep_target;
+    static const int wef_env = [] {
+        const char* v = getenv("SMOE_W_EVICT_FIRST");
+        return v ? atoi(v) : 1;
+    }();
+    p.w_evict_first = a.group_cnt && wef_env;  // expert weights: streamed once per pass
+    p.pf_early = static_cast<const uint8_t*>(a.l2_early);
+    p.pf_early_bytes = a.l2_early ? a.l2_early_bytes : 0;
     static const int pf_kb_env = [] {
         const char* v = getenv("SMOE_PF_KB");
         return v ? atoi(v) : 8;
