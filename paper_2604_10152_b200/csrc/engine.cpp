@@ -263,12 +263,20 @@ Engine::Engine(const smoe_engine_config& c) {
     if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
     if (const char* v = getenv("SMOE_GATE_FLAG")) gate_flag = atoi(v) != 0;
     if (const char* v = getenv("SMOE_COMBINE_FLAG")) combine_flag = atoi(v) != 0;
+    {  // tiled expert pools (kernels.h tiled_index): tcgen05 engines whose pool rows come in 256-row tiles
+        const char* v = getenv("SMOE_TILED");
+        const bool want = !(v && v[0] == '0');
+        if (want && use_tc && wt != kF32 && U % 256 == 0 && d % 256 == 0 && d % 64 == 0 && f % 64 == 0) {
+            tile_up = d;
+            tile_dn = f;
+        }
+    }
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
     op_mix = {mix, (long long)L * d, d};
-    op_up = {up_pool, (long long)n_slots * U, d};
-    op_down = {down_pool, (long long)n_slots * d, f};
+    op_up = {up_pool, (long long)n_slots * U, d, tile_up > 0};
+    op_down = {down_pool, (long long)n_slots * d, f, tile_dn > 0};
     op_head = {head, (long long)V, d};
     op_xa = {xa, (long long)Tmax, d};
     op_xperm = {xperm, (long long)seg_rows, d};
@@ -438,14 +446,14 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
     } else if (name == "up" || name == "w1") {
         need((long long)d * f);
         // SwiGLU: w1 feature j -> pool row 2j, w3 feature j -> row 2j+1 (one 128-row tile = 64 features)
-        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, kind == kSwiglu3 ? 2 : 1, 0);
+        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, kind == kSwiglu3 ? 2 : 1, 0, tile_up > 0);
     } else if (name == "w3") {
         need((long long)d * f);
         if (kind != kSwiglu3) throw Error(kConfig, "upload_tensor: w3 needs the swiglu3 expert kind");
-        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, 2, 1);
+        launch_convert_transpose(stage(n), d, f, up_dst(), wt, stream, 2, 1, tile_up > 0);
     } else if (name == "down" || name == "w2") {
         need((long long)f * d);
-        launch_convert_transpose(stage(n), f, d, down_dst(), wt, stream);
+        launch_convert_transpose(stage(n), f, d, down_dst(), wt, stream, 1, 0, tile_dn > 0);
     } else {
         throw Error(kConfig, "upload_tensor: unknown tensor " + name);
     }
@@ -542,30 +550,30 @@ void Engine::init_device(uint64_t s) {
             for (int e = e_lo; e < e_hi; ++e) {
                 const int key = m * E + e, slot = h_slot_of[key];
                 launch_fill_normal(static_cast<char*>(up_pool) + (size_t)slot * U * d * ws, wt, (long long)U * d, sd, s,
-                                   tid_up, stream, (long long)key * U * d);
+                                   tid_up, stream, (long long)key * U * d, tile_up);
                 launch_fill_normal(static_cast<char*>(down_pool) + (size_t)slot * d * f * ws, wt, (long long)d * f, sd,
-                                   s, tid_down, stream, (long long)key * d * f);
+                                   s, tid_down, stream, (long long)key * d * f, tile_dn);
             }
         for (int l = 0, k = 0; l < L; ++l)
             if (!mask[l]) {
                 const long long gi = (long long)(M * E + k);
                 launch_fill_normal(static_cast<char*>(up_pool) + (size_t)dense_slot[l] * U * d * ws, wt, (long long)U * d,
-                                   sd, s, tid_up, stream, gi * U * d);
+                                   sd, s, tid_up, stream, gi * U * d, tile_up);
                 launch_fill_normal(static_cast<char*>(down_pool) + (size_t)dense_slot[l] * d * f * ws, wt,
-                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f);
+                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f, tile_dn);
                 ++k;
             }
     } else if (!offload) {
-        launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid_up, stream);
-        launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid_down, stream);
+        launch_fill_normal(up_pool, wt, (long long)n_slots * U * d, sd, s, tid_up, stream, 0, tile_up);
+        launch_fill_normal(down_pool, wt, (long long)n_slots * d * f, sd, s, tid_down, stream, 0, tile_dn);
     } else {
         // identical values to the HBM-resident layout (element index = key*U*d + j), staged per expert;
         // under expert parallelism only this rank's experts
         const size_t ws = wt == kF32 ? 4 : 2;
         for (int key = 0; key < M * E; ++key) {
             if (!owns(key)) continue;
-            launch_fill_normal(stage_up, wt, (long long)U * d, sd, s, tid_up, stream, (long long)key * U * d);
-            launch_fill_normal(stage_down, wt, (long long)d * f, sd, s, tid_down, stream, (long long)key * d * f);
+            launch_fill_normal(stage_up, wt, (long long)U * d, sd, s, tid_up, stream, (long long)key * U * d, tile_up);
+            launch_fill_normal(stage_down, wt, (long long)d * f, sd, s, tid_down, stream, (long long)key * d * f, tile_dn);
             device_to_host(key, 0, stage_up);
             device_to_host(key, 1, stage_down);
         }
@@ -573,9 +581,9 @@ void Engine::init_device(uint64_t s) {
             if (!mask[l]) {
                 const long long gi = (long long)(M * E + k);
                 launch_fill_normal(static_cast<char*>(up_pool) + (size_t)dense_slot[l] * U * d * ws, wt, (long long)U * d,
-                                   sd, s, tid_up, stream, gi * U * d);
+                                   sd, s, tid_up, stream, gi * U * d, tile_up);
                 launch_fill_normal(static_cast<char*>(down_pool) + (size_t)dense_slot[l] * d * f * ws, wt,
-                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f);
+                                   (long long)d * f, sd, s, tid_down, stream, gi * d * f, tile_dn);
                 ++k;
             }
     }
@@ -620,9 +628,9 @@ void Engine::build_affinity_device() {
             for (int e = 0; e < E; ++e) {
                 const long long key = (long long)m * E + e;
                 launch_fill_normal(static_cast<char*>(tmp_up) + (size_t)e * U * d * ws, wt, (long long)U * d, sd, dev_seed,
-                                   4, stream, key * U * d);
+                                   4, stream, key * U * d, tile_up);
                 launch_fill_normal(static_cast<char*>(tmp_down) + (size_t)e * d * f * ws, wt, (long long)d * f, sd,
-                                   dev_seed, 5, stream, key * d * f);
+                                   dev_seed, 5, stream, key * d * f, tile_dn);
             }
             upload_ints(group_slot, ident.data(), E);
             slots = group_slot;

@@ -30,6 +30,7 @@ struct TcOperand {
     const void* base;  // bf16, row-major [rows][K]
     long long rows;
     int K;
+    bool tiled = false;  // [rows/256][K/64][256][64] chunks (kernels.h tiled_index): a 3D tensor map
 };
 struct TcGemmArgs {
     TcOperand A;        // weight pool, 2D [slots*rows_per_slot, K]
@@ -239,6 +240,7 @@ public:
     int n_pred = 0;
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
     int s_mix = 1, s_down = 1;
+    int tile_up = 0, tile_dn = 0;  // tiled expert pools: their K (d, f); 0 = row-major (kernels.h tiled_index)
     float* logits = nullptr;  // [Tmax][V]
     int* amax = nullptr;
     uint8_t* in_draft = nullptr;  // [M][E]

@@ -297,7 +297,10 @@ __device__ __forceinline__ void prefetch_predicted(const TcParams& p, const Weig
     const CUtensorMap* map = ph ? &mapA1.m[pair] : &mapA0.m[pair];
     const int arow = (int)((long long)slot * P.a_rows_per_slot + mt * (pair ? 2 * BM : BM));
     const int kb0 = ks * P.kb_per_split, kb1 = min(P.num_kb, min(kb0 + P.kb_per_split, kb0 + p.pf_kb));
-    for (int kb = kb0; kb < kb1; ++kb) tma_prefetch_2d(map, kb * BK, arow);
+    for (int kb = kb0; kb < kb1; ++kb) {
+        if (P.tiled) tma_prefetch_3d(map, arow & 255, (arow >> 8) * P.num_kb + kb);
+        else tma_prefetch_2d(map, kb * BK, arow);
+    }
 }
 
 template <int EPI0, int EPI1>
@@ -440,6 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n0 = __shfl_sync(0xffffffffu, w.n0, 0), g = __shfl_sync(0xffffffffu, w.g, 0);
             const int nval = __shfl_sync(0xffffffffu, w.n_valid, 0);
             const int arow = __shfl_sync(0xffffffffu, (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0), 0);
+            const int wtiled = p.ph[phase].tiled;
+            const int tc1 = arow & 255, tc2 = (arow >> 8) * p.ph[phase].num_kb;  // tiled-layout box coordinates
             const CUtensorMap* mA = phase ? &mapA1.m[wp] : &mapA0.m[wp];
             // the unit's tokens as ONE box per stage: the smallest of 32/64/128/256 rows covering them
             // (one TMA issue per stage; rows past the group are fetched but never multiplied in)
@@ -469,8 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* st = smem + s * sbytes;
                 if (elect_one()) {
                     mbar_expect_tx(&full[s], bytes);
-                    if (wef) tma_load_2d_hint(mA, &full[s], st, kb * BK, arow, wpol);
-                    else tma_load_2d(mA, &full[s], st, kb * BK, arow);
+                    if (wtiled) {
+                        if (wef) tma_load_3d_hint(mA, &full[s], st, tc1, tc2 + kb, wpol);
+                        else tma_load_3d(mA, &full[s], st, tc1, tc2 + kb);
+                    } else {
+                        if (wef) tma_load_2d_hint(mA, &full[s], st, kb * BK, arow, wpol);
+                        else tma_load_2d(mA, &full[s], st, kb * BK, arow);
+                    }
                     if (ready) tma_load_2d(mB, &full[s], st + a_space, kb * BK, n0);
                 }
                 __syncwarp();
@@ -677,14 +687,27 @@ EncodeTiledFn encode_fn() {
 
 const CUtensorMap& tensor_map(const TcOperand& op, int box_rows) {
     static std::mutex mu;
-    static std::map<std::tuple<const void*, long long, int, int>, CUtensorMap> cache;
+    static std::map<std::tuple<const void*, long long, int, int, bool>, CUtensorMap> cache;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(op.base, op.rows, op.K, box_rows);
+    auto key = std::make_tuple(op.base, op.rows, op.K, box_rows, op.tiled);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     EncodeTiledFn fn = encode_fn();
     if (!fn) throw Error(kCuda, "cuTensorMapEncodeTiled entry point unavailable");
     CUtensorMap m;
+    if (op.tiled) {  // [rows/256 * K/64] chunks of [256][64]: box {64, box_rows, 1} = one contiguous 16 / 32 KB piece
+        if (op.rows % 256 || op.K % 64 || box_rows > 256)
+            throw Error(kInvariant, "tcgen05 GEMM: tiled operand needs rows % 256 == 0 and K % 64 == 0");
+        cuuint64_t dims[3] = {64, 256, (cuuint64_t)(op.rows / 256) * (cuuint64_t)(op.K / 64)};
+        cuuint64_t strides[2] = {128, 32768};
+        cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(op.base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled (3D) failed: " + std::to_string((int)r));
+        return cache.emplace(key, m).first->second;
+    }
     cuuint64_t dims[2] = {(cuuint64_t)op.K, (cuuint64_t)op.rows};
     cuuint64_t strides[1] = {(cuuint64_t)op.K * 2};
     cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
@@ -723,6 +746,8 @@ Phase make_phase(const TcGemmArgs& a) {
     P.peer_eo = a.peer_eo;
     P.peer_me = a.peer_me;
     P.peer_seg = a.seg;
+    P.tiled = a.A.tiled ? 1 : 0;
+    if (P.tiled && a.a_rows_per_slot % 256) throw Error(kInvariant, "tcgen05 GEMM: tiled slots need 256-row multiples");
     return P;
 }
 }  // namespace tc

@@ -576,9 +576,9 @@ __device__ __forceinline__ double normal_at(uint64_t seed, uint64_t tid, long lo
 }
 
 template <typename T>
-__global__ void k_fill_normal(T* dst, long long n, double sd, uint64_t seed, uint64_t tid, long long idx0) {
+__global__ void k_fill_normal(T* dst, long long n, double sd, uint64_t seed, uint64_t tid, long long idx0, int tile_k) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        dst[i] = from_f<T>((float)(sd * normal_at(seed, tid, idx0 + i)));
+        dst[tile_k ? tiled_index(i / tile_k, i % tile_k, tile_k) : i] = from_f<T>((float)(sd * normal_at(seed, tid, idx0 + i)));
 }
 __global__ void k_fill_normal_f64(double* dst, long long n, double sd, uint64_t seed, uint64_t tid) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -587,7 +587,7 @@ __global__ void k_fill_normal_f64(double* dst, long long n, double sd, uint64_t 
 
 template <typename T>
 __global__ void k_convert_transpose(const double* __restrict__ src, int rows, int cols, T* __restrict__ dst, int mul,
-                                    int off) {
+                                    int off, int tiled) {
     __shared__ double tile[32][33];
     int c = blockIdx.x * 32 + threadIdx.x;
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -598,7 +598,10 @@ __global__ void k_convert_transpose(const double* __restrict__ src, int rows, in
     int r = blockIdx.y * 32 + threadIdx.x;
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         int cc = blockIdx.x * 32 + j;
-        if (r < rows && cc < cols) dst[((long long)cc * mul + off) * rows + r] = from_f<T>((float)tile[threadIdx.x][j]);
+        if (r < rows && cc < cols) {
+            const long long orow = (long long)cc * mul + off;
+            dst[tiled ? tiled_index(orow, r, rows) : orow * rows + r] = from_f<T>((float)tile[threadIdx.x][j]);
+        }
     }
 }
 template <typename T>
@@ -740,11 +743,11 @@ void launch_commit(double* seq_sum, int* seq_len, const double* emb64, const int
 }
 
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
-                        cudaStream_t s, long long index0) {
+                        cudaStream_t s, long long index0, int tile_k) {
     int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
     if (grid <= 0) return;
-    if (t == kF32) k_fill_normal<float><<<grid, 256, 0, s>>>((float*)dst, n, stddev, seed, tensor_id, index0);
-    else k_fill_normal<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst, n, stddev, seed, tensor_id, index0);
+    if (t == kF32) k_fill_normal<float><<<grid, 256, 0, s>>>((float*)dst, n, stddev, seed, tensor_id, index0, tile_k);
+    else k_fill_normal<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst, n, stddev, seed, tensor_id, index0, tile_k);
 }
 void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
                             cudaStream_t s) {
@@ -754,10 +757,10 @@ void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t se
 }
 
 void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s, int mul,
-                              int off) {
+                              int off, bool tiled) {
     dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32)), block(32, 8);
-    if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst, mul, off);
-    else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst, mul, off);
+    if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst, mul, off, (int)tiled);
+    else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst, mul, off, (int)tiled);
 }
 void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s) {
     int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);

@@ -115,14 +115,24 @@ void launch_gemm_simt(const GemmArgs& a, WType wt, cudaStream_t s);
 // Device init / conversion helpers.
 // Counter-based N(0, stddev) fill; element i of dst draws the variate of global index index0 + i, so
 // a tensor filled in pieces equals the tensor filled at once.
+// tile_k > 0: dst is an expert pool region in the tiled layout (tiled_index below) with K = tile_k; the
+// values are those of the row-major fill (the variate of logical element i lands at tiled_index(i)).
 void launch_fill_normal(void* dst, WType t, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
-                        cudaStream_t s, long long index0 = 0);
+                        cudaStream_t s, long long index0 = 0, int tile_k = 0);
 void launch_fill_normal_f64(double* dst, long long n, double stddev, uint64_t seed, uint64_t tensor_id,
                             cudaStream_t s);
 // dst[c*mul+off][r] = (T)src[r][c] for a rows x cols float64 source (reference row-major -> K-major;
 // mul=2 interleaves the SwiGLU w1/w3 rows).
 void launch_convert_transpose(const double* src, int rows, int cols, void* dst, WType t, cudaStream_t s,
-                              int mul = 1, int off = 0);
+                              int mul = 1, int off = 0, bool tiled = false);
+
+// Tiled expert-pool layout of the tcgen05 engines (engine.h `tiled`): the pool [rows][K] is stored as
+// [rows/256][K/64] chunks of 256 rows x 64 columns, each chunk 32 KB contiguous, so one TMA weight box of a
+// pair unit is one contiguous DRAM stream instead of 256 pieces of 128 B at a K*2-byte stride
+// (tools/bw_probe2.cu: 7.40 vs 7.01 TB/s at K=4096 on 148 SMs, 7.41 vs 6.77 on 88).  Needs rows % 256 == 0.
+__host__ __device__ __forceinline__ long long tiled_index(long long row, long long k, int K) {
+    return (((row >> 8) * (K >> 6) + (k >> 6)) << 14) + ((row & 255) << 6) + (k & 63);
+}
 void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s);
 void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
 
