@@ -106,6 +106,16 @@ Engine::Engine(const smoe_engine_config& c) {
     else if (c.gemm_backend == SMOE_GEMM_TCGEN05) use_tc = 1;
     else use_tc = wt == kBF16 ? 1 : 0;
     if (use_tc && wt != kBF16) throw Error(kConfig, "engine: the tcgen05 path needs bf16 weights");
+    {  // tiled weight layout (kernels.h tiled_index) for tcgen05 engines, per matrix whose rows come in 256s
+        const char* v = getenv("SMOE_TILED");
+        const bool want = use_tc && !(v && v[0] == '0');
+        if (want && U % 256 == 0 && d % 256 == 0 && f % 64 == 0) {
+            tile_up = d;
+            tile_dn = f;
+        }
+        tile_mix = want && d % 256 == 0;
+        tile_head = want && V % 256 == 0 && d % 64 == 0;
+    }
 
     SMOE_CUDA(cudaSetDevice(device));
     SMOE_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -168,8 +178,10 @@ Engine::Engine(const smoe_engine_config& c) {
         kv_pages.assign(Bmax, {});
         for (int pg = (int)n_pages - 1; pg >= 0; --pg) kv_free.push_back(pg);
         h_seq_len.assign(Bmax, 0);
-        op_wqkv = {wqkv, (long long)L * QKVD, d};
-        op_wo = {wo, (long long)L * d, QD};
+        tile_qkv = tile_mix && QKVD % 256 == 0;
+        tile_wo = tile_mix && QD % 64 == 0;
+        op_wqkv = {wqkv, (long long)L * QKVD, d, tile_qkv};
+        op_wo = {wo, (long long)L * d, QD, tile_wo};
         op_ao = {attn_o, (long long)Tmax, QD};
     }
     seq_sum = dalloc<double>((size_t)Bmax * d);
@@ -263,21 +275,14 @@ Engine::Engine(const smoe_engine_config& c) {
     if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
     if (const char* v = getenv("SMOE_GATE_FLAG")) gate_flag = atoi(v) != 0;
     if (const char* v = getenv("SMOE_COMBINE_FLAG")) combine_flag = atoi(v) != 0;
-    {  // tiled expert pools (kernels.h tiled_index): tcgen05 engines whose pool rows come in 256-row tiles
-        const char* v = getenv("SMOE_TILED");
-        const bool want = !(v && v[0] == '0');
-        if (want && use_tc && wt != kF32 && U % 256 == 0 && d % 256 == 0 && d % 64 == 0 && f % 64 == 0) {
-            tile_up = d;
-            tile_dn = f;
-        }
-    }
+
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
 
-    op_mix = {mix, (long long)L * d, d};
+    op_mix = {mix, (long long)L * d, d, tile_mix};
     op_up = {up_pool, (long long)n_slots * U, d, tile_up > 0};
     op_down = {down_pool, (long long)n_slots * d, f, tile_dn > 0};
-    op_head = {head, (long long)V, d};
+    op_head = {head, (long long)V, d, tile_head};
     op_xa = {xa, (long long)Tmax, d};
     op_xperm = {xperm, (long long)seg_rows, d};
     if (xrecv) op_xrecv = {xrecv, (long long)seg_rows, d};
@@ -420,21 +425,24 @@ void Engine::upload_tensor(const std::string& name, int layer, int expert, const
         h2d(emb64, src, sizeof(double) * n);
     } else if (name == "head") {
         need((long long)d * V);
-        launch_convert_transpose(stage(n), d, V, head, wt, stream);
+        launch_convert_transpose(stage(n), d, V, head, wt, stream, 1, 0, tile_head);
     } else if (name == "mix") {
         need((long long)d * d);
         if (attn()) throw Error(kConfig, "upload_tensor: an attention model has no mix (wq/wk/wv/wo)");
-        launch_convert(stage(n), n, at(mix, (size_t)layer * d * d), wt, stream);
+        if (tile_mix) launch_convert(stage(n), n, mix, wt, stream, d, (long long)layer * d);
+        else launch_convert(stage(n), n, at(mix, (size_t)layer * d * d), wt, stream);
     } else if (name == "wq" || name == "wk" || name == "wv" || name == "wo") {
         if (!attn()) throw Error(kConfig, "upload_tensor: " + name + " needs an attention model");
         if (layer < 0 || layer >= L) throw Error(kConfig, "upload_tensor: layer out of range");
         if (name == "wo") {
             need((long long)d * QD);
-            launch_convert(stage(n), n, at(wo, (size_t)layer * d * QD), wt, stream);
+            if (tile_wo) launch_convert(stage(n), n, wo, wt, stream, QD, (long long)layer * d);
+            else launch_convert(stage(n), n, at(wo, (size_t)layer * d * QD), wt, stream);
         } else {
             const int row0 = name == "wq" ? 0 : name == "wk" ? QD : QD + KD;
             need((long long)(name == "wq" ? QD : KD) * d);
-            launch_convert(stage(n), n, at(wqkv, ((size_t)layer * QKVD + row0) * d), wt, stream);
+            if (tile_qkv) launch_convert(stage(n), n, wqkv, wt, stream, d, (long long)layer * QKVD + row0);
+            else launch_convert(stage(n), n, at(wqkv, ((size_t)layer * QKVD + row0) * d), wt, stream);
         }
     } else if (name == "gate") {
         need((long long)d * E);
@@ -534,11 +542,11 @@ void Engine::init_device(uint64_t s) {
     uint64_t tid = 1;
     launch_fill_normal_f64(emb64, (long long)V * d, sd, s, tid++, stream);
     if (attn()) {  // tensor ids 7, 8 (after the head's): the other tensors keep their streams
-        launch_fill_normal(wqkv, wt, (long long)L * QKVD * d, sd, s, 7, stream);
-        launch_fill_normal(wo, wt, (long long)L * d * QD, sd, s, 8, stream);
+        launch_fill_normal(wqkv, wt, (long long)L * QKVD * d, sd, s, 7, stream, 0, tile_qkv ? d : 0);
+        launch_fill_normal(wo, wt, (long long)L * d * QD, sd, s, 8, stream, 0, tile_wo ? QD : 0);
         ++tid;
     } else {
-        launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream);
+        launch_fill_normal(mix, wt, (long long)L * d * d, sd, s, tid++, stream, 0, tile_mix ? d : 0);
     }
     launch_fill_normal(gate_w, kF32, (long long)M * E * d, sd, s, tid++, stream);
     const uint64_t tid_up = tid++, tid_down = tid++;
@@ -587,7 +595,7 @@ void Engine::init_device(uint64_t s) {
                 ++k;
             }
     }
-    launch_fill_normal(head, wt, (long long)V * d, sd, s, tid++, stream);
+    launch_fill_normal(head, wt, (long long)V * d, sd, s, tid++, stream, 0, tile_head ? d : 0);
     SMOE_CUDA(cudaGetLastError());
     sync();
     have_affinity = false;

@@ -241,6 +241,7 @@ public:
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
     int s_mix = 1, s_down = 1;
     int tile_up = 0, tile_dn = 0;  // tiled expert pools: their K (d, f); 0 = row-major (kernels.h tiled_index)
+    bool tile_mix = false, tile_head = false, tile_qkv = false, tile_wo = false;  // tiled dense matrices
     float* logits = nullptr;  // [Tmax][V]
     int* amax = nullptr;
     uint8_t* in_draft = nullptr;  // [M][E]

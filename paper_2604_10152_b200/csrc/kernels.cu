@@ -605,9 +605,9 @@ __global__ void k_convert_transpose(const double* __restrict__ src, int rows, in
     }
 }
 template <typename T>
-__global__ void k_convert(const double* __restrict__ src, long long n, T* __restrict__ dst) {
+__global__ void k_convert(const double* __restrict__ src, long long n, T* __restrict__ dst, int tile_k, long long row0) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        dst[i] = from_f<T>((float)src[i]);
+        dst[tile_k ? tiled_index(row0 + i / tile_k, i % tile_k, tile_k) : i] = from_f<T>((float)src[i]);
 }
 
 template <typename T>
@@ -762,11 +762,11 @@ void launch_convert_transpose(const double* src, int rows, int cols, void* dst, 
     if (t == kF32) k_convert_transpose<float><<<grid, block, 0, s>>>(src, rows, cols, (float*)dst, mul, off, (int)tiled);
     else k_convert_transpose<__nv_bfloat16><<<grid, block, 0, s>>>(src, rows, cols, (__nv_bfloat16*)dst, mul, off, (int)tiled);
 }
-void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s) {
+void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s, int tile_k, long long row0) {
     int grid = (int)std::min<long long>(148LL * 16, (n + 255) / 256);
     if (grid <= 0) return;
-    if (t == kF32) k_convert<float><<<grid, 256, 0, s>>>(src, n, (float*)dst);
-    else k_convert<__nv_bfloat16><<<grid, 256, 0, s>>>(src, n, (__nv_bfloat16*)dst);
+    if (t == kF32) k_convert<float><<<grid, 256, 0, s>>>(src, n, (float*)dst, tile_k, row0);
+    else k_convert<__nv_bfloat16><<<grid, 256, 0, s>>>(src, n, (__nv_bfloat16*)dst, tile_k, row0);
 }
 void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s) {
     launch_convert(src, n, dst, kF32, s);

@@ -133,7 +133,9 @@ void launch_convert_transpose(const double* src, int rows, int cols, void* dst, 
 __host__ __device__ __forceinline__ long long tiled_index(long long row, long long k, int K) {
     return (((row >> 8) * (K >> 6) + (k >> 6)) << 14) + ((row & 255) << 6) + (k & 63);
 }
-void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s);
+// tile_k > 0: dst is a tiled matrix base and element i lands at tiled_index(row0 + i / tile_k, i % tile_k)
+void launch_convert(const double* src, long long n, void* dst, WType t, cudaStream_t s, int tile_k = 0,
+                    long long row0 = 0);
 void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStream_t s);
 
 // Pairwise L2 distance of expert weights (drafting.cpp:28-57) accumulated in float64:
