@@ -444,7 +444,7 @@ def section_gamma(eng, stream, a, spec, pk, gamma: int, B: int) -> dict:
            "tensor_target": "north_star: expert GEMMs >= 60% of tcgen05 peak at batch >= 32; verify-pass AI here is "
                             f"{r.get('verify', {}).get('flop_per_byte', 0):.0f} flop/B vs the ridge "
                             f"{pk['bf16_tflops'] * 1e3 / pk['hbm_gbs']:.0f}"}
-    prof = os.path.join(ROOT, "profiles", "r03_ncu_gamma8_verify.json")
+    prof = os.path.join(ROOT, "profiles", "r04_ncu_gamma8_verify.json")
     if os.path.exists(prof):
         out["ncu_verify_launch"] = json.load(open(prof)).get("launches", [None])[0]
     return out
@@ -632,12 +632,12 @@ def run_b200(a) -> None:
     roof_alg = "distinct (layer, expert) touched per pass x 3*d*f*2 B (swiglu3 bf16)"
     traffic, traffic_src = None, "no committed capture for this configuration"
     if a.shape == "c2" and a.batch == 64 and a.gamma == 4:
-        traffic = ncu_traffic(a.gamma, "r03_ncu_fused_moe.json")
-        traffic_src = ("ncu --set full, profiles/r03_ncu_fused_moe.json: dram read+write of one draft-pass and one "
+        traffic = ncu_traffic(a.gamma, "r04_ncu_fused_moe.json")
+        traffic_src = ("ncu --set full, profiles/r04_ncu_fused_moe.json: dram read+write of one draft-pass and one "
                        "verify-pass launch, weighted gamma:1 like the step (committed capture of this kernel)")
     elif a.shape == "c4" and a.batch == 32 and a.gamma == 4:
-        traffic = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
-        traffic_src = "ncu --set full, profiles/r03_ncu_c4_moe.json (committed capture), weighted gamma:1"
+        traffic = ncu_traffic(a.gamma, "r04_ncu_c4_moe.json")
+        traffic_src = "ncu --set full, profiles/r04_ncu_c4_moe.json (committed capture), weighted gamma:1"
     achieved = alg_bytes / (dom["ms"] * 1e-3) / 1e9 if dom["ms"] > 0 else 0.0
     ep_mode = os.environ.get("SMOE_EP_MODE", "p2p")
     exch = ("gate/down-projection epilogues store rows into peer memory over NVLink (fused dispatch/combine)"
@@ -705,7 +705,7 @@ def run_b200(a) -> None:
             except Exception as ex:
                 line[key] = {"error": str(ex)[:300]}
         if "expert_gemm" in line["c4"]:
-            line["c4"]["expert_gemm"]["traffic"] = ncu_traffic(a.gamma, "r03_ncu_c4_moe.json")
+            line["c4"]["expert_gemm"]["traffic"] = ncu_traffic(a.gamma, "r04_ncu_c4_moe.json")
     if not a.no_offload_section and world == 1:
         try:
             line["offload_c3"] = offload_section(a, local, a.offload_batch, a.offload_steps, 1, gammas=(2, 4, 8))
