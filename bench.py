@@ -18,8 +18,9 @@ the global batch's tokens / that time.  --replicas: independent replicas instead
 /root/reference) on the host cores.
 
 The default C2 run adds sections to the same JSON line: the batch sweep 1-32 (the metric is quoted over
-batch 1-64), the on-demand comparator, gamma=8, gate_skew=2.0 and C4, the C3 offloaded store (with the
-on-demand, overlap and caching comparators) and the CPU reference.
+batch 1-64), the on-demand comparator, gamma=8, C1 (configs[0]: reference CPU path vs the engine on the
+reference's own weights), gate_skew=2.0, C4, C2 with real attention, the C3 offloaded store (with the
+on-demand, overlap and caching comparators), the SSD tier and the CPU reference.
 """
 from __future__ import annotations
 
@@ -203,6 +204,48 @@ def cpu_reference(shape: str, expert: str, gamma: int, n_draft: int, threads: in
             "tau": tau_used, "tau_slice": tau_slice, "forward_s_slice": t1, "forward_s_full_extrapolated": t1 * scale,
             "ondemand_value": threads / fwd_s_full,
             "step_values": [threads * tau_used / ((2 * gamma + 1) * t * scale) for t in samples]}
+
+
+def section_c1(gamma: int = 4, n_draft: int = 4, new_tokens: int = 32) -> dict:
+    """BASELINE configs[0] side by side (SURVEY 8(d) 'C1 in full'): the tiny synthetic MoE with the
+    reference's own build_model weights, B=1, greedy, run end to end by the reference's CPU path
+    (oracle/_ref, one thread as written) and by the B200 engine (fp32 parity engine on the same weights --
+    its token stream must equal the reference's -- and the bf16 tcgen05 engine)."""
+    from oracle.oracle import LIBS, ModelSpec as OSpec, Oracle, RunCfg as ORun
+    from paper_2604_10152_b200.engine import BF16, F32, Engine, ModelSpec, RunCfg
+    from paper_2604_10152_b200.prompts import make_prompts
+    spec = dict(SHAPES["c1"], seed=0)
+    prompts = make_prompts(0, 1, 8, spec["vocab"])
+    cfg = dict(gamma=gamma, n_draft=n_draft, max_new_tokens=new_tokens, run_seed=0)
+    kind = "ref" if os.path.exists(LIBS["ref"]) else "port"
+    om = Oracle(kind).build(OSpec(**spec))
+    out = {"workload": f"C1 tiny synthetic MoE (L4 E8 K2 d512 f1024 V1024), reference build_model weights, B=1, "
+                       f"gamma={gamma}, N={n_draft}, {new_tokens} new tokens, greedy", "reference_kind": kind}
+    t0 = time.perf_counter()
+    rs = om.run_specmoe(ORun(**cfg), prompts)
+    ref_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ro = om.run_ondemand(ORun(**cfg), prompts)
+    ref_od_s = time.perf_counter() - t0
+    out["reference_cpu"] = {"spec_tokens_per_s": rs.metrics["tokens_total"] / ref_s,
+                            "ondemand_tokens_per_s": ro.metrics["tokens_total"] / ref_od_s,
+                            "tau": rs.metrics["tau_mean"], "cores": 1}
+    for name, wt in (("b200_fp32_parity", F32), ("b200_bf16_tcgen05", BF16)):
+        e = Engine(ModelSpec(**spec), weight_type=wt, max_batch=1, max_gamma=gamma).init_exact()
+        e.run_specmoe(RunCfg(**cfg), prompts)  # warm-up
+        t0 = time.perf_counter()
+        r = e.run_specmoe(RunCfg(**cfg), prompts)
+        wall = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        od = e.run_ondemand(RunCfg(**cfg), prompts)
+        od_wall = time.perf_counter() - t0
+        out[name] = {"spec_tokens_per_s": r.metrics["tokens_total"] / wall,
+                     "ondemand_tokens_per_s": od.metrics["tokens_total"] / od_wall,
+                     "tau": r.metrics["tau_mean"], "tokens_equal_reference": r.tokens == rs.tokens,
+                     "lossless": r.tokens == od.tokens,
+                     "speedup_vs_reference_spec": (r.metrics["tokens_total"] / wall) / (rs.metrics["tokens_total"] / ref_s)}
+        e.close()
+    return out
 
 
 # ---------------------------------------------------------------- the B200 arm
@@ -684,7 +727,8 @@ def run_b200(a) -> None:
     if default_sections:
         for key, fn in (("batch_sweep", lambda: section_sweep(eng, stream, a, spec, pk)),
                         ("ondemand_c2", lambda: section_ondemand(eng, a, spec, a.batch)),
-                        ("gamma8_c2", lambda: section_gamma(eng, stream, a, spec, pk, 8, a.batch))):
+                        ("gamma8_c2", lambda: section_gamma(eng, stream, a, spec, pk, 8, a.batch)),
+                        ("c1", lambda: section_c1())):
             try:
                 line[key] = fn()
             except Exception as ex:  # reported, never fatal
