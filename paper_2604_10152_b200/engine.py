@@ -222,20 +222,43 @@ class RunResult:
     metrics: dict = field(default_factory=dict)
 
 
+def _view(ptr, n, shape=None):
+    """numpy view of n elements behind a ctypes pointer (empty for n == 0 / NULL)."""
+    if n <= 0 or not ptr:
+        return np.zeros(0 if shape is None else (0,) + tuple(shape[1:]), dtype=np.int64)
+    a = np.ctypeslib.as_array(ptr, shape=(n,))
+    return a if shape is None else a.reshape(shape)
+
+
 def _collect(rp) -> RunResult:
+    """Flatten the C result into Python values (whole arrays at a time: a B=64 run_specmoe of 128 tokens
+    carries ~30k ledger entries, whose per-element ctypes reads cost ~0.1 s)."""
     r = rp.contents
     try:
-        toks = [[r.tokens[b * r.max_new + i] for i in range(r.n_tokens[b])] for b in range(r.B)]
-        led = [(PHASES[r.ledger[i].phase], r.ledger[i].step, r.ledger[i].layer, r.ledger[i].expert, r.ledger[i].bytes)
-               for i in range(r.n_ledger)]
+        ntok = _view(r.n_tokens, r.B)
+        tok = _view(r.tokens, r.B * r.max_new, (r.B, r.max_new)) if r.B * r.max_new else None
+        toks = [tok[b, :ntok[b]].tolist() if tok is not None else [] for b in range(r.B)]
+        lv = _view(r.ledger, r.n_ledger)
+        if r.n_ledger:
+            led = list(zip([PHASES[x] for x in lv["phase"].tolist()], lv["step"].tolist(), lv["layer"].tolist(),
+                           lv["expert"].tolist(), lv["bytes"].tolist()))
+        else:
+            led = []
         g = r.gamma
-        outc = [(r.outcomes[i].seq, r.outcomes[i].phase, r.outcomes[i].accepted, r.outcomes[i].correction,
-                 r.outcomes[i].tokens_generated, tuple(r.outcome_drafts[i * g + j] for j in range(g)))
-                for i in range(r.n_outcomes)]
+        ov = _view(r.outcomes, r.n_outcomes)
+        if r.n_outcomes:
+            dr = _view(r.outcome_drafts, r.n_outcomes * g, (r.n_outcomes, g)).tolist() if g else [[]] * r.n_outcomes
+            outc = list(zip(ov["seq"].tolist(), ov["phase"].tolist(), ov["accepted"].tolist(), ov["correction"].tolist(),
+                            ov["tokens_generated"].tolist(), [tuple(x) for x in dr]))
+        else:
+            outc = []
         K = r.top_k
-        tr = [(r.trace[i * (3 + K)], r.trace[i * (3 + K) + 1], r.trace[i * (3 + K) + 2],
-               tuple(r.trace[i * (3 + K) + 3 + k] for k in range(K))) for i in range(r.n_trace)]
-        hot = np.array([r.hotness[i] for i in range(r.moe_layers * r.experts)], dtype=np.uint64)
+        if r.n_trace:
+            tv = _view(r.trace, r.n_trace * (3 + K), (r.n_trace, 3 + K)).tolist()
+            tr = [(x[0], x[1], x[2], tuple(x[3:])) for x in tv]
+        else:
+            tr = []
+        hot = np.array(_view(r.hotness, r.moe_layers * r.experts), dtype=np.uint64)
         met = {k: getattr(r, k) for k in ("tau_mean", "tokens_total", "phases", "speculation_s", "verification_s",
                                           "modeled_seconds", "tokens_per_sec", "bytes_spec", "bytes_verify",
                                           "bytes_baseline", "bytes_total", "setup_bytes", "warmup_bytes",
