@@ -267,14 +267,7 @@ Engine::Engine(const smoe_engine_config& c) {
     SMOE_CUDA(cudaMemset(sched, 0, 8 * sizeof(int)));
     moe_done = dalloc<int>(128);
     SMOE_CUDA(cudaMemset(moe_done, 0, 128 * sizeof(int)));
-    gate_ctr = dalloc<unsigned>(1);
-    SMOE_CUDA(cudaMemset(gate_ctr, 0, sizeof(unsigned)));
-    comb_ctr = dalloc<unsigned>(1);
-    SMOE_CUDA(cudaMemset(comb_ctr, 0, sizeof(unsigned)));
     if (const char* v = getenv("SMOE_FUSED_MOE")) fuse_moe = atoi(v) != 0;
-    if (const char* v = getenv("SMOE_L2_PREFETCH")) l2_prefetch = atoi(v) != 0;
-    if (const char* v = getenv("SMOE_GATE_FLAG")) gate_flag = atoi(v) != 0;
-    if (const char* v = getenv("SMOE_COMBINE_FLAG")) combine_flag = atoi(v) != 0;
 
     h_small_n = (size_t)Tmax * 8 + (size_t)M * E * (E + 2) + 4096;
     SMOE_CUDA(cudaMallocHost(&h_small, h_small_n * sizeof(int)));
@@ -302,7 +295,7 @@ Engine::~Engine() {
     fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos); fr(rope);
     fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
-    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(gate_ctr); fr(comb_ctr); fr(scratch64); fr(pass_ctr);
+    fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
     fr(stage_up); fr(stage_down);
@@ -764,11 +757,6 @@ void Engine::gemm(const void* W, long long slot_stride, const TcOperand& amap, l
         if (splits > 1 && epi != kEpiStoreF32) throw Error(kInvariant, "split-K needs the f32 store epilogue");
         TcGemmArgs a{amap, a_rows_per_slot, bmap, Nout, Kd, gcnt, gslot, G, seg, single_rows, single_slot, rows_bound,
                      Y, ldy, epi, splits, split_stride, sched + 4 * (gemm_launches++ & 1)};
-        if (gemm_dep) {
-            a.dep_ctr = gemm_dep;
-            a.dep_target = comb_epoch;
-            gemm_dep = nullptr;
-        }
         launch_gemm_tc(a, stream);
     } else {
         if (splits != 1) throw Error(kInvariant, "the CUDA-core GEMM has no split-K");
@@ -803,22 +791,6 @@ void Engine::expert_ffn(int T, const int* cnt, const int* slots, const char* cls
                   moe_done + 64 * slot};
     TcGemmArgs dn{op_down, d, op_h, d, f, cnt, slots, E, T, 0, 0, T, ybuf, d, kEpiStoreF32, s_down, yd_stride,
                   sched + 4 * slot, moe_done + 64 * slot};
-    if (l2_next && l2_prefetch) {
-        up.l2_next = l2_next;
-        up.l2_next_bytes = l2_next_bytes;
-    }
-    static const bool mix_early = [] {  // opt-in: measured neutral (C2 50.6 ms/step either way)
-        const char* v = getenv("SMOE_MIX_EARLY");
-        return v && v[0] == '1';
-    }();
-    if (l2_next && mix_early) {  // next layer's Mix (QKV) weights, during this layer's gate
-        up.l2_early = l2_next;
-        up.l2_early_bytes = l2_next_bytes;
-    }
-    if (moe_dep) {
-        up.dep_ctr = moe_dep;
-        up.dep_target = gate_epoch;
-    }
     up.pred_groups = pred_groups;
     up.n_pred = n_pred;
     if (peer_y) {
@@ -883,27 +855,13 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
                        draft_sorted + (size_t)mo * E, rank + (size_t)mo * E * std::max(1, cur_n_draft), cur_n_draft,
                        use_aff, mo, 0, row_plen, flags};
             const bool fetch = offload && !restricted;
-            // hand-off gate -> MoE launch by a block counter (no store fetch or profiling event between)
-            const bool flag = gate_flag && !fetch && !profiling && use_tc && fuse_moe && E <= 64;
-            if (flag) {
-                g.done_ctr = gate_ctr;
-                gate_epoch += (unsigned)T;
-            }
             {
                 ProfScope ps(*this, "gate");
                 launch_gate(g, stream);  // x += a; rms; gate, top-K, remap; dispatch rows into xperm
             }
-            moe_dep = flag ? gate_ctr : nullptr;
             if (fetch) store_fetch_layer(mo, cnt);  // expert store: migrate this layer's missing experts
             // weight slots: the store's table for this layer's fetch, else the resident slot map (draft
             // passes touch only pinned draft experts)
-            if (attn()) {  // the next layer's QKV weights
-                l2_next = l + 1 < L ? static_cast<const char*>(wqkv) + (size_t)(l + 1) * QKVD * d * ws : nullptr;
-                l2_next_bytes = (long long)QKVD * d * (long long)ws;
-            } else {
-                l2_next = l + 1 < L ? static_cast<const char*>(mix) + (size_t)(l + 1) * d * d * ws : nullptr;
-                l2_next_bytes = (long long)d * d * (long long)ws;
-            }
             static const bool pf_pred = [] {
                 const char* v = getenv("SMOE_PF_PRED");
                 return !(v && v[0] == '0');
@@ -915,17 +873,11 @@ void Engine::pass(int T, const int* rseq, const int* rextra, int extra_uniform, 
             expert_ffn(T, cnt, fetch ? group_slot : slot_of + (size_t)mo * E, "expert_gemm");
             pred_groups = nullptr;
             n_pred = 0;
-            l2_next = nullptr;
-            moe_dep = nullptr;
             if (fetch) store_finish_layer(mo);
             {
                 // K9 combine + residual + the next layer's (or the head's) rms
                 ProfScope ps(*this, "combine");
-                const bool cflag = combine_flag && !profiling && use_tc;
-                if (cflag) comb_epoch += (unsigned)T * (unsigned)combine_blocks_per_row(d);
-                launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream,
-                                   cflag ? comb_ctr : nullptr);
-                gemm_dep = cflag ? comb_ctr : nullptr;  // the next Mix (or head) launch
+                launch_combine_rms(x, ybuf, s_down, yd_stride, pos, wgt, T, K, d, 0, xa, wt, stream);
             }
         } else {
             launch_resid_rms(x, pmix, s_mix, pm_stride, T, d, xa, wt, stream);

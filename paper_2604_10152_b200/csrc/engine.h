@@ -51,16 +51,6 @@ struct TcGemmArgs {
     int* done = nullptr;      // device [64] zeroed per-group completion counters (fused launches)
     void* const* peer_y = nullptr;  // EP fused return (see tc::Phase): device table of the ranks' return buffers
     int peer_eo = 0, peer_me = 0;
-    // bytes to prefetch into L2 once the launch runs out of units (its tail): the next layer's Mix weights
-    const void* l2_next = nullptr;
-    long long l2_next_bytes = 0;
-    // grouped launches: bytes prefetched into L2 by the CTAs while they wait for the dependency (HBM idle)
-    const void* l2_early = nullptr;
-    long long l2_early_bytes = 0;
-    // grouped launches: wait for *dep_ctr to reach dep_target (the gate blocks' completion count)
-    // instead of the previous grid's completion (nullptr: griddepcontrol.wait)
-    const unsigned* dep_ctr = nullptr;
-    unsigned dep_target = 0;
     // grouped launches of draft passes: the groups expected to have rows (device, ascending), whose first
     // weight boxes are prefetched into L2 before the dependency wait
     const int* pred_groups = nullptr;
@@ -235,7 +225,6 @@ public:
     void* xperm = nullptr;  // [E*Tmax][d] expert segments of T rows (gate dispatch)
     void* hbuf = nullptr;   // [E*Tmax][f]
     float* ybuf = nullptr;  // [s_down][E*Tmax][d] split-K partials of the down projection
-    const void* l2_next = nullptr;  // next layer's Mix weights, prefetched into L2 in the MoE launch's tail
     const int* pred_groups = nullptr;  // draft passes: this layer's draft experts (fused MoE launch prefetch)
     int n_pred = 0;
     float* pmix = nullptr;  // [s_mix][Tmax][d] split-K partials of the mix GEMM
@@ -265,17 +254,6 @@ public:
     int* sched = nullptr;        // tcgen05 GEMM dynamic tile scheduler counters [2 slots][4]
     int* moe_done = nullptr;     // fused expert GEMM per-group completion counters [2 slots][64]
     int fuse_moe = 1;            // one launch per MoE layer for up+down (env SMOE_FUSED_MOE=0: two)
-    int l2_prefetch = 0;         // MoE launch tail prefetches the next Mix weights into L2 (env SMOE_L2_PREFETCH=1; measured
-                                 // slower once the fused MoE stream reached 0.95: it delays the MoE tail more than it saves)
-    int gate_flag = 0;           // MoE launch waits on the gate blocks' counter, not the gate grid (env SMOE_GATE_FLAG)
-    unsigned* gate_ctr = nullptr;  // device: gate blocks finished (monotonic)
-    unsigned gate_epoch = 0;       // host: gate blocks launched so far
-    const unsigned* moe_dep = nullptr;  // the next fused MoE launch's hand-off counter (gate_flag)
-    int combine_flag = 0;        // the next Mix/head launch waits on the combine blocks' counter (env SMOE_COMBINE_FLAG)
-    unsigned* comb_ctr = nullptr;  // device: combine blocks finished (monotonic)
-    unsigned comb_epoch = 0;
-    const unsigned* gemm_dep = nullptr;  // hand-off counter of the next gemm() launch
-    int* pass_ctr = nullptr;     // pass kernel dependency counters (self-resetting)
     unsigned gemm_launches = 0;
     double* scratch64 = nullptr;  // staging for exact uploads / affinity partials
     size_t scratch64_n = 0;
@@ -330,7 +308,6 @@ public:
     TcOperand op_wqkv{}, op_wo{}, op_ao{};
     std::vector<std::vector<int>> kv_pages;  // host: pages of each sequence
     std::vector<int> kv_free, h_seq_len;
-    long long l2_next_bytes = 0;
     bool attn() const { return Hq > 0; }
     void kv_fit(int b);     // pages for positions [0, h_seq_len[b] + Gmax] (and the table row uploaded)
     void kv_advance(const std::vector<int>& seqs, const std::vector<int>& takes);

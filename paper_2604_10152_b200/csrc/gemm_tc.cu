@@ -75,13 +75,8 @@ struct TcParams {
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
     int pair_ok;           // grouped launches: phases (bit 0 up, bit 1 down) that may use pair units
     int pair_big;          // grouped launches: pair units also for groups of 129..256 tokens (both TMEM buffers)
-    int pair_min_units;    // grouped launches: the first phase pairs only if that leaves >= this many units
     int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
-    int* sched;            // [3]: next-unit counter, finished-CTA counter, L2 prefetch chunk counter (self-resetting)
-    const uint8_t* pf;     // prefetched into L2 by the producers that run out of units (the launch's tail)
-    long long pf_bytes;
-    const unsigned* dep_ctr;  // wait for *dep_ctr >= dep_target instead of the previous grid's completion
-    unsigned dep_target;
+    int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
     int tr;                // trace slot (SMOE_TC_TRACE builds)
     // draft passes: the groups the launch will most likely have (the layer's draft experts, ascending);
@@ -89,8 +84,6 @@ struct TcParams {
     const int* pred;
     int n_pred, pf_kb;
     int w_evict_first;         // weight boxes loaded with an L2 evict_first policy
-    const uint8_t* pf_early;   // prefetched into L2 before the dependency wait (the next layer's Mix weights)
-    long long pf_early_bytes;
 };
 
 #ifdef SMOE_TC_TRACE
@@ -117,7 +110,6 @@ __device__ __forceinline__ long long gtimer() {
 // TMA issue count per weight byte halves, which is what bounded the stream: isolated up projection
 // 0.865 -> 0.97 of the HBM copy peak, down 0.80 -> 0.99 (tools/gemm_bench.py, T <= 32).  Needs groups of
 // <= 128 tokens (2 accumulators x 2 buffers x 128 TMEM columns).
-constexpr long long kPfChunk = 256 * 1024;
 __device__ __forceinline__ int row_tiles(const Phase& P, int pair) { return pair ? (P.m_tiles + 1) / 2 : P.m_tiles; }
 
 // Grouped launches enumerate their units over a compacted list of work items = the (group, token tile)
@@ -157,9 +149,6 @@ __device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Pl
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) {
         int pair = p.pair_ok && (mx <= BN_MAX / 2 || p.pair_big) ? p.pair_ok : 0;
-        // few groups (a draft pass: N experts): paired first-phase units may not cover the SMs, and every
-        // such unit is on the first -> second phase critical path; unpaired units halve it
-        if ((pair & 1) && n * row_tiles(p.ph[0], 1) * p.ph[0].splits < p.pair_min_units) pair &= ~1;
         const int stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
         plan->n_items = n;
         plan->pair = pair;
@@ -250,25 +239,8 @@ __device__ __forceinline__ bool next_unit(const TcParams& p, const int16_t* item
     return true;
 }
 
-// The dependency wait of a launch: the previous grid's completion (PDL), or, when the launch carries a
-// hand-off counter, that counter reaching its target (the gate / combine blocks count themselves after
-// their stores), which a resident CTA sees ~2 us before the grid-completion signal.
-__device__ __forceinline__ void dep_wait(const TcParams& p) {
-    if (!p.dep_ctr) {
-        pdl_wait();
-        return;
-    }
-    const long long t0 = clock64();
-    while ((int)((unsigned)ld_relaxed(reinterpret_cast<const int*>(p.dep_ctr)) - p.dep_target) < 0) {
-        __nanosleep(64);
-        if (clock64() - t0 > 4000000000ll) {
-            printf("smoe dep_wait timeout: block %d\n", (int)blockIdx.x);
-            __trap();
-        }
-    }
-    fence_acquire();
-    proxy_fence_async();  // the producer kernel's generic stores before this launch's TMA reads
-}
+// The dependency wait of a launch: the previous grid's completion and memory flush (PDL).
+__device__ __forceinline__ void dep_wait(const TcParams&) { pdl_wait(); }
 
 // Draft passes: while the CTAs wait for the gate (HBM is idle then), prefetch into L2 the first weight
 // boxes of the first wave of units as they will be enumerated if every predicted group has rows (the
@@ -370,14 +342,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // grouped launches: the unit geometry (rows per expert) is written by the gate kernel that
         // immediately precedes this one, so it may only be read after the dependency wait
         if (p.pred && threadIdx.x == 0) prefetch_predicted(p, mapA0, mapA1);
-        if (p.pf_early && threadIdx.x == 32) {  // this CTA's slice of the next launch's weights, while HBM idles
-            const long long per = ((p.pf_early_bytes + gridDim.x - 1) / gridDim.x + 255) & ~255ll;
-            for (long long off = (long long)blockIdx.x * per, end = min(p.pf_early_bytes, off + per); off < end;
-                 off += kPfChunk) {
-                const uint32_t n = (uint32_t)min((long long)kPfChunk, end - off);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_early + off), "r"(n) : "memory");
-            }
-        }
         dep_wait(p);
         if (warp == 0) build_plan(p, s_items, plan);
         __syncthreads();
@@ -424,19 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(&ring_full[r]);
             }
             __syncwarp();
-            if (u >= total_units) {
-                // out of units: the launch's tail has begun and HBM has spare bandwidth; pull the next
-                // launch's weights (the next layer's Mix, 32 MB at C2) into L2 in 256 KB chunks
-                if (lane == 0)
-                    for (;;) {
-                        const long long off = (long long)atomicAdd(&p.sched[2], 1) * kPfChunk;
-                        if (off >= p.pf_bytes) break;
-                        const uint32_t n = (uint32_t)min((long long)kPfChunk, p.pf_bytes - off);
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf + off), "r"(n) : "memory");
-                    }
-                __syncwarp();
-                break;
-            }
+            if (u >= total_units) break;  // out of units
             // lane 0's decode, broadcast (the other lanes' w is unset)
             const int phase = __shfl_sync(0xffffffffu, w.phase, 0), wp = __shfl_sync(0xffffffffu, w.pair, 0);
             const int kb0 = __shfl_sync(0xffffffffu, w.kb0, 0), kb1 = __shfl_sync(0xffffffffu, w.kb1, 0);
@@ -652,7 +604,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         if (atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1) {
             p.sched[0] = 0;
-            p.sched[2] = 0;
             if (p.nphase > 1)
                 for (int g = 0; g < p.G; ++g) p.done[g] = 0;
             p.sched[1] = 0;
@@ -804,12 +755,7 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
         const char* v = getenv("SMOE_TC_PAIR_BIG");
         return v ? atoi(v) : 1;
     }();
-    static const int pair_min_env = [] {  // 0: always pair (measured: unpaired units are slower even when
-        const char* v = getenv("SMOE_TC_PAIR_MIN");  // the paired ones leave SMs idle, C4 draft 0.44 -> 0.40)
-        return v ? atoi(v) : 0;
-    }();
     p.pair_big = pair_big_env;
-    p.pair_min_units = pair_min_env;
     // single-group launches pair only when that does not load the busiest SM with more weight bytes
     // (the C2 Mix launch at T=64 would run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us; the head
     // at T=64, 250 units = 2 waves of 1 MB, becomes 1 wave of 2 MB paired units)
@@ -825,17 +771,12 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.stages = std::max(2, std::min(kMaxStages, p.stage_space / stage_bytes));
     p.sched = a.sched;
     p.done = a.done;
-    p.pf = static_cast<const uint8_t*>(a.l2_next);
-    p.pf_bytes = a.l2_next ? a.l2_next_bytes : 0;
-    p.dep_ctr = a.dep_ctr;
-    p.dep_target = a.dep_target;
     static const int wef_env = [] {
         const char* v = getenv("SMOE_W_EVICT_FIRST");
         return v ? atoi(v) : 1;
     }();
     p.w_evict_first = a.group_cnt && wef_env;  // expert weights: streamed once per pass
-    p.pf_early = static_cast<const uint8_t*>(a.l2_early);
-    p.pf_early_bytes = a.l2_early ? a.l2_early_bytes : 0;
+
     static const int pf_kb_env = [] {
         const char* v = getenv("SMOE_PF_KB");
         return v ? atoi(v) : 8;

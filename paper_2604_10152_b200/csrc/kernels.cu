@@ -415,11 +415,6 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
         store_row4<OT>(base, row * d, xf4, d4, 1.0f);
     }
     if (a.peer_x) __threadfence_system();
-    if (a.done_ctr) {  // hand-off to the MoE launch: every thread's stores, then one count per row
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(a.done_ctr, 1u);
-    }
     RK_END(1);
 }
 
@@ -427,7 +422,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
 template <typename OT>
 __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
                               const int* __restrict__ pos, const float* __restrict__ wgt, int K, int d, int dense,
-                              void* __restrict__ xa, unsigned* done_ctr) {
+                              void* __restrict__ xa) {
     RK_IN();
     pdl_wait();
     pdl_trigger();
@@ -469,11 +464,6 @@ __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, con
 #pragma unroll 1
     for (int j = 0; j < rc.nv; ++j)
         for (int i = rc.vt(j); i < d4; i += rc.VB) store4_op<OT>(xa, base + 4ll * i, row4[i], inv);
-    if (done_ctr) {  // hand-off to the next GEMM launch: every thread's stores, then one count per block
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(done_ctr, 1u);
-    }
     RK_END(2);
 }
 
@@ -704,19 +694,17 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
     else launch_kc(k_gate<__nv_bfloat16>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
 }
 
-int combine_blocks_per_row(int d) { return row_shape(row_threads(d)).C; }
 
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
-                        int K, int d, int dense, void* xa, WType op, cudaStream_t s, unsigned* done_ctr) {
+                        int K, int d, int dense, void* xa, WType op, cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
     const RowShape rs = row_shape(row_threads(d));
     if (op == kF32)
-        launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa,
-                  done_ctr);
+        launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa);
     else
         launch_kc(k_combine_rms<__nv_bfloat16>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense,
-                  xa, done_ctr);
+                  xa);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s) {

@@ -64,7 +64,6 @@ struct GateArgs {
     void* const* peer_x = nullptr;
     int ep_eo = 0, ep_me = 0;
     int stage_gw = 0;  // set by launch_gate: gate weights staged into shared memory before the dependency wait
-    unsigned* done_ctr = nullptr;  // incremented once per row after its dispatch stores (MoE launch hand-off)
 };
 void launch_gate(const GateArgs& a, cudaStream_t s);
 
@@ -72,10 +71,8 @@ void launch_gate(const GateArgs& a, cudaStream_t s);
 // K9 (model.cpp:248-257) + the next rms: y_k = sum_s P[s][pos[t,k]] (split-K partials, s in order;
 // pos == nullptr: row t*K+k),
 // x[t] += sum_k wgt[t,k] * y_k (k in order; dense: x[t] += y), then xa[t] = rms(x[t]).
-// blocks per row of the combine launch (its hand-off counter counts blocks)
-int combine_blocks_per_row(int d);
 void launch_combine_rms(float* x, const float* P, int S, long long pstride, const int* pos, const float* wgt, int T,
-                        int K, int d, int dense, void* xa, WType op, cudaStream_t s, unsigned* done_ctr = nullptr);
+                        int K, int d, int dense, void* xa, WType op, cudaStream_t s);
 
 // K10 (model.cpp:172-176): per-row argmax, first max wins; non-finite -> flag.
 void launch_argmax(const float* logits, int T, int V, int* out, int* flags, cudaStream_t s);
