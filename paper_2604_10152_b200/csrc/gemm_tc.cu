@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kb0 = __shfl_sync(0xffffffffu, w.kb0, 0), kb1 = __shfl_sync(0xffffffffu, w.kb1, 0);
             const int n0 = __shfl_sync(0xffffffffu, w.n0, 0), g = __shfl_sync(0xffffffffu, w.g, 0);
             const int nval = __shfl_sync(0xffffffffu, w.n_valid, 0);
-            const int arow = __shfl_sync(0xffffffffu, (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0), 0);
+            const int arow = __shfl_sync(
+                0xffffffffu, lane == 0 ? (int)((long long)w.slot * p.ph[w.phase].a_rows_per_slot + w.m0) : 0, 0);
             const int wtiled = p.ph[phase].tiled;
             const int tc1 = arow & 255, tc2 = (arow >> 8) * p.ph[phase].num_kb;  // tiled-layout box coordinates
             const CUtensorMap* mA = phase ? &mapA1.m[wp] : &mapA0.m[wp];
