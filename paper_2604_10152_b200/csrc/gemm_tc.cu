@@ -74,7 +74,6 @@ struct TcParams {
     int stages, b_region;  // host layout (single-group launches): stage count, token bytes per stage
     int stage_space;       // shared bytes available to the stage ring (run-time layout of grouped launches)
     int pair_ok;           // grouped launches: phases (bit 0 up, bit 1 down) that may use pair units
-    int pair_big;          // grouped launches: pair units also for groups of 129..256 tokens (both TMEM buffers)
     int pair_single;       // single-group launch in pair units (host-decided: rows <= 128)
     int* sched;            // [2]: next-unit counter, finished-CTA counter (self-resetting)
     int* done;             // [kMaxGroups]: finished phase-0 units per group (two-phase; self-resetting)
@@ -148,7 +147,7 @@ __device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Pl
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) {
-        int pair = p.pair_ok && (mx <= BN_MAX / 2 || p.pair_big) ? p.pair_ok : 0;
+        const int pair = p.pair_ok && mx <= BN_MAX / 2 ? p.pair_ok : 0;
         const int stage_bytes = (pair ? 2 : 1) * kABytes + tok_box_bytes(tok_box_index(mx));
         plan->n_items = n;
         plan->pair = pair;
@@ -202,7 +201,6 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, const int16_t* it
     w.n_valid = min(BN_MAX, r1 - w.n0);
     w.m0 = mt * (pair ? 2 * BM : BM);
     w.pair = pair;
-    w.big = pair && w.n_valid > BN_MAX / 2;
     w.ks = ks;
     w.kb0 = ks * P.kb_per_split;
     w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
@@ -466,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // loop -- this thread's per-stage latency (full barrier -> stage released) is on the stream's
         // critical path.
         // TMEM = two 256-column accumulator buffers used alternately (epilogue of one unit overlaps the
-        // MMAs of the next); a big pair unit (two tiles x up to 256 tokens) takes both
+        // MMAs of the next)
         // (bit a of `par`: phase parity of buffer a)
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
         const int stg = __shfl_sync(0xffffffffu, stages, 0);
@@ -478,14 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         Unit w;
         while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, true, w, pair)) {
             const int kb0 = __shfl_sync(0xffffffffu, w.kb0, 0), kb1 = __shfl_sync(0xffffffffu, w.kb1, 0);
-            const int wpair = __shfl_sync(0xffffffffu, w.pair, 0), big = __shfl_sync(0xffffffffu, w.big, 0);
+            const int wpair = __shfl_sync(0xffffffffu, w.pair, 0);
             const int nval = __shfl_sync(0xffffffffu, w.n_valid, 0);
-            const int acc = big ? 0 : nb;
+            const int acc = nb;
             mbar_wait(&acc_empty[acc], ((par >> acc) & 1) ^ 1);
-            if (big) mbar_wait(&acc_empty[1], ((par >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tm + (uint32_t)(acc * BN_MAX);
-            const uint32_t d_tile1 = d_tmem + (uint32_t)(big ? BN_MAX : BM);  // pair units' second tile
+            const uint32_t d_tile1 = d_tmem + (uint32_t)BM;  // pair units' second tile
             const uint32_t idesc = idesc_bf16(BM, (nval + 15) & ~15);
             for (int kb = kb0; kb < kb1; ++kb) {
                 const int s = ms;
@@ -511,17 +508,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
             }
-            if (elect_one()) {
-                mma_commit(&acc_full[acc]);
-                if (big) mma_commit(&acc_full[1]);
-            }
+            if (elect_one()) mma_commit(&acc_full[acc]);
             __syncwarp();
-            if (big) {
-                par ^= 3u;
-            } else {
-                par ^= 1u << acc;
-                nb ^= 1;
-            }
+            par ^= 1u << acc;
+            nb ^= 1;
             TR(if (lane == 0) g_tr_unit[trs][w.id % kTrUnits].mma_done = gtimer();)
         }
     } else {  // -------------------------- epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
@@ -531,16 +521,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t par = 0;
         Unit w;
         while (next_unit(p, items, n_items, ring_full, ring_empty, ring, cons, true, w, pair)) {
-            const int acc = w.big ? 0 : nb;  // the MMA issuer's buffer sequence
+            const int acc = nb;  // the MMA issuer's buffer sequence
             mbar_wait(&acc_full[acc], (par >> acc) & 1);
-            if (w.big) mbar_wait(&acc_full[1], (par >> 1) & 1);
             tc_fence_after();
             TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_start = gtimer();)
             const Phase& P = p.ph[w.phase];
             for (int h = 0; h < (w.pair ? 2 : 1); ++h) {  // pair units: the two 128-row tiles in turn
                 const int row = w.m0 + h * BM + q * 32 + lane;  // weight row within the slot
                 const uint32_t taddr =
-                    tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * (w.big ? BN_MAX : BM));
+                    tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_MAX + h * BM);
 #ifndef SMOE_EPI32_MIN
 #define SMOE_EPI32_MIN 16
 #endif
@@ -584,16 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             }
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&acc_empty[acc]);
-                if (w.big) mbar_arrive(&acc_empty[1]);
-            }
-            if (w.big) {
-                par ^= 3u;
-            } else {
-                par ^= 1u << acc;
-                nb ^= 1;
-            }
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            par ^= 1u << acc;
+            nb ^= 1;
             TR(if (warp == 2 && lane == 0) g_tr_unit[trs][w.id % kTrUnits].epi_done = gtimer();)
         }
     }
@@ -752,11 +734,6 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     }();
     // grouped launches: bit 0 pairs the first phase, bit 1 the second (applied when the counts allow)
     p.pair_ok = a.group_cnt && pair_env ? (1 | (b && pair_down_env ? 2 : 0)) : 0;
-    static const int pair_big_env = [] {
-        const char* v = getenv("SMOE_TC_PAIR_BIG");
-        return v ? atoi(v) : 1;
-    }();
-    p.pair_big = pair_big_env;
     // single-group launches pair only when that does not load the busiest SM with more weight bytes
     // (the C2 Mix launch at T=64 would run 64 paired units on 64 of 148 SMs: 20.8 vs 18.0 us; the head
     // at T=64, 250 units = 2 waves of 1 MB, becomes 1 wave of 2 MB paired units)

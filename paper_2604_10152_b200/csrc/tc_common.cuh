@@ -247,7 +247,6 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 struct Unit {
     int phase, g, slot, n0, n_valid, m0, kb0, kb1, ks, id;
     int pair;  // two 128-row tiles (gemm_tc.cu pair units)
-    int big;   // pair unit of more than 128 tokens: its two accumulators take both TMEM buffers
 };
 
 // SwiGLU over a 32-column TMEM chunk (two x16 loads in flight).  Rows 2i / 2i+1 of the slot hold w1 / w3 of

@@ -20,7 +20,7 @@ SHAPES = {
     # E=64 at d=1024: 1024-thread gate tree (4-CTA clusters), gate weights too large to stage
     "e64_d1024": (ModelSpec(num_layers=3, experts=64, top_k=6, hidden=1024, ffn=512, vocab=512,
                             expert_kind=SWIGLU3, moe_mask=[0, 1, 1], gate_skew=0.5), 8),
-    # B=64 verify passes of 320 rows over 4 experts: groups of > 128 tokens (big pair units)
+    # B=64 verify passes of 320 rows over 4 experts: groups of > 128 tokens (unpaired launches)
     "e4_b64": (ModelSpec(num_layers=2, experts=4, top_k=2, hidden=1024, ffn=512, vocab=512,
                          expert_kind=SWIGLU3, gate_skew=1.0), 2, 64),
 }
