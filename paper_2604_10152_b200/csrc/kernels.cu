@@ -142,12 +142,21 @@ int row_rt(int vb) {
 struct RowShape {
     int C, RT;
 };
-RowShape row_shape(int vb) {
+RowShape row_shape(int vb, int T = 0) {
     static const bool cl = [] {
         const char* v = std::getenv("SMOE_ROW_CLUSTER");
         return v && v[0] == '1';
     }();
+    static const int wide = [] {  // SMOE_ROW_WIDE=0: off
+        const char* v = std::getenv("SMOE_ROW_WIDE");
+        return v ? std::atoi(v) : 1;
+    }();
     if (cl && vb > 256) return {vb / 256, 256};
+    // A VB-thread row block fills an SM's register file (1024 x 64), so a pass with T rows takes
+    // ceil(T / SMs) waves; with more rows than SMs (a verify pass: 320 at B=64) 256-thread blocks playing
+    // the same VB-thread tree put four rows on an SM and finish in one wave (the gate of a C2 verify pass:
+    // 26.7 -> 18.8 us, bit-identical)
+    if (wide && T > tc::sm_count() && vb > 256 && vb % 256 == 0 && row_rt(vb) == vb) return {1, 256};
     return {1, row_rt(vb)};
 }
 
@@ -676,11 +685,14 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
     }();
     // stage the gate weights (E x d f32) in shared memory when they fit beside one row (C2: 128 KB); a row
     // cluster with one virtual thread per real thread stages only each CTA's experts (C4: 128 KB of 512)
-    const RowShape rs0 = row_shape(gate_threads(a.d, a.E));
+    // (wide row blocks only with few experts: the GEMV's virtual warps per expert shrink to a quarter)
+    const RowShape rs0 = row_shape(gate_threads(a.d, a.E), a.E <= 16 ? a.T : 0);
     const int vb = gate_threads(a.d, a.E), nvw = vb >> 5;
     const bool per_cta = rs0.C > 1 && rs0.C * rs0.RT == vb && a.E % nvw == 0;
     const size_t gw_bytes = sizeof(float) * (size_t)(per_cta ? (rs0.RT >> 5) * (a.E / nvw) : a.E) * a.d;
-    a.stage_gw = stage_env && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0
+    // wide passes read the gate weights from L2 (a staged copy per block would hold one block per SM again)
+    const bool wide = rs0.C == 1 && rs0.RT < vb && a.T > tc::sm_count();
+    a.stage_gw = stage_env && !wide && gw_bytes <= 160 * 1024 && (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0
                      ? (per_cta ? 2 : 1) : 0;
     size_t smem = sizeof(float) * (a.d + 2 * a.E + 8 * 32 + 33) + (a.stage_gw ? gw_bytes : 0) +
                   (a.in_draft ? sizeof(int) * ((size_t)a.E * a.N + a.N) + a.E : 0);
@@ -689,7 +701,7 @@ void launch_gate(const GateArgs& a0, cudaStream_t s) {
         SMOE_CUDA(cudaFuncSetAttribute(k_gate<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         SMOE_CUDA(cudaFuncSetAttribute(k_gate<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     }
-    const RowShape rs = row_shape(gate_threads(a.d, a.E));  // a row per cluster, a (virtual) warp per expert
+    const RowShape rs = rs0;  // a row per cluster, a (virtual) warp per expert
     if (a.op == kF32) launch_kc(k_gate<float>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
     else launch_kc(k_gate<__nv_bfloat16>, a.T * rs.C, rs.RT, smem, s, rs.C, a);
 }
@@ -699,7 +711,7 @@ void launch_combine_rms(float* x, const float* P, int S, long long pstride, cons
                         int K, int d, int dense, void* xa, WType op, cudaStream_t s) {
     if (T <= 0) return;
     const size_t sm = sizeof(float) * d;
-    const RowShape rs = row_shape(row_threads(d));
+    const RowShape rs = row_shape(row_threads(d));  // (wide blocks measured no faster for the combine)
     if (op == kF32)
         launch_kc(k_combine_rms<float>, T * rs.C, rs.RT, sm, s, rs.C, x, P, S, pstride, pos, wgt, K, d, dense, xa);
     else
