@@ -347,6 +347,13 @@ public:
 
     // ---- counters (bench.py): kernel launches, algorithmic HBM bytes, control-path PCIe bytes
     uint64_t launches = 0, ctl_h2d = 0, ctl_d2h = 0;
+    // captured speculative phases (loop.cpp spec_step, SMOE_GRAPH=1): key (rows, gamma, affinity)
+    struct PhaseGraph {
+        cudaGraphExec_t exec;
+        uint64_t launches;
+        double dense_bytes;
+    };
+    std::map<uint64_t, PhaseGraph> phase_graphs;
     double alg_expert_bytes = 0, alg_dense_bytes = 0;
 
     // ---- store (offload)
