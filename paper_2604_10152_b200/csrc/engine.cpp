@@ -296,6 +296,7 @@ Engine::~Engine() {
     fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos); fr(rope);
     fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
+    if (up_arena) cudaFreeHost(up_arena);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
@@ -352,6 +353,22 @@ void Engine::check_flags() {
     }
 }
 
+void Engine::upload_async(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    const size_t need = (up_arena_off + bytes + 255) & ~size_t(255);
+    if (need > up_arena_n) {  // grow: drain the queued copies first (they read the old arena)
+        SMOE_CUDA(cudaStreamSynchronize(stream));
+        if (up_arena) SMOE_CUDA(cudaFreeHost(up_arena));
+        up_arena_n = std::max<size_t>(2 * need, 1 << 20);
+        SMOE_CUDA(cudaMallocHost(&up_arena, up_arena_n));
+        up_arena_off = 0;
+    }
+    char* slot = up_arena + up_arena_off;
+    std::memcpy(slot, src, bytes);
+    up_arena_off = (up_arena_off + bytes + 255) & ~size_t(255);
+    ctl_h2d += bytes;
+    SMOE_CUDA(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, stream));
+}
 void Engine::upload_ints(int* dst, const int* src, size_t n) {
     // synchronous-safe: stage through pinned memory then wait, so callers may reuse src at once
     if (n == 0) return;
@@ -662,7 +679,7 @@ void Engine::build_affinity_device() {
 // For each MoE layer and raw expert r: the draft members ordered by (affinity distance to r, index)
 // -- the order nearest_draft_expert (drafting.cpp:123-138) scans implicitly.  The device walks this
 // list and takes the first member not already chosen, so no float64 compare happens on the GPU.
-void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft) {
+void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft, bool async) {
     if ((int)sets.size() != M) throw Error(kInvariant, "forward: restricted set count != MoE layer count");
     // per-layer sizes may differ (RestrictedExperts allows it); rows are padded with -1 to the widest
     // Duplicates are kept: the reference's candidate lists are multisets (drafting.cpp:140-151 sizes
@@ -699,9 +716,15 @@ void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_dra
             std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * nmax);
         }
     }
-    h2d(in_draft, ind.data(), ind.size());
-    upload_ints(draft_sorted, sorted.data(), sorted.size());
-    upload_ints(rank, rk.data(), rk.size());
+    if (async) {
+        upload_async(in_draft, ind.data(), ind.size());
+        upload_async(draft_sorted, sorted.data(), sorted.size() * sizeof(int));
+        upload_async(rank, rk.data(), rk.size() * sizeof(int));
+    } else {
+        h2d(in_draft, ind.data(), ind.size());
+        upload_ints(draft_sorted, sorted.data(), sorted.size());
+        upload_ints(rank, rk.data(), rk.size());
+    }
     cur_n_draft = nmax;
 }
 

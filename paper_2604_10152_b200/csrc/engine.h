@@ -287,7 +287,14 @@ public:
     void build_affinity_device();
 
     // ---- draft tables
-    void set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft);  // sorted per layer
+    void set_draft_sets(const std::vector<std::vector<int>>& sets, int n_draft, bool async = false);  // sorted per layer
+    // Control uploads of a stepped speculative run without a host sync each: staged in a pinned arena and
+    // queued on the engine stream; the arena is recycled (upload_reset) once the phase's readback has
+    // synchronised the stream, so no queued copy can still be reading a reused region.
+    void upload_async(void* dst, const void* src, size_t bytes);
+    void upload_reset() { up_arena_off = 0; }
+    char* up_arena = nullptr;
+    size_t up_arena_n = 0, up_arena_off = 0;
     int cur_n_draft = 0;
     // ---- real GQA attention (attn.cu; attn_heads > 0)
     int Hq = 0, Hkv = 0, hd = 0, QD = 0, KD = 0, QKVD = 0, max_seq = 0, maxp = 0, s_qkv = 1;

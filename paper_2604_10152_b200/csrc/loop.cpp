@@ -346,7 +346,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
             if (!S.res->pinned(m * E + ex) || !S.res->resident(m * E + ex))
                 throw Error(kInvariant, "run_specmoe: draft expert not pinned on device");
     if (S.sets_dirty) {
-        e.set_draft_sets(S.sets, S.nd);
+        e.set_draft_sets(S.sets, S.nd, true);
         S.sets_dirty = false;
     }
     // rows: [0, na*(g+1)) verify (seq, i); [Tmax, Tmax+na) draft (seq)
@@ -358,11 +358,12 @@ int spec_step(Engine& e, int* accepted_tokens) {
             S.rows[(size_t)TV + s * (g + 1) + i] = i;
         }
     for (int s = 0; s < na; ++s) S.rows[(size_t)2 * TV + s] = act[s];
-    e.upload_ints(e.row_seq, S.rows.data(), TV);
-    e.upload_ints(e.row_extra, S.rows.data() + TV, TV);
+    // the phase's control uploads are queued without host syncs (engine.h upload_async)
+    e.upload_async(e.row_seq, S.rows.data(), sizeof(int) * TV);
+    e.upload_async(e.row_extra, S.rows.data() + TV, sizeof(int) * TV);
     int* drows = e.row_seq + e.Tmax;
-    e.upload_ints(drows, S.rows.data() + 2 * TV, na);
-    e.upload_ints(e.seqs, act.data(), na);
+    e.upload_async(drows, S.rows.data() + 2 * TV, sizeof(int) * na);
+    e.upload_async(e.seqs, act.data(), sizeof(int) * na);
 
     // (a) speculation: gamma restricted passes, drafts stay on device.  Sampling mode: the draft token
     // of step t, sequence s is drawn with the (t*na + s)-th uniform of the phase (speculate's loop order,
@@ -473,6 +474,7 @@ int spec_step(Engine& e, int* accepted_tokens) {
         NvtxRange nv("smoe device wait");
         e.sync();
     }
+    e.upload_reset();  // the stream is idle: every queued control upload has been read
     if (g_host_prof) hp3 = host_now();
     NvtxRange nv_book("smoe bookkeeping (reference order)");
     e.check_flags();
@@ -583,8 +585,8 @@ int spec_step(Engine& e, int* accepted_tokens) {
                 }
     }
     // rollback / advance of the device prefix state: only the taken tokens enter the running sums
-    e.upload_ints(e.commit_toks, ctoks.data(), ctoks.size());
-    e.upload_ints(e.commit_take, ctake.data(), na);
+    e.upload_async(e.commit_toks, ctoks.data(), sizeof(int) * ctoks.size());
+    e.upload_async(e.commit_take, ctake.data(), sizeof(int) * na);
     launch_commit(e.seq_sum, e.seq_len, e.emb64, e.seqs, e.commit_toks, e.stride, e.commit_take, na, e.d, e.stream,
                   e.last_tok);
     e.kv_advance(act, ctake);
