@@ -297,6 +297,7 @@ Engine::~Engine() {
     fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
     if (up_arena) cudaFreeHost(up_arena);
+    if (dn_arena) cudaFreeHost(dn_arena);
     fr(commit_take); fr(seqs); fr(flags); fr(sched); fr(moe_done); fr(scratch64);
     if (h_small) cudaFreeHost(h_small);
     if (h_store) cudaFreeHost(h_store);
@@ -368,6 +369,31 @@ void Engine::upload_async(void* dst, const void* src, size_t bytes) {
     up_arena_off = (up_arena_off + bytes + 255) & ~size_t(255);
     ctl_h2d += bytes;
     SMOE_CUDA(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, stream));
+}
+void Engine::download_async(void* host_dst, const void* dev_src, size_t row_bytes, size_t rows, size_t dev_pitch) {
+    const size_t bytes = row_bytes * rows;
+    if (!bytes) return;
+    const size_t need = (dn_arena_off + bytes + 255) & ~size_t(255);
+    if (need > dn_arena_n) {  // grow: complete the queued readbacks out of the old arena first
+        SMOE_CUDA(cudaStreamSynchronize(stream));
+        download_finish();
+        if (dn_arena) SMOE_CUDA(cudaFreeHost(dn_arena));
+        dn_arena_n = std::max<size_t>(2 * need, 1 << 20);
+        SMOE_CUDA(cudaMallocHost(&dn_arena, dn_arena_n));
+    }
+    char* slot = dn_arena + dn_arena_off;
+    if (rows == 1)
+        SMOE_CUDA(cudaMemcpyAsync(slot, dev_src, bytes, cudaMemcpyDeviceToHost, stream));
+    else
+        SMOE_CUDA(cudaMemcpy2DAsync(slot, row_bytes, dev_src, dev_pitch, row_bytes, rows, cudaMemcpyDeviceToHost,
+                                    stream));
+    dn_pending.push_back({host_dst, dn_arena_off, bytes});
+    dn_arena_off = (dn_arena_off + bytes + 255) & ~size_t(255);
+}
+void Engine::download_finish() {  // the stream must be synchronised
+    for (const auto& pd : dn_pending) std::memcpy(pd.dst, dn_arena + pd.off, pd.bytes);
+    dn_pending.clear();
+    dn_arena_off = 0;
 }
 void Engine::upload_ints(int* dst, const int* src, size_t n) {
     // synchronous-safe: stage through pinned memory then wait, so callers may reuse src at once

@@ -295,6 +295,19 @@ public:
     void upload_reset() { up_arena_off = 0; }
     char* up_arena = nullptr;
     size_t up_arena_n = 0, up_arena_off = 0;
+    // The phase's readbacks the same way: queued device -> pinned-arena copies (rows of `rows` x `row_bytes`
+    // at a device pitch), one stream sync, then download_finish() moves them into the host vectors
+    // (a device -> pageable copy blocks the host once per call).
+    void download_async(void* host_dst, const void* dev_src, size_t row_bytes, size_t rows = 1,
+                        size_t dev_pitch = 0);
+    void download_finish();
+    char* dn_arena = nullptr;
+    size_t dn_arena_n = 0, dn_arena_off = 0;
+    struct PendingDown {
+        void* dst;
+        size_t off, bytes;
+    };
+    std::vector<PendingDown> dn_pending;
     int cur_n_draft = 0;
     // ---- real GQA attention (attn.cu; attn_heads > 0)
     int Hq = 0, Hkv = 0, hd = 0, QD = 0, KD = 0, QKVD = 0, max_seq = 0, maxp = 0, s_qkv = 1;

@@ -462,18 +462,24 @@ int spec_step(Engine& e, int* accepted_tokens) {
         launch_accept(e.drafts, e.vam, e.seqs, na, g, e.stride, e.acc, e.corr, e.stream);
     }
     S.h_acc.resize(na); S.h_corr.resize(na); S.h_drafts.resize((size_t)e.Bmax * e.stride);
-    SMOE_CUDA(cudaMemcpyAsync(S.h_acc.data(), e.acc, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
-    SMOE_CUDA(cudaMemcpyAsync(S.h_corr.data(), e.corr, sizeof(int) * na, cudaMemcpyDeviceToHost, e.stream));
-    SMOE_CUDA(cudaMemcpyAsync(S.h_drafts.data(), e.drafts, sizeof(int) * e.Bmax * e.stride, cudaMemcpyDeviceToHost,
-                              e.stream));
-    read_log(e, e.raw_log, g, TV, S.vraw);
+    // the phase's readbacks through the pinned arena: queued, one sync, then copied out
+    e.download_async(S.h_acc.data(), e.acc, sizeof(int) * na);
+    e.download_async(S.h_corr.data(), e.corr, sizeof(int) * na);
+    e.download_async(S.h_drafts.data(), e.drafts, sizeof(int) * e.Bmax * e.stride);
+    auto read_log_async = [&](const int* log, int slot, int T, std::vector<int>& out) {
+        out.resize((size_t)e.M * T * e.K);
+        e.download_async(out.data(), log + (size_t)slot * e.M * e.Tmax * e.K, sizeof(int) * T * e.K, (size_t)e.M,
+                         sizeof(int) * e.Tmax * e.K);
+    };
+    read_log_async(e.raw_log, g, TV, S.vraw);
     std::vector<std::vector<int>> dfin(g);
-    for (int t = 0; t < g; ++t) read_log(e, e.fin_log, t, na, dfin[t]);
+    for (int t = 0; t < g; ++t) read_log_async(e.fin_log, t, na, dfin[t]);
     if (g_host_prof) hp2 = host_now();
     {
         NvtxRange nv("smoe device wait");
         e.sync();
     }
+    e.download_finish();
     e.upload_reset();  // the stream is idle: every queued control upload has been read
     if (g_host_prof) hp3 = host_now();
     NvtxRange nv_book("smoe bookkeeping (reference order)");
