@@ -287,6 +287,7 @@ Engine::~Engine() {
     auto fr = [](void* p) { if (p) cudaFree(p); };
     if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : phase_graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (capture_stream) cudaStreamDestroy(capture_stream);
     fr(emb64); fr(mix); fr(gate_w); fr(gate_b); fr(up_pool); fr(down_pool); fr(head); fr(slot_of);
     fr(seq_sum); fr(seq_len); fr(drafts); fr(vam); fr(row_seq); fr(row_extra); fr(row_plen); fr(x); fr(xa);
     fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);

@@ -374,6 +374,8 @@ public:
         double dense_bytes;
     };
     std::map<uint64_t, PhaseGraph> phase_graphs;
+    uint64_t last_phase_key = ~0ull;
+    cudaStream_t capture_stream = nullptr;  // phase graphs are recorded here while the engine stream runs
     double alg_expert_bytes = 0, alg_dense_bytes = 0;
 
     // ---- store (offload)

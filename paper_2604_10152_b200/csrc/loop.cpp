@@ -410,38 +410,52 @@ int spec_step(Engine& e, int* accepted_tokens) {
         }
         e.repin_hook = nullptr;
     };
-    if (graphable) {
-        const uint64_t key = ((uint64_t)na << 32) | ((uint64_t)g << 20) | ((uint64_t)e.cur_n_draft << 4) |
-                             (uint64_t)(S.c.use_affinity != 0);
-        auto it = e.phase_graphs.find(key);
-        if (it == e.phase_graphs.end()) {
-            const uint64_t l0 = e.launches;
-            const double b0 = e.alg_dense_bytes;
-            SMOE_CUDA(cudaStreamBeginCapture(e.stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                phase_device();
-            } catch (...) {
-                cudaGraph_t gr;
-                cudaStreamEndCapture(e.stream, &gr);
-                if (gr) cudaGraphDestroy(gr);
-                throw;
-            }
-            cudaGraph_t gr = nullptr;
-            SMOE_CUDA(cudaStreamEndCapture(e.stream, &gr));
-            cudaGraphExec_t ex = nullptr;
-            SMOE_CUDA(cudaGraphInstantiate(&ex, gr, 0));
-            SMOE_CUDA(cudaGraphDestroy(gr));
-            Engine::PhaseGraph pg{ex, e.launches - l0, e.alg_dense_bytes - b0};
-            e.launches = l0;
-            e.alg_dense_bytes = b0;
-            it = e.phase_graphs.emplace(key, pg).first;
-        }
-        SMOE_CUDA(cudaGraphLaunch(it->second.exec, e.stream));
-        e.launches += it->second.launches;
-        e.alg_dense_bytes += it->second.dense_bytes;
+    const uint64_t gkey = ((uint64_t)na << 32) | ((uint64_t)g << 20) | ((uint64_t)e.cur_n_draft << 4) |
+                          (uint64_t)(S.c.use_affinity != 0);
+    // capture on the second consecutive phase with the same key: a capture + instantiate costs tens of ms,
+    // which only the steady state (the active count unchanged for many phases) repays -- not the tail of a
+    // run, where sequences finish and the row count changes from phase to phase
+    const bool repeat = gkey == e.last_phase_key;
+    e.last_phase_key = gkey;
+    // the graph is captured on a side stream while the GPU runs this phase's direct launches (capture +
+    // instantiate of ~660 launches costs ~60 ms of host time, which the phase's device time hides)
+    auto gi = graphable ? e.phase_graphs.find(gkey) : e.phase_graphs.end();
+    const bool have_graph = graphable && gi != e.phase_graphs.end();
+    const bool capture_after = graphable && !have_graph && repeat;
+    if (have_graph) {
+        SMOE_CUDA(cudaGraphLaunch(gi->second.exec, e.stream));
+        e.launches += gi->second.launches;
+        e.alg_dense_bytes += gi->second.dense_bytes;
     } else {
         phase_device();
     }
+    auto capture_phase = [&]() {
+        if (!e.capture_stream) SMOE_CUDA(cudaStreamCreateWithFlags(&e.capture_stream, cudaStreamNonBlocking));
+        const uint64_t l0 = e.launches;
+        const double b0 = e.alg_dense_bytes;
+        cudaStream_t live = e.stream;
+        e.stream = e.capture_stream;
+        cudaGraph_t gr = nullptr;
+        SMOE_CUDA(cudaStreamBeginCapture(e.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            phase_device();
+        } catch (...) {
+            cudaStreamEndCapture(e.stream, &gr);
+            if (gr) cudaGraphDestroy(gr);
+            e.stream = live;
+            e.launches = l0;
+            e.alg_dense_bytes = b0;
+            throw;
+        }
+        e.stream = live;
+        SMOE_CUDA(cudaStreamEndCapture(e.capture_stream, &gr));
+        cudaGraphExec_t ex = nullptr;
+        SMOE_CUDA(cudaGraphInstantiate(&ex, gr, 0));
+        SMOE_CUDA(cudaGraphDestroy(gr));
+        e.phase_graphs.emplace(gkey, Engine::PhaseGraph{ex, e.launches - l0, e.alg_dense_bytes - b0});
+        e.launches = l0;
+        e.alg_dense_bytes = b0;
+    };
     // (c) accept: greedy (specdec.cpp:76-78) or Leviathan acceptance with the residual resample
     // (specdec.cpp:104-157) over a pool of na*(g+1) uniforms; the stream then advances by what was used
     std::mt19937_64 srng_before;
@@ -474,6 +488,11 @@ int spec_step(Engine& e, int* accepted_tokens) {
     read_log_async(e.raw_log, g, TV, S.vraw);
     std::vector<std::vector<int>> dfin(g);
     for (int t = 0; t < g; ++t) read_log_async(e.fin_log, t, na, dfin[t]);
+    if (capture_after) {
+        const double c0 = g_host_prof ? host_now() : 0.0;
+        capture_phase();
+        if (g_host_prof) fprintf(stderr, "smoe host: phase graph captured (rows %d): %.3f ms\n", na, (host_now() - c0) * 1e3);
+    }
     if (g_host_prof) hp2 = host_now();
     {
         NvtxRange nv("smoe device wait");
