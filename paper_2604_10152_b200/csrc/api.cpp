@@ -296,6 +296,7 @@ smoe::Engine& engine_for(const ModelWeights& w, int batch, int gamma, const Affi
             e.affinity.clear();
             for (const auto& d : aff->dist) e.affinity.insert(e.affinity.end(), d.begin(), d.end());
             e.have_affinity = true;
+            ++e.affinity_gen;
             slot.aff_ptr = aff;
             slot.aff_fp = afp;
         }

@@ -146,6 +146,7 @@ int smoe_set_affinity(smoe_engine* h, const double* dist) {
         auto& e = *h->e;
         e.affinity.assign(dist, dist + (size_t)e.M * e.E * e.E);
         e.have_affinity = true;
+        ++e.affinity_gen;
     });
 }
 int smoe_build_affinity_device(smoe_engine* h) { return guarded([&] { h->e->build_affinity_device(); }); }

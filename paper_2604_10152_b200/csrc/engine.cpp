@@ -293,7 +293,7 @@ Engine::~Engine() {
     fr(raw_log); fr(fin_log); fr(wgt); fr(pos); fr(group_slot); fr(grp_cnt); fr(xperm); fr(hbuf); fr(ybuf); fr(pmix);
     for (void* q : ep_ipc_opened) cudaIpcCloseMemHandle(q);
     fr(xrecv); fr(ysend); fr(yret); fr(rcnt); fr(ep_gslot); fr(ep_logs); fr(amax_loc); fr(logits_loc);
-    fr(ep_flags); fr(ep_peer);
+    fr(ep_flags); fr(ep_peer); fr(aff_dev);
     fr(ep_cntg); fr(wqkv); fr(wo); fr(pqkv); fr(qbuf); fr(attn_o); fr(kv); fr(ptab); fr(last_tok); fr(row_pos); fr(rope);
     fr(pre_tok); fr(pre_pos); fr(samp_u); fr(samp_q); fr(samp_stats); fr(samp_ratio); fr(samp_i);
     fr(logits); fr(amax); fr(in_draft); fr(draft_sorted); fr(rank); fr(acc); fr(corr); fr(commit_toks);
@@ -573,6 +573,7 @@ void Engine::init_exact() {
     ps.fill(buf, (size_t)d * V, sd);
     upload_tensor("head", -1, -1, buf.data(), (long long)buf.size());
     have_affinity = true;
+    ++affinity_gen;
 }
 
 void Engine::init_device(uint64_t s) {
@@ -700,6 +701,7 @@ void Engine::build_affinity_device() {
     if (tmp_down) SMOE_CUDA(cudaFree(tmp_down));
     if (offload) h2d_bytes = 0;
     have_affinity = true;
+    ++affinity_gen;
 }
 
 // ------------------------------------------------------------------ draft tables
@@ -722,36 +724,34 @@ void Engine::set_draft_sets(const std::vector<std::vector<int>>& sets, int n_dra
     }
     (void)n_draft;
     std::vector<uint8_t> ind((size_t)M * E, 0);
-    std::vector<int> sorted((size_t)M * E, -1), rk((size_t)M * E * nmax, -1);
+    std::vector<int> sorted((size_t)M * E, -1);
     for (int m = 0; m < M; ++m) {
         std::vector<int> srt(sets[m]);
         std::sort(srt.begin(), srt.end());
         for (size_t i = 0; i < srt.size(); ++i) {
-            if (srt[i] < 0 || srt[i] >= E) throw Error(kInvariant, "forward: draft expert out of range");
             ind[(size_t)m * E + srt[i]] = 1;
             sorted[(size_t)m * E + i] = srt[i];
         }
-        for (int r = 0; r < E; ++r) {
-            std::vector<int> o(srt);
-            if (have_affinity) {
-                const double* D = affinity.data() + (size_t)m * E * E + (size_t)r * E;
-                std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
-                    if (D[a] != D[b]) return D[a] < D[b];
-                    return a < b;
-                });
-            }
-            std::copy(o.begin(), o.end(), rk.begin() + ((size_t)m * E + r) * nmax);
-        }
+    }
+    // the per-(layer, raw expert) orders are built on the device from a resident copy of the affinity
+    if (have_affinity && aff_dev_gen != affinity_gen) {
+        if (!aff_dev) aff_dev = dalloc<double>((size_t)M * E * E);
+        if (affinity.size() != (size_t)M * E * E) throw Error(kInvariant, "affinity table shape does not match the model");
+        SMOE_CUDA(cudaMemcpyAsync(aff_dev, affinity.data(), affinity.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                  stream));
+        sync();
+        aff_dev_gen = affinity_gen;
     }
     if (async) {
         upload_async(in_draft, ind.data(), ind.size());
         upload_async(draft_sorted, sorted.data(), sorted.size() * sizeof(int));
-        upload_async(rank, rk.data(), rk.size() * sizeof(int));
     } else {
         h2d(in_draft, ind.data(), ind.size());
         upload_ints(draft_sorted, sorted.data(), sorted.size());
-        upload_ints(rank, rk.data(), rk.size());
     }
+    launch_rank_tables(have_affinity ? aff_dev : nullptr, draft_sorted, M, E, nmax, rank, stream);
+    SMOE_CUDA(cudaGetLastError());
+    ++launches;
     cur_n_draft = nmax;
 }
 

@@ -163,6 +163,9 @@ public:
     std::vector<int> dense_slot;  // raw layer -> slot in pools (dense layers)
     std::vector<double> affinity;  // [M][E][E]
     bool have_affinity = false;
+    uint64_t affinity_gen = 0;    // bumped whenever `affinity` is rebuilt or replaced
+    double* aff_dev = nullptr;    // [M][E][E] device copy for the rank-table kernel
+    uint64_t aff_dev_gen = ~0ull;
 
     // ---- expert store (offload mode, store.cpp): pinned host pools, HBM slot pool
     // offload 1: pinned host DRAM pools.  offload 2 (SSD tier): one file on local storage holding every

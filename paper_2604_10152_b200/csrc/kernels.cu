@@ -782,6 +782,45 @@ void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, lo
         k_pair_sqdist<__nv_bfloat16><<<grid, 512, 0, s>>>((const __nv_bfloat16*)pool, slot_stride, n, slots, E, out);
 }
 
+// Draft rank tables (engine.cpp set_draft_sets): thread (m, r) orders layer m's draft members by
+// (affinity distance to raw expert r, index) -- a stable insertion sort of the ascending member list,
+// the same total order the host's stable_sort used (drafting.cpp:123-138 nearest_draft_expert).
+__global__ void k_rank_tables(const double* __restrict__ aff, const int* __restrict__ sorted, int M, int E, int nmax,
+                              int* __restrict__ rank) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M * E) return;
+    const int m = i / E;
+    const int* srt = sorted + (size_t)m * E;
+    const double* D = aff ? aff + (size_t)i * E : nullptr;
+    int* o = rank + (size_t)i * nmax;
+    int n = 0;
+    for (int j = 0; j < nmax; ++j) {
+        const int v = srt[j];
+        if (v < 0) {
+            o[j] = -1;
+            continue;
+        }
+        int q = n++;
+        if (D) {
+            const double dv = D[v];
+            while (q > 0) {
+                const int u = o[q - 1];
+                const double du = D[u];
+                if (du < dv || (du == dv && u <= v)) break;
+                o[q] = u;
+                --q;
+            }
+        }
+        o[q] = v;
+    }
+}
+
+void launch_rank_tables(const double* aff, const int* sorted, int M, int E, int nmax, int* rank, cudaStream_t s) {
+    const int n = M * E;
+    if (n == 0 || nmax == 0) return;
+    k_rank_tables<<<(n + 127) / 128, 128, 0, s>>>(aff, sorted, M, E, nmax, rank);
+}
+
 }  // namespace smoe
 
 extern "C" int smoe_rk_trace_dump(const char* path) {

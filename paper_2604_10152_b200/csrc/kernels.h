@@ -137,6 +137,8 @@ void launch_cast_f64_to_f32(const double* src, long long n, float* dst, cudaStre
 
 // Pairwise L2 distance of expert weights (drafting.cpp:28-57) accumulated in float64:
 // out[i*E+j] += sum_k (a_i[k]-a_j[k])^2 over one matrix pool region, for all i<j.
+// draft members of each (layer, raw expert) ordered by (affinity distance, index); aff null = index order
+void launch_rank_tables(const double* aff, const int* sorted, int M, int E, int nmax, int* rank, cudaStream_t s);
 void launch_pairwise_sqdist(const void* pool, WType t, long long slot_stride, long long n, const int* slots, int E,
                             double* out, cudaStream_t s);
 

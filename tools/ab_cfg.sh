@@ -14,7 +14,7 @@ d = json.loads(open("gpurun_out/ab.json").read().strip().splitlines()[-1])
 bp = d["roofline"]["by_pass"]
 print(f"{sys.argv[1]:<34} {sys.argv[2]:<40} tok/s {d['value']:8.1f} ms {d['ms_per_step']:7.2f} tau {d['tau']:.3f} "
       f"draft {bp['draft']['hbm_frac']:.3f} verify {bp['verify']['hbm_frac']:.3f}/{bp['verify']['tensor_frac']:.3f} "
-      f"mhz {(d.get('clocks') or {}).get('sm_mhz')}", flush=True)
+      f"e2e {(d.get('e2e') or {}).get('value')} mhz {(d.get('clocks') or {}).get('sm_mhz')}", flush=True)
 PY
   done
 done
