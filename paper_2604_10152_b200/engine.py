@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -60,6 +61,9 @@ class RunConfig(C.Structure):
 
 class LedgerEntry(C.Structure):
     _fields_ = [("phase", C.c_int), ("step", C.c_int), ("layer", C.c_int), ("expert", C.c_int), ("bytes", C.c_uint64)]
+
+
+LEDGER_DTYPE = np.dtype(LedgerEntry)
 
 
 class Outcome(C.Structure):
@@ -212,10 +216,46 @@ class RunCfg:
                          {"greedy": 0, "sampling": 1}[self.mode], self.temperature)
 
 
+class Ledger(Sequence):
+    """The run's expert-residency ledger (ledger.hpp LedgerEntry list): (phase, step, layer, expert, bytes)
+    tuples, built on access from one copied record array (a B=32 run of 128 tokens per sequence carries
+    ~10^5 entries; turning them all into Python tuples up front cost ~20 ms of the run's wall time)."""
+
+    def __init__(self, rec=None):
+        self._rec = rec if rec is not None else np.zeros(0, dtype=LEDGER_DTYPE)
+        self._list = None
+
+    def _tuples(self) -> list:
+        if self._list is None:
+            lv = self._rec
+            self._list = list(zip([PHASES[x] for x in lv["phase"].tolist()], lv["step"].tolist(),
+                                  lv["layer"].tolist(), lv["expert"].tolist(), lv["bytes"].tolist()))
+        return self._list
+
+    def __len__(self) -> int:
+        return len(self._rec)
+
+    def __getitem__(self, i):
+        return self._tuples()[i]
+
+    def __iter__(self):
+        return iter(self._tuples())
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, Ledger):
+            return len(self) == len(other) and bool(np.array_equal(self._rec, other._rec))
+        if isinstance(other, (list, tuple)):
+            return self._tuples() == list(other)
+        return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"Ledger({self._tuples()!r})"
+
+
 @dataclass
 class RunResult:
     tokens: list
-    ledger: list = field(default_factory=list)
+    ledger: Ledger = field(default_factory=Ledger)
     outcomes: list = field(default_factory=list)
     trace: list = field(default_factory=list)
     hotness: np.ndarray | None = None
@@ -238,12 +278,7 @@ def _collect(rp) -> RunResult:
         ntok = _view(r.n_tokens, r.B)
         tok = _view(r.tokens, r.B * r.max_new, (r.B, r.max_new)) if r.B * r.max_new else None
         toks = [tok[b, :ntok[b]].tolist() if tok is not None else [] for b in range(r.B)]
-        lv = _view(r.ledger, r.n_ledger)
-        if r.n_ledger:
-            led = list(zip([PHASES[x] for x in lv["phase"].tolist()], lv["step"].tolist(), lv["layer"].tolist(),
-                           lv["expert"].tolist(), lv["bytes"].tolist()))
-        else:
-            led = []
+        led = Ledger(_view(r.ledger, r.n_ledger).copy() if r.n_ledger else None)
         g = r.gamma
         ov = _view(r.outcomes, r.n_outcomes)
         if r.n_outcomes:
