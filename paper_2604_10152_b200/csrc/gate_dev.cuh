@@ -25,26 +25,35 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
         if (l0 < E) p[l0] = expf(g0 - mx);
         if (l1 < E) p[l1] = expf(g1 - mx);
         __syncwarp();
+        // the sum in expert order on lane 0, its loads issued ahead of the dependent adds
         float sum = 0.f;
-        if (lane == 0)
-            for (int e = 0; e < E; ++e) sum += p[e];
+        if (lane == 0) {
+            int e = 0;
+            for (; e + 8 <= E; e += 8) {
+                float q[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q[j] = p[e + j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sum += q[j];
+            }
+            for (; e < E; ++e) sum += p[e];
+        }
         sum = __shfl_sync(FULL, sum, 0);
-        // top-K: K rounds of a warp argmax, ties -> lower index == repeated first-max (model.cpp:159-170)
-        unsigned long long taken = 0ull, chosen = 0ull;
+        // top-K (model.cpp:159-170: K rounds of first-max, ties -> lower index) as ranks: expert e is pick
+        // rank(e) = #{e' : g[e'] > g[e] or (g[e'] == g[e] and e' < e)} -- the same order, found with one
+        // pass of independent compares instead of K dependent warp reductions.  (Non-finite logits have
+        // raised the flag above, which fails the pass; their picks only need to be in range.)
+        int r0 = 0, r1 = 0;
+        for (int e = 0; e < E; ++e) {
+            const float ge = gl[e];
+            r0 += (ge > g0) | ((ge == g0) & (e < l0));
+            r1 += (ge > g1) | ((ge == g1) & (e < l1));
+        }
+        unsigned long long chosen = 0ull;
         int my_pick = 0, my_ex = 0;  // lane k keeps pick k
         for (int k = 0; k < K; ++k) {
-            float v = 0.f;
-            int idx = -1;
-            if (l0 < E && !((taken >> l0) & 1ull)) { v = g0; idx = l0; }
-            if (l1 < E && !((taken >> l1) & 1ull) && (idx < 0 || g1 > v)) { v = g1; idx = l1; }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const float ov = __shfl_xor_sync(FULL, v, o);
-                const int oi = __shfl_xor_sync(FULL, idx, o);
-                if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
-            }
-            const int pick = idx;
-            taken |= 1ull << pick;
+            const unsigned b0 = __ballot_sync(FULL, l0 < E && r0 == k), b1 = __ballot_sync(FULL, l1 < E && r1 == k);
+            const int pick = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : k);
             int ex = pick;
             if (a.in_draft && !(a.in_draft[pick] && !((chosen >> pick) & 1ull))) {
                 // restricted (draft) semantics: remap into draft \ chosen (drafting.cpp:123-151)

@@ -427,6 +427,148 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     RK_END(1);
 }
 
+// ---- K4/K5 gate, row-group form for many experts (C4: E=64, 512 KB of f32 gate weights).  k_gate reads
+// all E x d weights once per row (from L2: one SM pulls 512 KB per row, the GEMV's bound); here a
+// cluster of kGateRG CTAs takes kGateRG rows and CTA c owns row c (residual + rms, selection,
+// dispatch) and experts [c*E/kGateRG, (c+1)*E/kGateRG) of every row of the cluster, so the weights
+// are read once per cluster.  Every reduction is k_gate's: the row tree over VB virtual threads (each
+// of the RT real threads plays VB/RT of them) and, per (row, expert), the lane-strided float4 chain +
+// butterfly -- a row's logits and picks are bit-identical to k_gate's.
+constexpr int kGateRG = 8;
+
+template <typename OT>
+__global__ void __launch_bounds__(512, 1) k_gate_rg(GateArgs a) {
+    RK_IN();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ float4 sm4[];
+    __shared__ uint64_t gw_bar;
+    __shared__ float red[33];
+    __shared__ int dst[16];
+    const int d = a.d, d4 = d >> 2, E = a.E, K = a.K, Ec = E / kGateRG;
+    const int c = (int)cl.block_rank();
+    const int row0 = (int)(blockIdx.x / kGateRG) * kGateRG;
+    const int nrows = min(kGateRG, a.T - row0);
+    const int r = row0 + c;
+    float4* gw4 = sm4;                                               // [Ec][d4] when staged
+    float4* xall = gw4 + (a.stage_gw ? (size_t)Ec * d4 : 0);         // [kGateRG][d4] the cluster's rows
+    float* gl = reinterpret_cast<float*>(xall + (size_t)kGateRG * d4);  // [2E] own row's logits + scratch
+    int* s_rank = reinterpret_cast<int*>(gl + 2 * E);
+    int* s_sorted = s_rank + E * a.N;
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_sorted + a.N);
+    if (a.stage_gw && threadIdx.x == 0) {  // this CTA's expert rows: independent of the Mix, fetched now
+        tc::mbar_init(&gw_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t bytes = (uint32_t)Ec * d * 4;
+        tc::mbar_expect_tx(&gw_bar, bytes);
+        const char* src = reinterpret_cast<const char*>(a.gate_w + (size_t)c * Ec * d);
+        for (uint32_t off = 0; off < bytes; off += 32768)
+            tc::bulk_g2s(reinterpret_cast<char*>(gw4) + off, src + off, min(32768u, bytes - off), &gw_bar);
+    }
+    cl.sync();  // every CTA of the cluster is running before any writes into its shared memory
+    pdl_wait();
+    pdl_trigger();
+    RK_WAITED();
+    if (a.in_draft) {
+        for (int i = threadIdx.x; i < E * a.N; i += blockDim.x) s_rank[i] = a.rank[i];
+        for (int i = threadIdx.x; i < a.N; i += blockDim.x) s_sorted[i] = a.draft_sorted[i];
+        for (int i = threadIdx.x; i < E; i += blockDim.x) s_in[i] = a.in_draft[i];
+    }
+    const int VB = gate_threads(d, E), RT = blockDim.x, nv = VB / RT;
+    const long long base = (long long)r * d;
+    float4* own = xall + (size_t)c * d4;
+    if (c < nrows) {
+        // residual add of the mix partials + rms (k_gate's tree: virtual thread vt = t + j*RT)
+#pragma unroll 1
+        for (int j = 0; j < nv; ++j) {
+            float ss = 0.f;
+            for (int i = (int)threadIdx.x + j * RT; i < d4; i += VB) {
+                float4 v = ld4(a.x + base + 4ll * i);
+                add4(v, sum_splits<8>(a.pmix, a.pstride, a.s_mix, base + 4ll * i));
+                *reinterpret_cast<float4*>(a.x + base + 4ll * i) = v;
+                own[i] = v;
+                ss = __fadd_rn(ss, sumsq4(v));
+            }
+            ss = warp_sum(ss);
+            if ((threadIdx.x & 31) == 0) red[((int)threadIdx.x + j * RT) >> 5] = ss;
+        }
+        __syncthreads();
+        const float inv = 1.0f / sqrtf(vblock_total(VB >> 5, red) / (float)d + 1e-12f);
+        RK_MARK(0);
+        // the normalised row into slot c of every CTA of the cluster (each computes its experts for all rows)
+#pragma unroll 1
+        for (int i = threadIdx.x; i < d4; i += RT) {
+            const float4 v = own[i];
+            const float4 xn = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+#pragma unroll
+            for (int q = 0; q < kGateRG; ++q) cl.map_shared_rank(xall, q)[(size_t)c * d4 + i] = xn;
+        }
+    }
+    cl.sync();
+    // GEMV: warp w takes expert c*Ec + w % Ec for rows w / Ec, + rstep, ... four rows per weight load
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = RT >> 5;
+    const int rstep = max(1, nw / Ec);
+    if (a.stage_gw) tc::mbar_wait(&gw_bar, 0);
+#pragma unroll 1
+    for (int task = w; task < Ec * rstep; task += nw) {
+        const int el = task % Ec, e = c * Ec + el;
+        const float4* g = a.stage_gw ? gw4 + (size_t)el * d4 : reinterpret_cast<const float4*>(a.gate_w + (size_t)e * d);
+#pragma unroll 1
+        for (int qb = task / Ec; qb < nrows; qb += 4 * rstep) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const float4* x0 = xall + (size_t)qb * d4;
+            const int nq = min(4, (nrows - qb + rstep - 1) / rstep);
+            if (nq == 4) {
+#pragma unroll 4
+                for (int i = lane; i < d4; i += 32) {
+                    const float4 gv = g[i];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], dot4f(gv, x0[(size_t)k * rstep * d4 + i]));
+                }
+            } else {
+                for (int i = lane; i < d4; i += 32) {
+                    const float4 gv = g[i];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k < nq) acc[k] = __fadd_rn(acc[k], dot4f(gv, x0[(size_t)k * rstep * d4 + i]));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float v = warp_sum(acc[k]);
+                if (k < nq && lane == 0) cl.map_shared_rank(gl, qb + k * rstep)[e] = v + a.gate_b[e];
+            }
+        }
+    }
+    cl.sync();
+    RK_MARK(1);
+    if (c >= nrows) return;
+    if (threadIdx.x < 32) {
+        GateArgs sa = a;
+        if (a.in_draft) {
+            sa.rank = s_rank;
+            sa.draft_sorted = s_sorted;
+            sa.in_draft = s_in;
+        }
+        gate_select_warp(sa, r, gl, dst);
+    }
+    __syncthreads();
+    RK_MARK(2);
+    const int sg = a.seg > 0 ? a.seg : a.T;
+    for (int k = 0; k < K; ++k) {
+        void* obase = a.xperm;
+        long long row = dst[k];
+        if (a.peer_x) {  // fused EP dispatch over peer memory (as k_gate)
+            const int e = (int)(row / sg);
+            obase = a.peer_x[e / a.ep_eo];
+            row = (long long)(a.ep_me * a.ep_eo + e % a.ep_eo) * sg + (row - (long long)e * sg);
+        }
+        store_row4<OT>(obase, row * d, own, d4, 1.0f);
+    }
+    if (a.peer_x) __threadfence_system();
+    RK_END(1);
+}
+
 // ------------------------------------------------------------------ K9 combine (+ next rms)
 template <typename OT>
 __global__ void __launch_bounds__(1024) k_combine_rms(float* __restrict__ x, const float* __restrict__ P, int S, long long pstride,
@@ -679,6 +821,31 @@ void launch_rms(const float* x, int T, int d, void* xa, WType op, cudaStream_t s
 void launch_gate(const GateArgs& a0, cudaStream_t s) {
     if (a0.T <= 0) return;
     GateArgs a = a0;
+    static const int rg_env = [] {  // SMOE_GATE_RG: 0 off, 1 many-expert gates (default), 2 every gate
+        const char* v = std::getenv("SMOE_GATE_RG");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (rg_env && (a.E > 16 || rg_env == 2) && a.E % kGateRG == 0 && a.E <= 64 && a.K <= 16 && a.d % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(a.gate_w) & 15) == 0) {
+        const int clusters = (a.T + kGateRG - 1) / kGateRG;
+        // staged expert rows hold one CTA per SM: only when the pass's CTAs fit in one wave; otherwise
+        // 256-thread CTAs, two per SM, read their expert rows from L2
+        a.stage_gw = clusters * kGateRG <= tc::sm_count() ? 1 : 0;
+        const int vb = gate_threads(a.d, a.E), rt = std::min(a.stage_gw ? 512 : 256, vb);
+        const size_t smem = sizeof(float4) * ((size_t)(a.stage_gw ? a.E / kGateRG : 0) + kGateRG) * (a.d / 4) +
+                            sizeof(float) * 2 * a.E + (a.in_draft ? sizeof(int) * ((size_t)a.E * a.N + a.N) + a.E : 0);
+        static std::atomic<uint64_t> configured_rg{0};
+        if (first_use_on_device(configured_rg)) {
+            SMOE_CUDA(cudaFuncSetAttribute(k_gate_rg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            SMOE_CUDA(cudaFuncSetAttribute(k_gate_rg<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        }
+        if (smem <= 200 * 1024 && vb % rt == 0) {
+            if (a.op == kF32) launch_kc(k_gate_rg<float>, clusters * kGateRG, rt, smem, s, kGateRG, a);
+            else launch_kc(k_gate_rg<__nv_bfloat16>, clusters * kGateRG, rt, smem, s, kGateRG, a);
+            return;
+        }
+        a.stage_gw = 0;
+    }
     static const bool stage_env = [] {
         const char* v = std::getenv("SMOE_GATE_STAGE");
         return !(v && v[0] == '0');

@@ -56,10 +56,17 @@ def row_kernel_launches(path):
     rec = np.frombuffer(raw[4:4 + n * 56], dtype=np.dtype(
         [("kid", np.int32), ("blk", np.int32), ("t_in", np.int64), ("t_wait", np.int64), ("t_end", np.int64),
          ("t_m", np.int64, (3,))]))
-    g = rec[rec["kid"] == 1]
-    if len(g):  # gate anatomy per block (us after its wait released): rms done, GEMV done, selected, end
+    ga = np.sort(rec[rec["kid"] == 1], order="t_in")
+    gl = np.split(ga, np.nonzero(np.diff(ga["t_in"]) > 30_000)[0] + 1) if len(ga) else []
+    for label, sel in (("draft", [x for x in gl if len(x) <= 128]), ("verify", [x for x in gl if len(x) > 128])):
+        if not sel:
+            continue
+        # gate anatomy per block (us after its wait released): rms done, GEMV done, selected, end
+        g = np.concatenate(sel)
         w = g["t_wait"]
-        print(json.dumps({"gate_block_anatomy_us": {
+        print(json.dumps({"gate_block_anatomy_us": label, "launches": len(sel), "blocks": int(np.median([len(x) for x in sel])),
+            "launch_in_to_last_end": round(float(np.median([(x["t_end"].max() - x["t_in"].min()) / 1e3 for x in sel])), 2),
+            "first_wait_to_last_end": round(float(np.median([(x["t_end"].max() - x["t_wait"].min()) / 1e3 for x in sel])), 2), **{
             "rms_done": round(float(np.median((g["t_m"][:, 0] - w) / 1e3)), 2),
             "gemv_done": round(float(np.median((g["t_m"][:, 1] - w) / 1e3)), 2),
             "selected": round(float(np.median((g["t_m"][:, 2] - w) / 1e3)), 2),
