@@ -8,7 +8,10 @@ namespace smoe {
 
 // Called by ONE full warp for row r.  gl[0..E) = gate logits incl. bias; gl[E..2E) is scratch for
 // the softmax numerators.  Writes raw/fin/wgt/pos of row r and dst[k] = the xperm row of pick k.
-__device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float* gl, int* dst) {
+// The draft tables come as shared-memory copies (in_draft == nullptr: target semantics); `a` stays the
+// kernel parameter (a local copy of GateArgs would turn every field read into a local-memory load).
+__device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float* gl, int* dst, const int* s_rank,
+                                                 const int* s_sorted, const uint8_t* in_draft) {
     const int lane = threadIdx.x & 31, E = a.E, K = a.K;
     {
         const unsigned FULL = 0xffffffffu;
@@ -44,7 +47,18 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
         // pass of independent compares instead of K dependent warp reductions.  (Non-finite logits have
         // raised the flag above, which fails the pass; their picks only need to be in range.)
         int r0 = 0, r1 = 0;
-        for (int e = 0; e < E; ++e) {
+        int e = 0;
+        for (; e + 8 <= E; e += 8) {
+            float q[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) q[j] = gl[e + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                r0 += (q[j] > g0) | ((q[j] == g0) & (e + j < l0));
+                r1 += (q[j] > g1) | ((q[j] == g1) & (e + j < l1));
+            }
+        }
+        for (; e < E; ++e) {
             const float ge = gl[e];
             r0 += (ge > g0) | ((ge == g0) & (e < l0));
             r1 += (ge > g1) | ((ge == g1) & (e < l1));
@@ -55,14 +69,14 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
             const unsigned b0 = __ballot_sync(FULL, l0 < E && r0 == k), b1 = __ballot_sync(FULL, l1 < E && r1 == k);
             const int pick = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : k);
             int ex = pick;
-            if (a.in_draft && !(a.in_draft[pick] && !((chosen >> pick) & 1ull))) {
+            if (in_draft && !(in_draft[pick] && !((chosen >> pick) & 1ull))) {
                 // restricted (draft) semantics: remap into draft \ chosen (drafting.cpp:123-151)
                 ex = -1;
                 if (a.use_affinity) {
                     // nearest by (distance, index) = first rank entry not yet chosen; -1 pads short sets
                     for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
                         const int j = j0 + lane;
-                        const int c = j < a.N ? a.rank[pick * a.N + j] : -1;
+                        const int c = j < a.N ? s_rank[pick * a.N + j] : -1;
                         const unsigned pad = __ballot_sync(FULL, j < a.N && c < 0);
                         const unsigned ok = __ballot_sync(FULL, j < a.N && c >= 0 && !((chosen >> c) & 1ull));
                         const unsigned before_pad = pad ? (1u << (__ffs(pad) - 1)) - 1u : FULL;
@@ -74,7 +88,7 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
                     int total = 0;
                     for (int j0 = 0; j0 < a.N; j0 += 32) {
                         const int j = j0 + lane;
-                        const int c = j < a.N ? a.draft_sorted[j] : -1;
+                        const int c = j < a.N ? s_sorted[j] : -1;
                         total += __popc(__ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull)));
                     }
                     if (total > 0) {
@@ -83,7 +97,7 @@ __device__ __forceinline__ void gate_select_warp(const GateArgs& a, int r, float
                         int want = (int)(h % (uint64_t)total);
                         for (int j0 = 0; j0 < a.N && ex < 0; j0 += 32) {
                             const int j = j0 + lane;
-                            const int c = j < a.N ? a.draft_sorted[j] : -1;
+                            const int c = j < a.N ? s_sorted[j] : -1;
                             unsigned m = __ballot_sync(FULL, c >= 0 && !((chosen >> c) & 1ull));
                             const int n = __popc(m);
                             if (want < n) {

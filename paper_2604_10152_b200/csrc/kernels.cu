@@ -402,13 +402,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
     // ---- selection on warp 0 (E <= 64: lane l holds experts l and l+32)
     __shared__ int dst[16];
     if (threadIdx.x < 32) {
-        GateArgs sa = a;
-        if (a.in_draft) {
-            sa.rank = s_rank;
-            sa.draft_sorted = s_sorted;
-            sa.in_draft = s_in;
-        }
-        gate_select_warp(sa, r, gl, dst);
+        gate_select_warp(a, r, gl, dst, s_rank, s_sorted, a.in_draft ? s_in : nullptr);
     }
     __syncthreads();
     RK_MARK(2);
@@ -505,10 +499,10 @@ __global__ void __launch_bounds__(512, 1) k_gate_rg(GateArgs a) {
         }
     }
     cl.sync();
-    // GEMV: warp w takes expert c*Ec + w % Ec for rows w / Ec, + rstep, ... four rows per weight load
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = RT >> 5;
-    const int rstep = max(1, nw / Ec);
     if (a.stage_gw) tc::mbar_wait(&gw_bar, 0);
+    // GEMV: warp w takes expert c*Ec + w % Ec for rows w / Ec, + rstep, ... four rows per weight load
+    const int rstep = max(1, nw / Ec);
 #pragma unroll 1
     for (int task = w; task < Ec * rstep; task += nw) {
         const int el = task % Ec, e = c * Ec + el;
@@ -544,13 +538,7 @@ __global__ void __launch_bounds__(512, 1) k_gate_rg(GateArgs a) {
     RK_MARK(1);
     if (c >= nrows) return;
     if (threadIdx.x < 32) {
-        GateArgs sa = a;
-        if (a.in_draft) {
-            sa.rank = s_rank;
-            sa.draft_sorted = s_sorted;
-            sa.in_draft = s_in;
-        }
-        gate_select_warp(sa, r, gl, dst);
+        gate_select_warp(a, r, gl, dst, s_rank, s_sorted, a.in_draft ? s_in : nullptr);
     }
     __syncthreads();
     RK_MARK(2);
