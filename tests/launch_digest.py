@@ -20,6 +20,9 @@ SHAPES = {
     # E=64 at d=1024: 1024-thread gate tree (4-CTA clusters), gate weights too large to stage
     "e64_d1024": (ModelSpec(num_layers=3, experts=64, top_k=6, hidden=1024, ffn=512, vocab=512,
                             expert_kind=SWIGLU3, moe_mask=[0, 1, 1], gate_skew=0.5), 8),
+    # E=64 at B=32: verify passes of 160 rows > SMs (row-group gate without staged weights, 256-thread CTAs)
+    "e64_b32": (ModelSpec(num_layers=2, experts=64, top_k=6, hidden=1024, ffn=256, vocab=512,
+                          expert_kind=SWIGLU3, moe_mask=[0, 1], gate_skew=0.5), 8, 32),
     # B=64 verify passes of 320 rows over 4 experts: groups of > 128 tokens (unpaired launches)
     "e4_b64": (ModelSpec(num_layers=2, experts=4, top_k=2, hidden=1024, ffn=512, vocab=512,
                          expert_kind=SWIGLU3, gate_skew=1.0), 2, 64),
