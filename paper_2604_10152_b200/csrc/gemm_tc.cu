@@ -126,13 +126,15 @@ __device__ __forceinline__ int item_tile(const int16_t* items, int i) { return i
 
 // Warp 0 (all lanes), after the dependency wait: the item list and the stage ring of a grouped launch
 // (token space for the largest group's box, every other byte of shared memory for weight stages).
-__device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Plan* plan) {
+// slot_pre[j]: group_slot[j*32 + lane], read before the dependency wait (the slot tables are written by
+// stream-ordered host copies, never by the kernels this launch may overlap under PDL)
+__device__ __forceinline__ void build_plan(const TcParams& p, int16_t* items, Plan* plan, const int* slot_pre) {
     const int lane = threadIdx.x & 31;
     int n = 0, mx = 1;
     for (int g0 = 0; g0 < p.G; g0 += 32) {
         const int g = g0 + lane;
         int cnt = 0;
-        if (g < p.G && p.group_slot[g] >= 0) cnt = p.group_cnt[g];
+        if (g < p.G && slot_pre[g0 >> 5] >= 0) cnt = p.group_cnt[g];
         const int nt = min(p.n_tiles, (cnt + BN_MAX - 1) / BN_MAX);
         mx = max(mx, min(BN_MAX, cnt));
         int incl = nt;  // inclusive prefix of the tile counts over the lanes (groups stay in order)
@@ -340,8 +342,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // grouped launches: the unit geometry (rows per expert) is written by the gate kernel that
         // immediately precedes this one, so it may only be read after the dependency wait
         if (p.pred && threadIdx.x == 0) prefetch_predicted(p, mapA0, mapA1);
+        int slot_pre[kMaxGroups / 32];
+#pragma unroll
+        for (int j = 0; j < kMaxGroups / 32; ++j) {
+            const int g = j * 32 + lane;
+            slot_pre[j] = warp == 0 && g < p.G ? p.group_slot[g] : -1;
+        }
         dep_wait(p);
-        if (warp == 0) build_plan(p, s_items, plan);
+        if (warp == 0) build_plan(p, s_items, plan, slot_pre);
         __syncthreads();
         n_items = plan->n_items;
         pair = plan->pair;
@@ -718,6 +726,8 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
     p.n_tiles = (a.rows_bound + BN_MAX - 1) / BN_MAX;
     if (a.group_cnt && (long long)p.G * p.n_tiles > kMaxItems)
         throw Error(kInvariant, "tcgen05 GEMM: more (group, token tile) items than the plan holds");
+    if (a.group_cnt && p.G > kMaxGroups)
+        throw Error(kInvariant, "tcgen05 GEMM: more groups than the plan's slot preload holds");
 
     constexpr int kCtrl = 1024;  // control block (barriers, unit ring, TMEM slot) + alignment slack below
     static const bool pair_env = [] {
