@@ -83,6 +83,7 @@ struct TcParams {
     const int* pred;
     int n_pred, pf_kb;
     int w_evict_first;         // weight boxes loaded with an L2 evict_first policy
+    int static_first;          // CTA b starts with unit b (SMOE_STATIC_FIRST=0: every unit from the counter)
 };
 
 #ifdef SMOE_TC_TRACE
@@ -381,8 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             int u = 0;
             Unit w;
             if (lane == 0) {
+                // CTA b's first unit is unit b (no atomic round trip before the first TMA); later claims
+                // take units gridDim.x, gridDim.x + 1, ... from the counter
+                bool first = p.static_first && pub == 0 && (int)blockIdx.x < total_units;
                 do {
-                    u = atomicAdd(&p.sched[0], 1);
+                    u = first ? (int)blockIdx.x : (p.static_first ? (int)gridDim.x : 0) + atomicAdd(&p.sched[0], 1);
+                    first = false;
                 } while (u < total_units && !decode_unit(p, items, n_items, u, w, pair));
             }
             u = __shfl_sync(0xffffffffu, u, 0);
@@ -764,6 +769,11 @@ void launch_phases(const TcGemmArgs& a, const TcGemmArgs* b, cudaStream_t s) {
         return v ? atoi(v) : 1;
     }();
     p.w_evict_first = a.group_cnt && wef_env;  // expert weights: streamed once per pass
+    static const int static_first_env = [] {
+        const char* v = getenv("SMOE_STATIC_FIRST");
+        return v ? atoi(v) : 1;
+    }();
+    p.static_first = static_first_env;
 
     static const int pf_kb_env = [] {
         const char* v = getenv("SMOE_PF_KB");

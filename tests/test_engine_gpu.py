@@ -507,7 +507,7 @@ class _env:
 @pytest.mark.parametrize("env", ["SMOE_ROW_CLUSTER=1", "SMOE_ROW_THREADS=256", "SMOE_GATE_STAGE=0",
                                  "SMOE_TC_PAIR=0", "SMOE_TC_PAIR_DOWN=0", "SMOE_TC_PAIR_SINGLE=2",
                                  "SMOE_TILED=0", "SMOE_W_EVICT_FIRST=0", "SMOE_PF_PRED=0", "SMOE_PDL=0",
-                                 "SMOE_ROW_WIDE=0", "SMOE_GRAPH=0", "SMOE_GATE_RG=0", "SMOE_GATE_RG=2"])
+                                 "SMOE_ROW_WIDE=0", "SMOE_GRAPH=0", "SMOE_GATE_RG=0", "SMOE_GATE_RG=2", "SMOE_STATIC_FIRST=0"])
 def test_launch_shape_switches_bitexact(env):
     """Launch-shape switches change how the work is laid out on the GPU (row clusters with DSMEM
     reductions, fewer row threads playing the same reduction tree, gate weights staged in shared
