@@ -435,11 +435,17 @@ def expert_roofline(m: dict, pk: dict) -> dict:
     return out
 
 
+SHARED_DEVICE = False  # set by run_b200: N>1 ranks on fewer GPUs (host-transport test mode)
+
+
 def c2_engine(a, spec, dev, max_batch, max_gamma, rank=0, world=1, ep=False, max_seq_len=0):
     from paper_2604_10152_b200.engine import BF16, Engine
     eng = Engine(spec, weight_type=BF16, max_batch=max_batch, max_gamma=max_gamma, device=dev,
                  ep_rank=rank if ep else 0, ep_world=world if ep else 1, max_seq_len=max_seq_len)
-    if ep:
+    if ep and SHARED_DEVICE:
+        from paper_2604_10152_b200.engine import HostTransport, gloo_allgather
+        eng.attach_host(HostTransport(gloo_allgather()))
+    elif ep:
         eng.attach_nccl(share_nccl_id(rank))
     eng.init_device(0)
     eng.build_affinity_device()
@@ -600,11 +606,16 @@ def section_ssd(a, dev: int, B: int = 64, steps: int = 2) -> dict:
 
 def run_b200(a) -> None:
     import torch
+    global SHARED_DEVICE
     rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
+        # more ranks than visible GPUs (a one-GPU box exercising the N>1 path): ranks share devices, the
+        # engines exchange over the C ABI's host transport (gloo all-gather + CUDA IPC), not NCCL
+        SHARED_DEVICE = torch.cuda.device_count() < world
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if SHARED_DEVICE else "nccl")
     from paper_2604_10152_b200.engine import SWIGLU3, TANH2, ModelSpec, RunCfg
     from paper_2604_10152_b200.prompts import make_prompts
 
@@ -686,6 +697,8 @@ def run_b200(a) -> None:
     ep_mode = os.environ.get("SMOE_EP_MODE", "p2p")
     exch = ("gate/down-projection epilogues store rows into peer memory over NVLink (fused dispatch/combine)"
             if ep_mode != "a2a" else "NCCL all-to-all dispatch/combine")
+    if SHARED_DEVICE:
+        exch += f" (TEST MODE: {world} ranks on {torch.cuda.device_count()} GPU(s), host transport; not a multi-GPU number)"
     line = {
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
