@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(1024) k_gate(GateArgs a) {
         float ss = 0.f;
         for (int i = rc.vt(j); i < d4; i += rc.VB) {
             float4 v = ld4(a.x + base + 4ll * i);
-            add4(v, sum_splits<8>(a.pmix, a.pstride, a.s_mix, base + 4ll * i));
+            add4(v, sum_splits<4>(a.pmix, a.pstride, a.s_mix, base + 4ll * i));
             *reinterpret_cast<float4*>(a.x + base + 4ll * i) = v;
             xf4[i] = v;
             ss = __fadd_rn(ss, sumsq4(v));
